@@ -1,0 +1,134 @@
+/*
+ * hcnn-b200: C ABI of the B200-native RNS-CKKS engine.
+ *
+ * Drop-in boundary for the hot path of the reference package `hcnn`
+ * (/root/reference/pkg/src/hcnn).  The reference has no FFI: its seams are
+ * the kernel function table of kernels.py:339-371 (per-row modular kernels)
+ * and the ckks.* object API of ckks.py.  Every entry point below
+ * replaces one of those, over DEVICE pointers to residues laid out exactly
+ * like RnsPoly.coeffs (uint64 [nlimbs][N], limb-major, ring.py:204-213).
+ *
+ * Conventions
+ *  - Plain C types only; device buffers are passed as uint64_t*, streams as
+ *    void* (a cudaStream_t; NULL = legacy default stream).
+ *  - A "basis" is (nq, np): limbs 0..nq-1 over q_0..q_{nq-1}, then np limbs
+ *    over the special primes p_0..p_{np-1} (ckks.py:139-145 mods_at/ext_mods).
+ *  - A batch of `npolys` polynomials over one basis is contiguous:
+ *    poly z starts at base + z*(nq+np)*N.  A ciphertext is a batch of 2
+ *    (c0 then c1), always in the evaluation domain (ckks.py:215-218).
+ *  - Switch keys are two device arrays (rows_b, rows_a) of shape
+ *    [dnum][Lq+K][N] in Montgomery form, as SwitchKey holds them
+ *    (ckks.py:315-324, 392-393).
+ *  - All results are canonical residues in [0,q): bit-exact with the
+ *    reference for every integer operation.
+ *  - Return value: HCNN_OK or an hcnn_status; hcnn_last_error() gives text.
+ *    Codes map 1:1 onto the reference's exception taxonomy (errors.py:8-53).
+ *  - Calls are asynchronous on `stream`; a context is reentrant across
+ *    streams except for the lazily built conversion tables, which are
+ *    created under a lock.
+ */
+#ifndef HCNN_B200_H
+#define HCNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hcnn_ctx hcnn_ctx;
+
+typedef enum hcnn_status {
+  HCNN_OK = 0,
+  HCNN_E_PARAMETER = 1, /* ParameterError  errors.py:12 */
+  HCNN_E_DOMAIN = 2,    /* DomainError     errors.py:16 */
+  HCNN_E_BASIS = 3,     /* BasisError      errors.py:20 */
+  HCNN_E_LEVEL = 4,     /* LevelError      errors.py:24 */
+  HCNN_E_SCALE = 5,     /* ScaleError      errors.py:28 */
+  HCNN_E_KEY = 6,       /* KeyError_       errors.py:32 */
+  HCNN_E_CUDA = 100,    /* CUDA runtime failure */
+  HCNN_E_NOMEM = 101
+} hcnn_status;
+
+const char* hcnn_last_error(void);
+int hcnn_abi_version(void);
+
+/* ---- context: CkksParams on the device (ckks.py:65-161, ring.py:32-72,
+ *      ring.py:141-197 twiddles from the reference's psi) ------------------ */
+int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_moduli, uint32_t n_q,
+                    const uint64_t* p_moduli, uint32_t n_p);
+void hcnn_ctx_destroy(hcnn_ctx* ctx);
+/* psi chosen for modulus index i (q's then p's): TwiddleTable.psi ring.py:141-157 */
+int hcnn_ctx_psi(const hcnn_ctx* ctx, uint32_t mod_index, uint64_t* psi);
+
+/* ---- ring.py / kernels.py row-level ops over a batch --------------------- */
+/* ntt_forward ring.py:317-325 (kernels.ntt_inplace kernels.py:232-253) */
+int hcnn_ntt_forward(hcnn_ctx* ctx, uint64_t* data, uint32_t nq, uint32_t np, uint32_t npolys, void* stream);
+/* ntt_inverse ring.py:328-336 (kernels.intt_inplace kernels.py:255-281) */
+int hcnn_ntt_inverse(hcnn_ctx* ctx, uint64_t* data, uint32_t nq, uint32_t np, uint32_t npolys, void* stream);
+/* poly_add / poly_sub / poly_neg ring.py:264-284 (kernels.addmod/submod/negmod kernels.py:208-230).
+ * b_broadcast != 0: b is a single poly applied to every poly of a. */
+int hcnn_poly_add(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
+                  uint32_t npolys, int b_broadcast, void* stream);
+int hcnn_poly_sub(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
+                  uint32_t npolys, int b_broadcast, void* stream);
+int hcnn_poly_neg(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, uint32_t nq, uint32_t np, uint32_t npolys,
+                  void* stream);
+/* poly_mul_pointwise ring.py:287-296: both operands ordinary residues */
+int hcnn_poly_mul(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
+                  uint32_t npolys, int b_broadcast, void* stream);
+/* poly_mul_mont_rows ring.py:307-314, pmult_mont ckks.py:499-503
+ * (kernels.mulmod_mont kernels.py:190-193): b in Montgomery form */
+int hcnn_poly_mul_mont(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b_mont, uint32_t nq,
+                       uint32_t np, uint32_t npolys, int b_broadcast, void* stream);
+/* kernels.muladd_mont kernels.py:200-206: out += a * b_mont */
+int hcnn_poly_mac_mont(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b_mont, uint32_t nq,
+                       uint32_t np, uint32_t npolys, int b_broadcast, void* stream);
+/* to_mont_rows ring.py:299-304 / its inverse */
+int hcnn_to_mont(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, uint32_t nq, uint32_t np, uint32_t npolys,
+                 void* stream);
+int hcnn_from_mont(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, uint32_t nq, uint32_t np, uint32_t npolys,
+                   void* stream);
+/* _scalar_mul_rows ckks.py:350-356: limb i times consts[i] (host array, any value, reduced here) */
+int hcnn_scalar_mul(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* consts, uint32_t nq,
+                    uint32_t np, uint32_t npolys, void* stream);
+/* signed int64 coefficient rows [npolys][N] (device) -> residues in every limb:
+ * sample_poly replication ring.py:463-467, encode reduction ckks.py:284-288 */
+int hcnn_from_signed(hcnn_ctx* ctx, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np, uint32_t npolys,
+                     void* stream);
+/* automorphism X -> X^g.  eval_domain=0: ring.automorphism ring.py:427-439
+ * (coefficient domain, signed permutation); eval_domain=1: the equivalent
+ * index permutation of the bit-reversed NTT output. */
+int hcnn_automorphism(hcnn_ctx* ctx, uint64_t* out, const uint64_t* in, uint64_t g, int eval_domain, uint32_t nq,
+                      uint32_t np, uint32_t npolys, void* stream);
+/* base_convert ring.py:378-398 (centred FBC, kernels.fbc_row kernels.py:283-301).
+ * Source/target limbs are given as modulus indices (q's 0..Lq-1, p's Lq..). */
+int hcnn_base_convert(hcnn_ctx* ctx, uint64_t* out, const uint64_t* in, const uint32_t* src_mods, uint32_t n_src,
+                      const uint32_t* dst_mods, uint32_t n_dst, uint32_t npolys, void* stream);
+
+/* ---- ckks.py scheme ops --------------------------------------------------- */
+/* scratch needed by keyswitch/hmult/rotate at `level` */
+size_t hcnn_ks_workspace_bytes(const hcnn_ctx* ctx, uint32_t level);
+/* _keyswitch_coeff ckks.py:548-602 applied to iNTT(x_eval): x_eval is an
+ * eval-domain poly over q_0..q_level; out0/out1 eval-domain over the same basis */
+int hcnn_keyswitch(hcnn_ctx* ctx, uint64_t* out0, uint64_t* out1, const uint64_t* x_eval, uint32_t level,
+                   const uint64_t* key_b, const uint64_t* key_a, void* ws, void* stream);
+/* hmult ckks.py:605-613 (tensor product + relinearisation; caller rescales) */
+int hcnn_hmult(hcnn_ctx* ctx, uint64_t* out_ct, const uint64_t* a_ct, const uint64_t* b_ct, uint32_t level,
+               const uint64_t* rlk_b, const uint64_t* rlk_a, void* ws, void* stream);
+/* n_rot single-key rotations of one ciphertext sharing one ModUp (hoisted);
+ * rotation i applies galois[i] with key (keys_b[i], keys_a[i]) and is
+ * bit-exact with ckks._apply_step ckks.py:620-625.  outs[i] are ct buffers. */
+int hcnn_rotate_hoisted(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* ct, uint32_t level, uint32_t n_rot,
+                        const uint64_t* galois, const uint64_t* const* keys_b, const uint64_t* const* keys_a,
+                        void* ws, void* stream);
+/* rescale ckks.py:506-528 for npolys polys at `level` -> level-1 */
+size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* ctx, uint32_t npolys);
+int hcnn_rescale(hcnn_ctx* ctx, uint64_t* out, const uint64_t* in, uint32_t level, uint32_t npolys, void* ws,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCNN_B200_H */

@@ -1,0 +1,10 @@
+"""hcnn-b200: B200-native RNS-CKKS engine for encrypted CNN inference.
+
+Drop-in for the hot path of the reference package ``hcnn``
+(/root/reference/pkg/src/hcnn): ``ring`` and ``ckks`` keep its API with
+ciphertexts resident in HBM; ``packing`` and ``graph`` run the HyPHEN /
+AESPA layers on top.  All integer arithmetic is CUDA (sm_100a) behind the C
+ABI in include/hcnn_b200.h; there is no CPU fallback.
+"""
+
+__version__ = "0.1.0"

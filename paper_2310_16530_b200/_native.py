@@ -1,0 +1,124 @@
+"""ctypes binding of the C ABI in include/hcnn_b200.h.
+
+This is the only place Python touches the CUDA engine.  There is no CPU
+fallback: if ``libhcnn_b200.so`` is missing or no CUDA device is visible,
+every entry point raises ``NativeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+from .errors import (
+    BasisError,
+    DomainError,
+    HcnnError,
+    KeyError_,
+    LevelError,
+    NativeError,
+    ParameterError,
+    ScaleError,
+)
+
+LIB_NAME = "libhcnn_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+
+_VP = ctypes.c_void_p
+_U32 = ctypes.c_uint32
+_U64 = ctypes.c_uint64
+_INT = ctypes.c_int
+_SZ = ctypes.c_size_t
+_PU64 = ctypes.POINTER(ctypes.c_uint64)
+_PU32 = ctypes.POINTER(ctypes.c_uint32)
+
+# name -> (restype, argtypes); keep in sync with include/hcnn_b200.h
+SIGNATURES = {
+    "hcnn_last_error": (ctypes.c_char_p, []),
+    "hcnn_abi_version": (_INT, []),
+    "hcnn_ctx_create": (_INT, [ctypes.POINTER(_VP), _INT, _U32, _PU64, _U32, _PU64, _U32]),
+    "hcnn_ctx_destroy": (None, [_VP]),
+    "hcnn_ctx_psi": (_INT, [_VP, _U32, _PU64]),
+    "hcnn_ntt_forward": (_INT, [_VP, _VP, _U32, _U32, _U32, _VP]),
+    "hcnn_ntt_inverse": (_INT, [_VP, _VP, _U32, _U32, _U32, _VP]),
+    "hcnn_poly_add": (_INT, [_VP, _VP, _VP, _VP, _U32, _U32, _U32, _INT, _VP]),
+    "hcnn_poly_sub": (_INT, [_VP, _VP, _VP, _VP, _U32, _U32, _U32, _INT, _VP]),
+    "hcnn_poly_neg": (_INT, [_VP, _VP, _VP, _U32, _U32, _U32, _VP]),
+    "hcnn_poly_mul": (_INT, [_VP, _VP, _VP, _VP, _U32, _U32, _U32, _INT, _VP]),
+    "hcnn_poly_mul_mont": (_INT, [_VP, _VP, _VP, _VP, _U32, _U32, _U32, _INT, _VP]),
+    "hcnn_poly_mac_mont": (_INT, [_VP, _VP, _VP, _VP, _U32, _U32, _U32, _INT, _VP]),
+    "hcnn_to_mont": (_INT, [_VP, _VP, _VP, _U32, _U32, _U32, _VP]),
+    "hcnn_from_mont": (_INT, [_VP, _VP, _VP, _U32, _U32, _U32, _VP]),
+    "hcnn_scalar_mul": (_INT, [_VP, _VP, _VP, _PU64, _U32, _U32, _U32, _VP]),
+    "hcnn_from_signed": (_INT, [_VP, _VP, _VP, _U32, _U32, _U32, _VP]),
+    "hcnn_automorphism": (_INT, [_VP, _VP, _VP, _U64, _INT, _U32, _U32, _U32, _VP]),
+    "hcnn_base_convert": (_INT, [_VP, _VP, _VP, _PU32, _U32, _PU32, _U32, _U32, _VP]),
+    "hcnn_ks_workspace_bytes": (_SZ, [_VP, _U32]),
+    "hcnn_keyswitch": (_INT, [_VP, _VP, _VP, _VP, _U32, _VP, _VP, _VP, _VP]),
+    "hcnn_hmult": (_INT, [_VP, _VP, _VP, _VP, _U32, _VP, _VP, _VP, _VP]),
+    "hcnn_rotate_hoisted": (_INT, [_VP, ctypes.POINTER(_VP), _VP, _U32, _U32, _PU64,
+                                   ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP, _VP]),
+    "hcnn_rescale_workspace_bytes": (_SZ, [_VP, _U32]),
+    "hcnn_rescale": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP, _VP]),
+}
+
+_STATUS = {
+    1: ParameterError,
+    2: DomainError,
+    3: BasisError,
+    4: LevelError,
+    5: ScaleError,
+    6: KeyError_,
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> ctypes.CDLL:
+    """Load the engine (once).  Fails loudly: there is no fallback path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = os.environ.get("HCNN_B200_LIB", str(LIB_PATH))
+        if not os.path.exists(path):
+            raise NativeError(
+                f"CUDA engine {path} is not built; run __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (load().hcnn_last_error() or b"").decode(errors="replace")
+    cls = _STATUS.get(rc, NativeError)
+    raise cls(f"hcnn-b200: {msg} (status {rc})")
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
+
+
+def u64_array(values) -> ctypes.Array:
+    vals = [int(v) for v in values]
+    return (ctypes.c_uint64 * len(vals))(*vals)
+
+
+def u32_array(values) -> ctypes.Array:
+    vals = [int(v) for v in values]
+    return (ctypes.c_uint32 * len(vals))(*vals)
+
+
+__all__ = ["load", "check", "exported_symbols", "u64_array", "u32_array", "LIB_PATH", "HcnnError"]

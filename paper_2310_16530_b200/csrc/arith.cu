@@ -1,0 +1,423 @@
+// Element-wise, base-conversion, key-switch and rescale kernels (sm_100a).
+//
+// All of these are HBM-bound streaming kernels over [poly][limb][N] u64
+// residues.  Each maps one CTA row to one (poly, limb) pair so the modulus
+// constants are warp-uniform, and moves 16 B per thread per access.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "arith.cuh"
+
+namespace hcnn {
+
+// ---------------------------------------------------------------------------
+// element-wise (ring.py:264-314, kernels.py:190-230)
+// grid: x over N/(2*blockDim), y over rows = npolys*nlimbs
+// ---------------------------------------------------------------------------
+struct RowCtx {
+  u32 row, z, r, mod;
+};
+__device__ __forceinline__ RowCtx row_ctx(const Basis& b) {
+  RowCtx c;
+  c.row = blockIdx.y;
+  u32 nl = b.nlimbs();
+  c.z = c.row / nl;
+  c.r = c.row - c.z * nl;
+  c.mod = b.mod_of(c.r);
+  return c;
+}
+
+__global__ void k_ew_binary(int op, u64* __restrict__ out, const u64* __restrict__ a, const u64* __restrict__ b,
+                            Basis basis, u32 logN, int b_bcast, const ModConsts* __restrict__ mc) {
+  RowCtx rc = row_ctx(basis);
+  const u32 N = 1u << logN;
+  const ModConsts C = mc[rc.mod];
+  const size_t off = (size_t)rc.row * N;
+  const size_t boff = (size_t)(b_bcast ? rc.r : rc.row) * N;
+  const ulonglong2* A = reinterpret_cast<const ulonglong2*>(a + off);
+  const ulonglong2* B = reinterpret_cast<const ulonglong2*>(b + boff);
+  ulonglong2* O = reinterpret_cast<ulonglong2*>(out + off);
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < N / 2; i += gridDim.x * blockDim.x) {
+    ulonglong2 x = A[i], y = B[i], o;
+    switch (op) {
+      case EW_ADD:
+        o.x = add_mod(x.x, y.x, C.q);
+        o.y = add_mod(x.y, y.y, C.q);
+        break;
+      case EW_SUB:
+        o.x = sub_mod(x.x, y.x, C.q);
+        o.y = sub_mod(x.y, y.y, C.q);
+        break;
+      case EW_MUL_MONT:  // a * b_mont * 2^-64  (pmult_mont, _mul_rows_mont)
+        o.x = mont_mul(x.x, y.x, C.q, C.ninv);
+        o.y = mont_mul(x.y, y.y, C.q, C.ninv);
+        break;
+      case EW_MUL:  // both ordinary residues (poly_mul_pointwise)
+        o.x = mont_mul(mont_mul(x.x, y.x, C.q, C.ninv), C.r2, C.q, C.ninv);
+        o.y = mont_mul(mont_mul(x.y, y.y, C.q, C.ninv), C.r2, C.q, C.ninv);
+        break;
+      default:  // EW_MAC_MONT: out += a * b_mont
+      {
+        ulonglong2 acc = O[i];
+        o.x = add_mod(acc.x, mont_mul(x.x, y.x, C.q, C.ninv), C.q);
+        o.y = add_mod(acc.y, mont_mul(x.y, y.y, C.q, C.ninv), C.q);
+      }
+    }
+    O[i] = o;
+  }
+}
+
+__global__ void k_ew_unary(int op, u64* __restrict__ out, const u64* __restrict__ a, Basis basis, u32 logN,
+                           const ModConsts* __restrict__ mc, const u64* __restrict__ consts,
+                           const u64* __restrict__ consts_sh) {
+  RowCtx rc = row_ctx(basis);
+  const u32 N = 1u << logN;
+  const ModConsts C = mc[rc.mod];
+  const size_t off = (size_t)rc.row * N;
+  const ulonglong2* A = reinterpret_cast<const ulonglong2*>(a + off);
+  ulonglong2* O = reinterpret_cast<ulonglong2*>(out + off);
+  u64 w = 0, wp = 0;
+  if (op == EW_SCALAR) {
+    w = consts[rc.r];
+    wp = consts_sh[rc.r];
+  }
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < N / 2; i += gridDim.x * blockDim.x) {
+    ulonglong2 x = A[i], o;
+    switch (op) {
+      case EW_NEG:
+        o.x = neg_mod(x.x, C.q);
+        o.y = neg_mod(x.y, C.q);
+        break;
+      case EW_TO_MONT:
+        o.x = mont_mul(x.x, C.r2, C.q, C.ninv);
+        o.y = mont_mul(x.y, C.r2, C.q, C.ninv);
+        break;
+      case EW_FROM_MONT:
+        o.x = mont_mul(x.x, 1ull, C.q, C.ninv);
+        o.y = mont_mul(x.y, 1ull, C.q, C.ninv);
+        break;
+      default:  // EW_SCALAR
+        o.x = shoup_mul(x.x, w, wp, C.q);
+        o.y = shoup_mul(x.y, w, wp, C.q);
+    }
+    O[i] = o;
+  }
+}
+
+// signed int64 coefficients (one row of N per poly) -> residues in every
+// limb (ring.py:446-468 replication, ckks.py:284-288 encode reduction)
+__global__ void k_from_signed(u64* __restrict__ out, const long long* __restrict__ in, Basis basis, u32 logN,
+                              const ModConsts* __restrict__ mc) {
+  RowCtx rc = row_ctx(basis);
+  const u32 N = 1u << logN;
+  const ModConsts C = mc[rc.mod];
+  const long long* src = in + (size_t)rc.z * N;
+  u64* O = out + (size_t)rc.row * N;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    long long v = src[i];
+    u64 mag = v >= 0 ? (u64)v : (u64)(-(v + 1)) + 1ull;
+    u64 red = mont_mul(mag, C.one_m, C.q, C.ninv);  // |v| mod q
+    O[i] = v >= 0 ? red : neg_mod(red, C.q);
+  }
+}
+
+// Galois automorphisms.  Eval domain: pure permutation.
+// Coefficient domain: out[i*g mod 2N] = +-in[i] (ring.py:405-439).
+__global__ void k_automorph(int eval_domain, u64* __restrict__ out, const u64* __restrict__ in, Basis basis,
+                            u32 logN, u64 g, const ModConsts* __restrict__ mc) {
+  RowCtx rc = row_ctx(basis);
+  const u32 N = 1u << logN;
+  const u64 q = mc[rc.mod].q;
+  const u64* I = in + (size_t)rc.row * N;
+  u64* O = out + (size_t)rc.row * N;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    if (eval_domain) {
+      O[k] = I[galois_src(k, g, logN)];
+    } else {
+      u64 j = ((u64)k * g) & ((2ull << logN) - 1);
+      u64 v = I[k];
+      if (j < N) O[j] = v;
+      else O[j - N] = neg_mod(v, q);
+    }
+  }
+}
+
+// hmult tensor product (ckks.py:609-611): d0=a0b0, d1=a0b1+a1b0, d2=a1b1
+__global__ void k_tensor(u64* __restrict__ d0, u64* __restrict__ d1, u64* __restrict__ d2,
+                         const u64* __restrict__ a, const u64* __restrict__ b, u32 nlimbs, u32 logN,
+                         const ModConsts* __restrict__ mc) {
+  const u32 r = blockIdx.y;
+  const u32 N = 1u << logN;
+  const ModConsts C = mc[r];
+  const size_t pst = (size_t)nlimbs * N;
+  const size_t off = (size_t)r * N;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    u64 a0 = a[off + k], a1 = a[pst + off + k];
+    u64 b0 = b[off + k], b1 = b[pst + off + k];
+    u64 t0 = mont_mul(a0, b0, C.q, C.ninv);
+    u64 t2 = mont_mul(a1, b1, C.q, C.ninv);
+    u64 hi = 0, lo = 0;
+    mac128(hi, lo, a0, b1, C.q);
+    mac128(hi, lo, a1, b0, C.q);
+    u64 t1 = redc128(hi, lo, C.q, C.ninv);
+    d0[off + k] = mont_mul(t0, C.r2, C.q, C.ninv);
+    d1[off + k] = mont_mul(t1, C.r2, C.q, C.ninv);
+    d2[off + k] = mont_mul(t2, C.r2, C.q, C.ninv);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// centred fast base conversion (ring.py:378-398, kernels.py:283-301)
+// ---------------------------------------------------------------------------
+#define FBC_MAX_SRC 64
+
+__device__ __forceinline__ void fbc_point(const FbcDev& T, const ModConsts* __restrict__ mc,
+                                          const u64* __restrict__ src, size_t src_limb_stride,
+                                          u64* __restrict__ dst, u32 k, u32 N, u32 nt) {
+  u64 mag[FBC_MAX_SRC];
+  u32 negmask_lo = 0, negmask_hi = 0;
+  const u32 ns = T.ns;
+  for (u32 i = 0; i < ns; ++i) {
+    const u64 qi = mc[T.src_mod[i]].q;
+    u64 y = shoup_mul(src[(size_t)i * src_limb_stride + k], T.inv_punc[i], T.inv_punc_sh[i], qi);
+    bool neg = y > (qi >> 1);
+    mag[i] = neg ? qi - y : y;
+    if (neg) {
+      if (i < 32) negmask_lo |= 1u << i;
+      else negmask_hi |= 1u << (i - 32);
+    }
+  }
+  for (u32 t = 0; t < nt; ++t) {
+    const ModConsts C = mc[T.dst_mod[t]];
+    const u64* row = T.tmat + (size_t)t * ns;
+    u64 phi = 0, plo = 0, nhi = 0, nlo = 0;
+    for (u32 i = 0; i < ns; ++i) {
+      bool neg = i < 32 ? (negmask_lo >> i) & 1u : (negmask_hi >> (i - 32)) & 1u;
+      if (neg) mac128(nhi, nlo, mag[i], row[i], C.q);
+      else mac128(phi, plo, mag[i], row[i], C.q);
+    }
+    // (pos - neg) mod q*2^64, then one REDC
+    u64 lo = plo - nlo;
+    u64 borrow = plo < nlo ? 1ull : 0ull;
+    long long hi = (long long)phi - (long long)nhi - (long long)borrow;
+    if (hi < 0) hi += (long long)C.q;
+    dst[(size_t)T.dst_pos[t] * N + k] = redc128((u64)hi, lo, C.q, C.ninv);
+  }
+}
+
+// generic base_convert: poly z: src limbs at in + z*in_pst + i*N
+__global__ void k_fbc(FbcDev T, const ModConsts* __restrict__ mc, const u64* __restrict__ in, size_t in_pst,
+                      u64* __restrict__ out, size_t out_pst, u32 logN, u32 nt) {
+  const u32 N = 1u << logN, z = blockIdx.y;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x)
+    fbc_point(T, mc, in + (size_t)z * in_pst, N, out + (size_t)z * out_pst, k, N, nt);
+}
+
+// ModUp of every digit of a key-switch input (ckks.py:563-578):
+// digit j's limbs [j*alpha, ...) of xc are converted to the extended basis
+// minus the digit, written into raised[j] at their basis positions.
+__global__ void k_modup(const FbcDev* __restrict__ tabs, const ModConsts* __restrict__ mc,
+                        const u64* __restrict__ xc, u64* __restrict__ raised, u32 alpha, u32 n_ext, u32 logN) {
+  const u32 N = 1u << logN, j = blockIdx.y;
+  const FbcDev T = tabs[j];
+  const u64* src = xc + (size_t)j * alpha * N;
+  u64* dst = raised + (size_t)j * n_ext * N;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x)
+    fbc_point(T, mc, src, N, dst, k, N, T.nt);
+}
+
+// Key-switch inner product (ckks.py:579-586), fused over digits with one
+// REDC per output: acc_{b,a}[r] = sum_j raised_j[r] * key_{b,a}[j][mod(r)]
+// (key rows are Montgomery form, so the 128-bit sum REDCs straight to the
+// ordinary residue).  g != 1 applies the eval-domain Galois permutation to
+// the raised digits on the fly (hoisted rotation).
+__global__ void k_ks_inner(u64* __restrict__ acc, const u64* __restrict__ x_eval, const u64* __restrict__ raised,
+                           const u64* __restrict__ key_b, const u64* __restrict__ key_a, Basis basis, u32 alpha,
+                           u32 ndig, u32 logN, u64 g, const ModConsts* __restrict__ mc) {
+  const u32 N = 1u << logN, r = blockIdx.y;
+  const u32 n_ext = basis.nlimbs();
+  const u32 mod = basis.mod_of(r);
+  const ModConsts C = mc[mod];
+  const size_t key_dst = (size_t)(basis.Lq + basis.np) * N;  // per-digit key stride
+  // digit owning limb r (only q limbs belong to digits)
+  const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    const u32 ks = g == 1 ? k : galois_src(k, g, logN);
+    u64 bhi = 0, blo = 0, ahi = 0, alo = 0;
+    for (u32 j = 0; j < ndig; ++j) {
+      u64 v = (j == own) ? x_eval[(size_t)r * N + ks] : raised[((size_t)j * n_ext + r) * N + ks];
+      const size_t kofs = (size_t)j * key_dst + (size_t)mod * N + k;
+      mac128(bhi, blo, v, key_b[kofs], C.q);
+      mac128(ahi, alo, v, key_a[kofs], C.q);
+    }
+    acc[(size_t)r * N + k] = redc128(bhi, blo, C.q, C.ninv);
+    acc[((size_t)n_ext + r) * N + k] = redc128(ahi, alo, C.q, C.ninv);
+  }
+}
+
+// ModDown combine (ckks.py:593-601): out_z[r] = add_z[perm(k)] + (acc_z[r] - lift_z[r]) * P^-1
+__global__ void k_moddown_combine(u64* __restrict__ out0, u64* __restrict__ out1, const u64* __restrict__ acc,
+                                  const u64* __restrict__ lift, const u64* __restrict__ add0,
+                                  const u64* __restrict__ add1, u64 g_add, u32 nq, u32 n_ext, u32 logN,
+                                  const u64* __restrict__ pinv, const u64* __restrict__ pinv_sh,
+                                  const ModConsts* __restrict__ mc) {
+  const u32 N = 1u << logN, r = blockIdx.y, z = blockIdx.z;
+  const u64 q = mc[r].q;
+  const u64 w = pinv[r], wp = pinv_sh[r];
+  const u64* A = acc + ((size_t)z * n_ext + r) * N;
+  const u64* L = lift + ((size_t)z * nq + r) * N;
+  const u64* ADD = z == 0 ? add0 : add1;
+  u64* O = (z == 0 ? out0 : out1) + (size_t)r * N;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    u64 v = shoup_mul(sub_mod(A[k], L[k], q), w, wp, q);
+    if (ADD) {
+      u32 ks = g_add == 1 ? k : galois_src(k, g_add, logN);
+      v = add_mod(v, ADD[(size_t)r * N + ks], q);
+    }
+    O[k] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// rescale (ckks.py:506-528)
+// ---------------------------------------------------------------------------
+// centred lift of the (coefficient-domain) top limb into limbs 0..l-1
+__global__ void k_rescale_lift(u64* __restrict__ out, const u64* __restrict__ top, u32 l, u32 logN,
+                               const ModConsts* __restrict__ mc) {
+  const u32 N = 1u << logN, i = blockIdx.y, z = blockIdx.z;
+  const ModConsts C = mc[i];
+  const u64 qt = mc[l].q;
+  const u64 qt_mod = qt % C.q;  // uniform
+  const u64* T = top + (size_t)z * N;
+  u64* O = out + ((size_t)z * l + i) * N;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    u64 t = T[k];
+    u64 rr = mont_mul(t, C.one_m, C.q, C.ninv);  // t mod q_i
+    if (t > (qt >> 1)) rr = sub_mod(rr, qt_mod, C.q);
+    O[k] = rr;
+  }
+}
+
+// out = (body - lift) * q_l^-1 ; lift already NTT'd in `out`
+__global__ void k_rescale_combine(u64* __restrict__ out, const u64* __restrict__ in, u32 l, u32 logN,
+                                  const u64* __restrict__ inv, const u64* __restrict__ inv_sh,
+                                  const ModConsts* __restrict__ mc) {
+  const u32 N = 1u << logN, i = blockIdx.y, z = blockIdx.z;
+  const u64 q = mc[i].q, w = inv[i], wp = inv_sh[i];
+  const u64* B = in + ((size_t)z * (l + 1) + i) * N;
+  u64* O = out + ((size_t)z * l + i) * N;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x)
+    O[k] = shoup_mul(sub_mod(B[k], O[k], q), w, wp, q);
+}
+
+// copy the top limb (index l) of each poly into a packed [npolys][N] buffer
+__global__ void k_gather_limb(u64* __restrict__ out, const u64* __restrict__ in, u32 limb, u32 nlimbs, u32 logN) {
+  const u32 N = 1u << logN, z = blockIdx.y;
+  const u64* I = in + ((size_t)z * nlimbs + limb) * N;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) out[(size_t)z * N + k] = I[k];
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+static inline dim3 row_grid(u32 work_per_row, u32 rows, u32 threads) {
+  u32 x = (work_per_row + threads - 1) / threads;
+  if (x == 0) x = 1;
+  if (x > 1024) x = 1024;
+  return dim3(x, rows, 1);
+}
+
+cudaError_t launch_ew_binary(int op, u64* out, const u64* a, const u64* b, Basis basis, u32 logN, u32 npolys,
+                             int b_bcast, const ModConsts* mc, cudaStream_t st) {
+  u32 rows = npolys * basis.nlimbs();
+  if (!rows) return cudaSuccess;
+  u32 N = 1u << logN;
+  k_ew_binary<<<row_grid(N / 2, rows, 256), 256, 0, st>>>(op, out, a, b, basis, logN, b_bcast, mc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ew_unary(int op, u64* out, const u64* a, Basis basis, u32 logN, u32 npolys,
+                            const ModConsts* mc, const u64* consts, const u64* consts_sh, cudaStream_t st) {
+  u32 rows = npolys * basis.nlimbs();
+  if (!rows) return cudaSuccess;
+  u32 N = 1u << logN;
+  k_ew_unary<<<row_grid(N / 2, rows, 256), 256, 0, st>>>(op, out, a, basis, logN, mc, consts, consts_sh);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_from_signed(u64* out, const long long* in, Basis basis, u32 logN, u32 npolys,
+                               const ModConsts* mc, cudaStream_t st) {
+  u32 rows = npolys * basis.nlimbs();
+  if (!rows) return cudaSuccess;
+  k_from_signed<<<row_grid(1u << logN, rows, 256), 256, 0, st>>>(out, in, basis, logN, mc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_automorph(int eval_domain, u64* out, const u64* in, Basis basis, u32 logN, u32 npolys, u64 g,
+                             const ModConsts* mc, cudaStream_t st) {
+  u32 rows = npolys * basis.nlimbs();
+  if (!rows) return cudaSuccess;
+  k_automorph<<<row_grid(1u << logN, rows, 256), 256, 0, st>>>(eval_domain, out, in, basis, logN, g, mc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tensor(u64* d0, u64* d1, u64* d2, const u64* a, const u64* b, u32 nlimbs, u32 logN,
+                          const ModConsts* mc, cudaStream_t st) {
+  k_tensor<<<row_grid(1u << logN, nlimbs, 256), 256, 0, st>>>(d0, d1, d2, a, b, nlimbs, logN, mc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fbc(const FbcDev& T, const ModConsts* mc, const u64* in, size_t in_pst, u64* out,
+                       size_t out_pst, u32 logN, u32 npolys, u32 nt, cudaStream_t st) {
+  if (T.ns > FBC_MAX_SRC) return cudaErrorInvalidValue;
+  k_fbc<<<row_grid(1u << logN, npolys, 128), 128, 0, st>>>(T, mc, in, in_pst, out, out_pst, logN, nt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_modup(const FbcDev* tabs, u32 ndig, const ModConsts* mc, const u64* xc, u64* raised, u32 alpha,
+                         u32 n_ext, u32 logN, cudaStream_t st) {
+  if (alpha > FBC_MAX_SRC) return cudaErrorInvalidValue;
+  k_modup<<<row_grid(1u << logN, ndig, 128), 128, 0, st>>>(tabs, mc, xc, raised, alpha, n_ext, logN);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
+                            Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
+                            cudaStream_t st) {
+  k_ks_inner<<<row_grid(1u << logN, basis.nlimbs(), 256), 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis,
+                                                                        alpha, ndig, logN, g, mc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,
+                                   const u64* add1, u64 g_add, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
+                                   const u64* pinv_sh, const ModConsts* mc, cudaStream_t st) {
+  dim3 g = row_grid(1u << logN, nq, 256);
+  g.z = 2;
+  k_moddown_combine<<<g, 256, 0, st>>>(out0, out1, acc, lift, add0, add1, g_add, nq, n_ext, logN, pinv, pinv_sh,
+                                       mc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 npolys, const ModConsts* mc,
+                                cudaStream_t st) {
+  dim3 g = row_grid(1u << logN, l, 256);
+  g.z = npolys;
+  k_rescale_lift<<<g, 256, 0, st>>>(out, top, l, logN, mc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rescale_combine(u64* out, const u64* in, u32 l, u32 logN, u32 npolys, const u64* inv,
+                                   const u64* inv_sh, const ModConsts* mc, cudaStream_t st) {
+  dim3 g = row_grid(1u << logN, l, 256);
+  g.z = npolys;
+  k_rescale_combine<<<g, 256, 0, st>>>(out, in, l, logN, inv, inv_sh, mc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_limb(u64* out, const u64* in, u32 limb, u32 nlimbs, u32 logN, u32 npolys,
+                               cudaStream_t st) {
+  k_gather_limb<<<row_grid(1u << logN, npolys, 256), 256, 0, st>>>(out, in, limb, nlimbs, logN);
+  return cudaGetLastError();
+}
+
+}  // namespace hcnn

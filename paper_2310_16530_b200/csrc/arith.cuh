@@ -1,0 +1,36 @@
+#pragma once
+#include "kernels.cuh"
+
+namespace hcnn {
+
+enum { EW_ADD = 0, EW_SUB = 1, EW_MUL_MONT = 2, EW_MUL = 3, EW_MAC_MONT = 4 };
+enum { EW_NEG = 0, EW_TO_MONT = 1, EW_FROM_MONT = 2, EW_SCALAR = 3 };
+
+cudaError_t launch_ew_binary(int op, u64* out, const u64* a, const u64* b, Basis basis, u32 logN, u32 npolys,
+                             int b_bcast, const ModConsts* mc, cudaStream_t st);
+cudaError_t launch_ew_unary(int op, u64* out, const u64* a, Basis basis, u32 logN, u32 npolys,
+                            const ModConsts* mc, const u64* consts, const u64* consts_sh, cudaStream_t st);
+cudaError_t launch_from_signed(u64* out, const long long* in, Basis basis, u32 logN, u32 npolys,
+                               const ModConsts* mc, cudaStream_t st);
+cudaError_t launch_automorph(int eval_domain, u64* out, const u64* in, Basis basis, u32 logN, u32 npolys, u64 g,
+                             const ModConsts* mc, cudaStream_t st);
+cudaError_t launch_tensor(u64* d0, u64* d1, u64* d2, const u64* a, const u64* b, u32 nlimbs, u32 logN,
+                          const ModConsts* mc, cudaStream_t st);
+cudaError_t launch_fbc(const FbcDev& T, const ModConsts* mc, const u64* in, size_t in_pst, u64* out,
+                       size_t out_pst, u32 logN, u32 npolys, u32 nt, cudaStream_t st);
+cudaError_t launch_modup(const FbcDev* tabs, u32 ndig, const ModConsts* mc, const u64* xc, u64* raised, u32 alpha,
+                         u32 n_ext, u32 logN, cudaStream_t st);
+cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
+                            Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
+                            cudaStream_t st);
+cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,
+                                   const u64* add1, u64 g_add, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
+                                   const u64* pinv_sh, const ModConsts* mc, cudaStream_t st);
+cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 npolys, const ModConsts* mc,
+                                cudaStream_t st);
+cudaError_t launch_rescale_combine(u64* out, const u64* in, u32 l, u32 logN, u32 npolys, const u64* inv,
+                                   const u64* inv_sh, const ModConsts* mc, cudaStream_t st);
+cudaError_t launch_gather_limb(u64* out, const u64* in, u32 limb, u32 nlimbs, u32 logN, u32 npolys,
+                               cudaStream_t st);
+
+}  // namespace hcnn

@@ -1,0 +1,628 @@
+// C ABI: device context (CkksParams in HBM) and the scheme-level
+// orchestration of keyswitch / hmult / rotate / rescale.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/hcnn_b200.h"
+#include "arith.cuh"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace hcnn;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return fail(HCNN_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+  } while (0)
+
+// host-resident FBC table with its device copy
+struct FbcStore {
+  FbcDev dev{};
+  void* mem = nullptr;
+};
+
+struct ModupSet {
+  std::vector<FbcStore> digits;
+  FbcDev* d_tabs = nullptr;  // device array of FbcDev, one per digit
+};
+
+struct hcnn_ctx {
+  int device = 0;
+  u32 n = 0, logN = 0, Lq = 0, K = 0, nmods = 0, alpha = 0, dnum = 0;
+  std::vector<u64> mods, psi;
+  std::vector<ModConsts> hmc;
+  ModConsts* d_mc = nullptr;
+  u64 *d_tw = nullptr, *d_twp = nullptr, *d_itw = nullptr, *d_itwp = nullptr;
+  FbcStore moddown;                  // P -> q_0..q_{Lq-1}
+  u64 *d_pinv = nullptr, *d_pinv_sh = nullptr;  // P^-1 mod q_i
+  u64 *d_rinv = nullptr, *d_rinv_sh = nullptr;  // [l][i] q_l^-1 mod q_i
+  std::mutex mu;
+  std::map<u32, ModupSet> modup;
+  std::map<std::vector<u32>, FbcStore> generic;
+  NttTables tables() const {
+    NttTables T;
+    T.logN = logN;
+    T.mc = d_mc;
+    T.tw = d_tw;
+    T.twp = d_twp;
+    T.itw = d_itw;
+    T.itwp = d_itwp;
+    return T;
+  }
+  Basis basis(u32 nq, u32 np) const {
+    Basis b;
+    b.nq = nq;
+    b.np = np;
+    b.Lq = Lq;
+    return b;
+  }
+};
+
+static u32 bitrev(u32 x, u32 bits) {
+  u32 r = 0;
+  for (u32 i = 0; i < bits; ++i) {
+    r = (r << 1) | (x & 1);
+    x >>= 1;
+  }
+  return r;
+}
+
+// _find_psi (ring.py:160-167): smallest r in [2,1000) whose (q-1)/2N power
+// is a primitive 2N-th root
+static bool find_psi(u64 q, u32 n, u64* out) {
+  if ((q - 1) % (2ull * n) != 0) return false;
+  for (u64 r = 2; r < 1000; ++r) {
+    u64 psi = h_powmod(r, (q - 1) / (2ull * n), q);
+    if (psi != 1 && h_powmod(psi, n, q) == q - 1) {
+      *out = psi;
+      return true;
+    }
+  }
+  return false;
+}
+
+static int build_fbc(hcnn_ctx* c, const std::vector<u32>& src, const std::vector<u32>& dst,
+                     const std::vector<u32>& dst_pos, FbcStore* st) {
+  const u32 ns = (u32)src.size(), nt = (u32)dst.size();
+  std::vector<u32> u32buf;
+  u32buf.insert(u32buf.end(), src.begin(), src.end());
+  u32buf.insert(u32buf.end(), dst.begin(), dst.end());
+  u32buf.insert(u32buf.end(), dst_pos.begin(), dst_pos.end());
+  while (u32buf.size() % 2) u32buf.push_back(0);
+  std::vector<u64> u64buf(2 * ns + (size_t)nt * ns);
+  for (u32 i = 0; i < ns; ++i) {
+    u64 qi = c->mods[src[i]];
+    u64 prod = 1;
+    for (u32 j = 0; j < ns; ++j)
+      if (j != i) prod = h_mulmod(prod, c->mods[src[j]] % qi, qi);
+    u64 inv = h_invmod(prod, qi);
+    u64buf[i] = inv;
+    u64buf[ns + i] = h_shoup(inv, qi);
+  }
+  for (u32 t = 0; t < nt; ++t) {
+    u64 qt = c->mods[dst[t]];
+    for (u32 i = 0; i < ns; ++i) {
+      u64 prod = 1 % qt;
+      for (u32 j = 0; j < ns; ++j)
+        if (j != i) prod = h_mulmod(prod, c->mods[src[j]] % qt, qt);
+      u64buf[2 * ns + (size_t)t * ns + i] = h_to_mont(prod, qt);
+    }
+  }
+  size_t b32 = u32buf.size() * 4, b64 = u64buf.size() * 8;
+  CK(cudaMalloc(&st->mem, b32 + b64));
+  CK(cudaMemcpy(st->mem, u32buf.data(), b32, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy((char*)st->mem + b32, u64buf.data(), b64, cudaMemcpyHostToDevice));
+  u32* d32 = (u32*)st->mem;
+  u64* d64 = (u64*)((char*)st->mem + b32);
+  st->dev.ns = ns;
+  st->dev.nt = nt;
+  st->dev.src_mod = d32;
+  st->dev.dst_mod = d32 + ns;
+  st->dev.dst_pos = d32 + ns + nt;
+  st->dev.inv_punc = d64;
+  st->dev.inv_punc_sh = d64 + ns;
+  st->dev.tmat = d64 + 2 * ns;
+  return HCNN_OK;
+}
+
+// ModUp tables for level l (ckks.py:563-571): digit j = q limbs
+// [j*alpha, min(j*alpha+alpha, nq)), targets = Q_l||P minus the digit
+static int get_modup(hcnn_ctx* c, u32 level, ModupSet** out) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  auto it = c->modup.find(level);
+  if (it != c->modup.end()) {
+    *out = &it->second;
+    return HCNN_OK;
+  }
+  ModupSet set;
+  const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
+  Basis b = c->basis(nq, c->K);
+  std::vector<FbcDev> devs;
+  for (u32 j = 0; j < nd; ++j) {
+    u32 lo = j * c->alpha, hi = std::min(lo + c->alpha, nq);
+    std::vector<u32> src, dst, pos;
+    for (u32 i = lo; i < hi; ++i) src.push_back(i);
+    for (u32 r = 0; r < n_ext; ++r) {
+      if (r >= lo && r < hi) continue;
+      dst.push_back(b.mod_of(r));
+      pos.push_back(r);
+    }
+    FbcStore st;
+    int rc = build_fbc(c, src, dst, pos, &st);
+    if (rc) return rc;
+    set.digits.push_back(st);
+    devs.push_back(st.dev);
+  }
+  CK(cudaMalloc(&set.d_tabs, sizeof(FbcDev) * devs.size()));
+  CK(cudaMemcpy(set.d_tabs, devs.data(), sizeof(FbcDev) * devs.size(), cudaMemcpyHostToDevice));
+  auto res = c->modup.emplace(level, set);
+  *out = &res.first->second;
+  return HCNN_OK;
+}
+
+extern "C" {
+
+const char* hcnn_last_error(void) { return g_err.c_str(); }
+int hcnn_abi_version(void) { return 1; }
+
+int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_moduli, uint32_t n_q,
+                    const uint64_t* p_moduli, uint32_t n_p) {
+  if (!out) return fail(HCNN_E_PARAMETER, "null output handle");
+  if (n < 4 || (n & (n - 1))) return fail(HCNN_E_PARAMETER, "ring degree must be a power of two >= 4");
+  if (n > (1u << 17)) return fail(HCNN_E_PARAMETER, "ring degree above 2^17 unsupported");
+  if (n_q == 0) return fail(HCNN_E_BASIS, "empty q chain");
+  if (n_q + n_p > HCNN_MAX_MODS) return fail(HCNN_E_PARAMETER, "too many moduli");
+  CK(cudaSetDevice(device));
+  hcnn_ctx* c = new hcnn_ctx();
+  c->device = device;
+  c->n = n;
+  c->logN = 0;
+  while ((1u << c->logN) < n) ++c->logN;
+  c->Lq = n_q;
+  c->K = n_p;
+  c->nmods = n_q + n_p;
+  c->alpha = n_p ? n_p : 1;
+  c->dnum = (n_q + c->alpha - 1) / c->alpha;
+  for (u32 i = 0; i < n_q; ++i) c->mods.push_back(q_moduli[i]);
+  for (u32 i = 0; i < n_p; ++i) c->mods.push_back(p_moduli[i]);
+  for (u32 i = 0; i < c->nmods; ++i) {
+    u64 q = c->mods[i];
+    if (q <= 2 || q >= (1ull << 62)) {
+      delete c;
+      return fail(HCNN_E_PARAMETER, "modulus outside (2, 2^62)");
+    }
+    for (u32 j = 0; j < i; ++j)
+      if (c->mods[j] == q) {
+        delete c;
+        return fail(HCNN_E_PARAMETER, "moduli must be pairwise distinct");
+      }
+    u64 psi;
+    if (!find_psi(q, n, &psi)) {
+      delete c;
+      return fail(HCNN_E_PARAMETER, "modulus is not 1 mod 2N or has no primitive 2N-th root");
+    }
+    c->psi.push_back(psi);
+  }
+  const size_t N = n;
+  std::vector<u64> tw(c->nmods * N), twp(c->nmods * N), itw(c->nmods * N), itwp(c->nmods * N);
+  std::vector<u64> pf(N), pi(N);
+  for (u32 m = 0; m < c->nmods; ++m) {
+    u64 q = c->mods[m], psi = c->psi[m], psi_inv = h_invmod(psi, q);
+    u64 f = 1, g = 1;
+    for (size_t j = 0; j < N; ++j) {
+      pf[j] = f;
+      pi[j] = g;
+      f = h_mulmod(f, psi, q);
+      g = h_mulmod(g, psi_inv, q);
+    }
+    for (size_t j = 0; j < N; ++j) {
+      u32 b = bitrev((u32)j, c->logN);
+      tw[m * N + j] = pf[b];
+      twp[m * N + j] = h_shoup(pf[b], q);
+      itw[m * N + j] = pi[b];
+      itwp[m * N + j] = h_shoup(pi[b], q);
+    }
+    ModConsts mc{};
+    mc.q = q;
+    u64 x = q;  // q^-1 mod 2^64 by Newton (3 correct bits, doubling)
+    for (int it = 0; it < 6; ++it) x *= 2 - q * x;
+    mc.ninv = (u64)(0 - x);
+    mc.r2 = (u64)(((unsigned __int128)1 << 127) % q);
+    mc.r2 = h_mulmod(mc.r2, 2, q);
+    mc.one_m = h_to_mont(1, q);
+    mc.ninvN = h_invmod(n % q, q);
+    mc.ninvN_sh = h_shoup(mc.ninvN, q);
+    mc.two_q = 2 * q;
+    u64 w1 = itw[m * N + (N > 1 ? 1 : 0)];
+    mc.ilast = h_mulmod(w1, mc.ninvN, q);
+    mc.ilast_sh = h_shoup(mc.ilast, q);
+    c->hmc.push_back(mc);
+  }
+  size_t tb = c->nmods * N * sizeof(u64);
+  CK(cudaMalloc(&c->d_mc, sizeof(ModConsts) * c->nmods));
+  CK(cudaMemcpy(c->d_mc, c->hmc.data(), sizeof(ModConsts) * c->nmods, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&c->d_tw, tb));
+  CK(cudaMalloc(&c->d_twp, tb));
+  CK(cudaMalloc(&c->d_itw, tb));
+  CK(cudaMalloc(&c->d_itwp, tb));
+  CK(cudaMemcpy(c->d_tw, tw.data(), tb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_twp, twp.data(), tb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_itw, itw.data(), tb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_itwp, itwp.data(), tb, cudaMemcpyHostToDevice));
+  // rescale table: q_l^-1 mod q_i
+  std::vector<u64> rinv((size_t)n_q * n_q, 0), rinv_sh((size_t)n_q * n_q, 0);
+  for (u32 l = 1; l < n_q; ++l)
+    for (u32 i = 0; i < l; ++i) {
+      u64 qi = c->mods[i];
+      u64 v = h_invmod(c->mods[l] % qi, qi);
+      rinv[(size_t)l * n_q + i] = v;
+      rinv_sh[(size_t)l * n_q + i] = h_shoup(v, qi);
+    }
+  CK(cudaMalloc(&c->d_rinv, rinv.size() * 8));
+  CK(cudaMalloc(&c->d_rinv_sh, rinv.size() * 8));
+  CK(cudaMemcpy(c->d_rinv, rinv.data(), rinv.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_rinv_sh, rinv_sh.data(), rinv.size() * 8, cudaMemcpyHostToDevice));
+  if (n_p) {
+    // ModDown tables: P -> every q (ckks.py:593-601)
+    std::vector<u32> src, dst, pos;
+    for (u32 k = 0; k < n_p; ++k) src.push_back(n_q + k);
+    for (u32 i = 0; i < n_q; ++i) {
+      dst.push_back(i);
+      pos.push_back(i);
+    }
+    int rc = build_fbc(c, src, dst, pos, &c->moddown);
+    if (rc) return rc;
+    std::vector<u64> pinv(n_q), pinv_sh(n_q);
+    for (u32 i = 0; i < n_q; ++i) {
+      u64 qi = c->mods[i], prod = 1;
+      for (u32 k = 0; k < n_p; ++k) prod = h_mulmod(prod, c->mods[n_q + k] % qi, qi);
+      pinv[i] = h_invmod(prod, qi);
+      pinv_sh[i] = h_shoup(pinv[i], qi);
+    }
+    CK(cudaMalloc(&c->d_pinv, n_q * 8));
+    CK(cudaMalloc(&c->d_pinv_sh, n_q * 8));
+    CK(cudaMemcpy(c->d_pinv, pinv.data(), n_q * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_pinv_sh, pinv_sh.data(), n_q * 8, cudaMemcpyHostToDevice));
+  }
+  CK(ntt_configure_smem());
+  *out = c;
+  return HCNN_OK;
+}
+
+void hcnn_ctx_destroy(hcnn_ctx* c) {
+  if (!c) return;
+  cudaFree(c->d_mc);
+  cudaFree(c->d_tw);
+  cudaFree(c->d_twp);
+  cudaFree(c->d_itw);
+  cudaFree(c->d_itwp);
+  cudaFree(c->d_pinv);
+  cudaFree(c->d_pinv_sh);
+  cudaFree(c->d_rinv);
+  cudaFree(c->d_rinv_sh);
+  cudaFree(c->moddown.mem);
+  for (auto& kv : c->modup) {
+    for (auto& d : kv.second.digits) cudaFree(d.mem);
+    cudaFree(kv.second.d_tabs);
+  }
+  for (auto& kv : c->generic) cudaFree(kv.second.mem);
+  delete c;
+}
+
+int hcnn_ctx_psi(const hcnn_ctx* c, uint32_t i, uint64_t* psi) {
+  if (!c || i >= c->nmods) return fail(HCNN_E_PARAMETER, "bad modulus index");
+  *psi = c->psi[i];
+  return HCNN_OK;
+}
+
+static int check_basis(const hcnn_ctx* c, u32 nq, u32 np) {
+  if (!c) return fail(HCNN_E_PARAMETER, "null context");
+  if (nq > c->Lq || np > c->K) return fail(HCNN_E_BASIS, "basis exceeds the context's chain");
+  if (nq + np == 0) return fail(HCNN_E_BASIS, "empty basis");
+  return HCNN_OK;
+}
+
+#define STREAM(s) ((cudaStream_t)(s))
+
+static int ntt_common(hcnn_ctx* c, uint64_t* data, u32 nq, u32 np, u32 npolys, void* s, bool inv) {
+  int rc = check_basis(c, nq, np);
+  if (rc) return rc;
+  LimbMap m{};
+  m.base = data;
+  m.poly_stride = (size_t)(nq + np) * c->n;
+  m.basis = c->basis(nq, np);
+  CK(launch_ntt(c->tables(), m, nq + np, npolys, inv, STREAM(s)));
+  return HCNN_OK;
+}
+
+int hcnn_ntt_forward(hcnn_ctx* c, uint64_t* data, uint32_t nq, uint32_t np, uint32_t npolys, void* s) {
+  return ntt_common(c, data, nq, np, npolys, s, false);
+}
+int hcnn_ntt_inverse(hcnn_ctx* c, uint64_t* data, uint32_t nq, uint32_t np, uint32_t npolys, void* s) {
+  return ntt_common(c, data, nq, np, npolys, s, true);
+}
+
+static int binop(hcnn_ctx* c, int op, uint64_t* out, const uint64_t* a, const uint64_t* b, u32 nq, u32 np,
+                 u32 npolys, int bc, void* s) {
+  int rc = check_basis(c, nq, np);
+  if (rc) return rc;
+  CK(launch_ew_binary(op, out, a, b, c->basis(nq, np), c->logN, npolys, bc, c->d_mc, STREAM(s)));
+  return HCNN_OK;
+}
+int hcnn_poly_add(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
+                  uint32_t npolys, int bc, void* s) {
+  return binop(c, EW_ADD, out, a, b, nq, np, npolys, bc, s);
+}
+int hcnn_poly_sub(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
+                  uint32_t npolys, int bc, void* s) {
+  return binop(c, EW_SUB, out, a, b, nq, np, npolys, bc, s);
+}
+int hcnn_poly_mul(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
+                  uint32_t npolys, int bc, void* s) {
+  return binop(c, EW_MUL, out, a, b, nq, np, npolys, bc, s);
+}
+int hcnn_poly_mul_mont(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
+                       uint32_t npolys, int bc, void* s) {
+  return binop(c, EW_MUL_MONT, out, a, b, nq, np, npolys, bc, s);
+}
+int hcnn_poly_mac_mont(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
+                       uint32_t npolys, int bc, void* s) {
+  return binop(c, EW_MAC_MONT, out, a, b, nq, np, npolys, bc, s);
+}
+
+static int unop(hcnn_ctx* c, int op, uint64_t* out, const uint64_t* a, u32 nq, u32 np, u32 npolys, void* s) {
+  int rc = check_basis(c, nq, np);
+  if (rc) return rc;
+  CK(launch_ew_unary(op, out, a, c->basis(nq, np), c->logN, npolys, c->d_mc, nullptr, nullptr, STREAM(s)));
+  return HCNN_OK;
+}
+int hcnn_poly_neg(hcnn_ctx* c, uint64_t* out, const uint64_t* a, uint32_t nq, uint32_t np, uint32_t npolys,
+                  void* s) {
+  return unop(c, EW_NEG, out, a, nq, np, npolys, s);
+}
+int hcnn_to_mont(hcnn_ctx* c, uint64_t* out, const uint64_t* a, uint32_t nq, uint32_t np, uint32_t npolys,
+                 void* s) {
+  return unop(c, EW_TO_MONT, out, a, nq, np, npolys, s);
+}
+int hcnn_from_mont(hcnn_ctx* c, uint64_t* out, const uint64_t* a, uint32_t nq, uint32_t np, uint32_t npolys,
+                   void* s) {
+  return unop(c, EW_FROM_MONT, out, a, nq, np, npolys, s);
+}
+
+int hcnn_scalar_mul(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* consts, uint32_t nq,
+                    uint32_t np, uint32_t npolys, void* s) {
+  int rc = check_basis(c, nq, np);
+  if (rc) return rc;
+  Basis b = c->basis(nq, np);
+  u32 nl = nq + np;
+  // constants travel in a small device scratch owned by the context stream-ordered
+  std::vector<u64> h(2 * nl);
+  for (u32 r = 0; r < nl; ++r) {
+    u64 q = c->mods[b.mod_of(r)];
+    h[r] = consts[r] % q;
+    h[nl + r] = h_shoup(h[r], q);
+  }
+  u64* d = nullptr;
+  CK(cudaMallocAsync((void**)&d, 2 * nl * 8, STREAM(s)));
+  CK(cudaMemcpyAsync(d, h.data(), 2 * nl * 8, cudaMemcpyHostToDevice, STREAM(s)));
+  CK(launch_ew_unary(EW_SCALAR, out, a, b, c->logN, npolys, c->d_mc, d, d + nl, STREAM(s)));
+  CK(cudaFreeAsync(d, STREAM(s)));
+  // the host vector must outlive the (pageable, synchronous-to-host) copy
+  return HCNN_OK;
+}
+
+int hcnn_from_signed(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np, uint32_t npolys,
+                     void* s) {
+  int rc = check_basis(c, nq, np);
+  if (rc) return rc;
+  CK(launch_from_signed(out, (const long long*)in, c->basis(nq, np), c->logN, npolys, c->d_mc, STREAM(s)));
+  return HCNN_OK;
+}
+
+int hcnn_automorphism(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint64_t g, int eval_domain, uint32_t nq,
+                      uint32_t np, uint32_t npolys, void* s) {
+  int rc = check_basis(c, nq, np);
+  if (rc) return rc;
+  if ((g & 1) == 0) return fail(HCNN_E_PARAMETER, "automorphism exponent must be odd");
+  g %= 2ull * c->n;
+  CK(launch_automorph(eval_domain, out, in, c->basis(nq, np), c->logN, npolys, g, c->d_mc, STREAM(s)));
+  return HCNN_OK;
+}
+
+int hcnn_base_convert(hcnn_ctx* c, uint64_t* out, const uint64_t* in, const uint32_t* src_mods, uint32_t n_src,
+                      const uint32_t* dst_mods, uint32_t n_dst, uint32_t npolys, void* s) {
+  if (!c) return fail(HCNN_E_PARAMETER, "null context");
+  if (n_src == 0 || n_dst == 0) return fail(HCNN_E_BASIS, "empty basis");
+  if (n_src > 64) return fail(HCNN_E_BASIS, "at most 64 source limbs");
+  std::vector<u32> key;
+  key.push_back(n_src);
+  for (u32 i = 0; i < n_src; ++i) {
+    if (src_mods[i] >= c->nmods) return fail(HCNN_E_BASIS, "bad source modulus index");
+    key.push_back(src_mods[i]);
+  }
+  for (u32 i = 0; i < n_dst; ++i) {
+    if (dst_mods[i] >= c->nmods) return fail(HCNN_E_BASIS, "bad target modulus index");
+    key.push_back(dst_mods[i]);
+  }
+  FbcStore* st;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    auto it = c->generic.find(key);
+    if (it == c->generic.end()) {
+      std::vector<u32> src(src_mods, src_mods + n_src), dst(dst_mods, dst_mods + n_dst), pos(n_dst);
+      for (u32 i = 0; i < n_dst; ++i) pos[i] = i;
+      FbcStore fs;
+      int rc = build_fbc(c, src, dst, pos, &fs);
+      if (rc) return rc;
+      it = c->generic.emplace(key, fs).first;
+    }
+    st = &it->second;
+  }
+  CK(launch_fbc(st->dev, c->d_mc, in, (size_t)n_src * c->n, out, (size_t)n_dst * c->n, c->logN, npolys, n_dst,
+                STREAM(s)));
+  return HCNN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// key switching
+// workspace: xc [nq] | raised [d][n_ext] | acc [2][n_ext] | lift [2][nq]  (limbs of N u64)
+// ---------------------------------------------------------------------------
+struct KsWs {
+  u64 *xc, *raised, *acc, *lift;
+};
+static KsWs ks_layout(const hcnn_ctx* c, u32 level, void* ws) {
+  const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
+  const size_t N = c->n;
+  KsWs w;
+  w.xc = (u64*)ws;
+  w.raised = w.xc + nq * N;
+  w.acc = w.raised + (size_t)nd * n_ext * N;
+  w.lift = w.acc + 2 * (size_t)n_ext * N;
+  return w;
+}
+
+size_t hcnn_ks_workspace_bytes(const hcnn_ctx* c, uint32_t level) {
+  const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
+  return ((size_t)nq + (size_t)nd * n_ext + 2 * (size_t)n_ext + 2 * (size_t)nq) * c->n * 8;
+}
+
+// ModUp: iNTT a copy of x, convert every digit to Q_l||P, NTT the new limbs
+static int ks_modup(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, cudaStream_t st) {
+  const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
+  const size_t N = c->n;
+  ModupSet* mu;
+  int rc = get_modup(c, level, &mu);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(w.xc, x_eval, nq * N * 8, cudaMemcpyDeviceToDevice, st));
+  LimbMap m{};
+  m.base = w.xc;
+  m.poly_stride = nq * N;
+  m.basis = c->basis(nq, 0);
+  CK(launch_ntt(c->tables(), m, nq, 1, true, st));
+  CK(launch_modup(mu->d_tabs, nd, c->d_mc, w.xc, w.raised, c->alpha, n_ext, c->logN, st));
+  LimbMap r{};
+  r.base = w.raised;
+  r.poly_stride = (size_t)n_ext * N;
+  r.basis = c->basis(nq, c->K);
+  r.skip_alpha = c->alpha;
+  CK(launch_ntt(c->tables(), r, n_ext, nd, false, st));
+  return HCNN_OK;
+}
+
+// inner product with one key (optionally Galois-permuted) + ModDown + combine
+static int ks_finish(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, u64 g, const u64* kb,
+                     const u64* ka, u64* out0, u64* out1, const u64* add0, const u64* add1, u64 g_add,
+                     cudaStream_t st) {
+  const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
+  const size_t N = c->n;
+  CK(launch_ks_inner(w.acc, x_eval, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, g, c->d_mc, st));
+  LimbMap m{};
+  m.base = w.acc + nq * N;
+  m.poly_stride = (size_t)n_ext * N;
+  m.basis = c->basis(nq, c->K);
+  m.first_limb = nq;
+  CK(launch_ntt(c->tables(), m, c->K, 2, true, st));
+  CK(launch_fbc(c->moddown.dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N, c->logN, 2, nq, st));
+  LimbMap l{};
+  l.base = w.lift;
+  l.poly_stride = nq * N;
+  l.basis = c->basis(nq, 0);
+  CK(launch_ntt(c->tables(), l, nq, 2, false, st));
+  CK(launch_moddown_combine(out0, out1, w.acc, w.lift, add0, add1, g_add, nq, n_ext, c->logN, c->d_pinv,
+                            c->d_pinv_sh, c->d_mc, st));
+  return HCNN_OK;
+}
+
+static int check_level(const hcnn_ctx* c, u32 level) {
+  if (!c) return fail(HCNN_E_PARAMETER, "null context");
+  if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
+  if (c->K == 0) return fail(HCNN_E_KEY, "no special primes: key switching unavailable");
+  return HCNN_OK;
+}
+
+int hcnn_keyswitch(hcnn_ctx* c, uint64_t* out0, uint64_t* out1, const uint64_t* x_eval, uint32_t level,
+                   const uint64_t* kb, const uint64_t* ka, void* ws, void* s) {
+  int rc = check_level(c, level);
+  if (rc) return rc;
+  KsWs w = ks_layout(c, level, ws);
+  rc = ks_modup(c, level, x_eval, w, STREAM(s));
+  if (rc) return rc;
+  return ks_finish(c, level, x_eval, w, 1, kb, ka, out0, out1, nullptr, nullptr, 1, STREAM(s));
+}
+
+int hcnn_hmult(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t level,
+               const uint64_t* kb, const uint64_t* ka, void* ws, void* s) {
+  int rc = check_level(c, level);
+  if (rc) return rc;
+  const u32 nq = level + 1;
+  const size_t N = c->n;
+  KsWs w = ks_layout(c, level, ws);
+  u64* d2 = w.lift;  // parked in the ModDown scratch until the inner product
+  CK(launch_tensor(out, out + nq * N, d2, a, b, nq, c->logN, c->d_mc, STREAM(s)));
+  rc = ks_modup(c, level, d2, w, STREAM(s));
+  if (rc) return rc;
+  return ks_finish(c, level, d2, w, 1, kb, ka, out, out + nq * N, out, out + nq * N, 1, STREAM(s));
+}
+
+int hcnn_rotate_hoisted(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* ct, uint32_t level, uint32_t n_rot,
+                        const uint64_t* galois, const uint64_t* const* kbs, const uint64_t* const* kas, void* ws,
+                        void* s) {
+  int rc = check_level(c, level);
+  if (rc) return rc;
+  const u32 nq = level + 1;
+  const size_t N = c->n;
+  KsWs w = ks_layout(c, level, ws);
+  const u64* c1 = ct + nq * N;
+  rc = ks_modup(c, level, c1, w, STREAM(s));
+  if (rc) return rc;
+  for (u32 i = 0; i < n_rot; ++i) {
+    u64 g = galois[i] % (2ull * c->n);
+    if ((g & 1) == 0) return fail(HCNN_E_PARAMETER, "galois element must be odd");
+    rc = ks_finish(c, level, c1, w, g, kbs[i], kas[i], outs[i], outs[i] + nq * N, ct, nullptr, g, STREAM(s));
+    if (rc) return rc;
+  }
+  return HCNN_OK;
+}
+
+size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* c, uint32_t npolys) { return (size_t)npolys * c->n * 8; }
+
+int hcnn_rescale(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint32_t level, uint32_t npolys, void* ws,
+                 void* s) {
+  if (!c) return fail(HCNN_E_PARAMETER, "null context");
+  if (level == 0) return fail(HCNN_E_LEVEL, "no limb left to rescale away");
+  if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
+  const u32 l = level;
+  u64* top = (u64*)ws;
+  CK(launch_gather_limb(top, in, l, l + 1, c->logN, npolys, STREAM(s)));
+  LimbMap m{};
+  m.base = top;
+  m.poly_stride = c->n;
+  m.basis = c->basis(l + 1, 0);
+  m.first_limb = l;
+  CK(launch_ntt(c->tables(), m, 1, npolys, true, STREAM(s)));
+  CK(launch_rescale_lift(out, top, l, c->logN, npolys, c->d_mc, STREAM(s)));
+  LimbMap o{};
+  o.base = out;
+  o.poly_stride = (size_t)l * c->n;
+  o.basis = c->basis(l, 0);
+  CK(launch_ntt(c->tables(), o, l, npolys, false, STREAM(s)));
+  CK(launch_rescale_combine(out, in, l, c->logN, npolys, c->d_rinv + (size_t)l * c->Lq,
+                            c->d_rinv_sh + (size_t)l * c->Lq, c->d_mc, STREAM(s)));
+  return HCNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// Kernel-level interfaces shared between the .cu translation units.
+#pragma once
+#include "common.cuh"
+
+namespace hcnn {
+
+// A batch of polynomials over one basis: poly z, limb r lives at
+// base + z*poly_stride + r*N.  skip_alpha != 0 marks the key-switch ModUp
+// layout: poly z is digit z and its own limbs [z*alpha, min(z*alpha+alpha, nq))
+// are left untouched (they are taken from the eval-domain input instead).
+struct LimbMap {
+  u64* base;          // address of (poly 0, limb first_limb)
+  size_t poly_stride;
+  Basis basis;
+  u32 skip_alpha;
+  u32 first_limb;     // basis position of the first processed limb
+};
+
+struct NttTables {
+  u32 logN;
+  const ModConsts* mc;
+  const u64* tw;    // [mod][N] psi^brv(j)
+  const u64* twp;   // Shoup companions
+  const u64* itw;   // [mod][N] psi^-brv(j)
+  const u64* itwp;
+};
+
+void ntt_split(u32 logN, u32* logN1);
+cudaError_t launch_ntt(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 npolys, bool inverse,
+                       cudaStream_t st);
+cudaError_t ntt_configure_smem();
+
+// --------------------------------------------------------------------------
+// fast base conversion tables (ring.py:343-375): for one source set and a
+// set of target moduli.
+//   y_i = x_i * (Q/q_i)^-1 mod q_i  (inv_punc, Shoup form with companion)
+//   out_t = sum_i [y_i]_centred * (Q/q_i mod t)   (tmat Montgomery form)
+// --------------------------------------------------------------------------
+struct FbcDev {
+  u32 ns, nt;
+  const u32* src_mod;     // [ns] modulus index of each source limb
+  const u32* dst_mod;     // [nt] modulus index of each target limb
+  const u32* dst_pos;     // [nt] output limb position of each target
+  const u64* inv_punc;    // [ns]
+  const u64* inv_punc_sh; // [ns]
+  const u64* tmat;        // [nt][ns] Montgomery form of (Q/q_i) mod t
+};
+
+}  // namespace hcnn

@@ -1,0 +1,241 @@
+"""Device context: one CkksParams (or one bare modulus chain) resident in HBM.
+
+Thin host wrapper over the C ABI.  Residue tensors are torch int64 tensors
+on the CUDA device holding the uint64 bit patterns, shaped [npolys, nlimbs, N]
+(or [nlimbs, N] for a single polynomial), limb-major exactly like
+RnsPoly.coeffs in the reference (ring.py:204-213).  Everything is enqueued on
+torch's current CUDA stream; torch's caching allocator provides outputs and
+scratch, so calls allocate nothing from the driver in steady state.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import BasisError, NativeError
+
+_ctx_cache: dict[tuple, "DeviceContext"] = {}
+_ctx_lock = threading.Lock()
+
+
+def _require_cuda(device: int) -> None:
+    if not torch.cuda.is_available():
+        raise NativeError("no CUDA device visible: the hcnn-b200 engine has no CPU fallback")
+
+
+def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(0)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def to_device_u64(arr: np.ndarray, device: int | torch.device = 0) -> torch.Tensor:
+    """uint64 numpy array -> int64 CUDA tensor with the same bits."""
+    a = np.ascontiguousarray(arr, dtype=np.uint64)
+    return torch.from_numpy(a.view(np.int64)).to(device=f"cuda:{device}" if isinstance(device, int) else device)
+
+
+def to_host_u64(t: torch.Tensor) -> np.ndarray:
+    """int64 CUDA tensor -> uint64 numpy array (synchronising copy)."""
+    return t.detach().to("cpu").contiguous().numpy().view(np.uint64)
+
+
+class DeviceContext:
+    """An hcnn_ctx: moduli constants, twiddles (reference psi) and the
+    lazily built base-conversion tables for one ring degree and chain."""
+
+    def __init__(self, n: int, q_list: Sequence[int], p_list: Sequence[int] = (), device: int = 0):
+        _require_cuda(device)
+        self.lib = _native.load()
+        self.n = int(n)
+        self.logn = self.n.bit_length() - 1
+        self.q_list = tuple(int(q) for q in q_list)
+        self.p_list = tuple(int(p) for p in p_list)
+        self.Lq = len(self.q_list)
+        self.K = len(self.p_list)
+        self.device = device
+        self.torch_device = torch.device(f"cuda:{device}")
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _native.check(self.lib.hcnn_ctx_create(
+                ctypes.byref(h), device, self.n,
+                _native.u64_array(self.q_list), self.Lq,
+                _native.u64_array(self.p_list) if self.p_list else None, self.K))
+        self.handle = h
+        self.launches = 0
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and self.handle.value:
+                self.lib.hcnn_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+    # -- helpers -----------------------------------------------------------
+    def empty(self, *shape) -> torch.Tensor:
+        return torch.empty(shape, dtype=torch.int64, device=self.torch_device)
+
+    def zeros(self, *shape) -> torch.Tensor:
+        return torch.zeros(shape, dtype=torch.int64, device=self.torch_device)
+
+    def psi(self, mod_index: int) -> int:
+        v = ctypes.c_uint64()
+        _native.check(self.lib.hcnn_ctx_psi(self.handle, mod_index, ctypes.byref(v)))
+        return int(v.value)
+
+    def _chk(self, rc: int) -> None:
+        self.launches += 1
+        _native.check(rc)
+
+    @staticmethod
+    def _npolys(t: torch.Tensor, nq: int, np_: int, n: int) -> int:
+        nl = nq + np_
+        total = t.numel()
+        if total % (nl * n):
+            raise BasisError(f"tensor of {total} residues is not a batch over {nl} limbs of {n}")
+        if not t.is_contiguous():
+            raise BasisError("residue tensors must be contiguous")
+        return total // (nl * n)
+
+    # -- ring.py level ops ----------------------------------------------------
+    def ntt(self, t: torch.Tensor, nq: int, np_: int = 0, inverse: bool = False) -> torch.Tensor:
+        """In-place forward (coeff->eval) or inverse NTT of every limb."""
+        npolys = self._npolys(t, nq, np_, self.n)
+        fn = self.lib.hcnn_ntt_inverse if inverse else self.lib.hcnn_ntt_forward
+        self._chk(fn(self.handle, _ptr(t), nq, np_, npolys, _stream()))
+        return t
+
+    def binop(self, op: str, a: torch.Tensor, b: torch.Tensor, nq: int, np_: int = 0,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+        npolys = self._npolys(a, nq, np_, self.n)
+        nb = self._npolys(b, nq, np_, self.n)
+        bcast = 1 if (nb == 1 and npolys > 1) else 0
+        if not bcast and nb != npolys:
+            raise BasisError("operand batch sizes differ")
+        if out is None:
+            out = torch.empty_like(a)
+        fn = {
+            "add": self.lib.hcnn_poly_add,
+            "sub": self.lib.hcnn_poly_sub,
+            "mul": self.lib.hcnn_poly_mul,
+            "mul_mont": self.lib.hcnn_poly_mul_mont,
+            "mac_mont": self.lib.hcnn_poly_mac_mont,
+        }[op]
+        self._chk(fn(self.handle, _ptr(out), _ptr(a), _ptr(b), nq, np_, npolys, bcast, _stream()))
+        return out
+
+    def unop(self, op: str, a: torch.Tensor, nq: int, np_: int = 0,
+             out: torch.Tensor | None = None) -> torch.Tensor:
+        npolys = self._npolys(a, nq, np_, self.n)
+        if out is None:
+            out = torch.empty_like(a)
+        fn = {
+            "neg": self.lib.hcnn_poly_neg,
+            "to_mont": self.lib.hcnn_to_mont,
+            "from_mont": self.lib.hcnn_from_mont,
+        }[op]
+        self._chk(fn(self.handle, _ptr(out), _ptr(a), nq, np_, npolys, _stream()))
+        return out
+
+    def scalar_mul(self, a: torch.Tensor, consts: Sequence[int], nq: int, np_: int = 0,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
+        npolys = self._npolys(a, nq, np_, self.n)
+        if len(consts) != nq + np_:
+            raise BasisError("one constant per limb required")
+        if out is None:
+            out = torch.empty_like(a)
+        self._chk(self.lib.hcnn_scalar_mul(self.handle, _ptr(out), _ptr(a), _native.u64_array(consts),
+                                           nq, np_, npolys, _stream()))
+        return out
+
+    def from_signed(self, rows: torch.Tensor, nq: int, np_: int = 0) -> torch.Tensor:
+        """int64 rows [npolys, N] -> residues [npolys, nlimbs, N]."""
+        rows = rows.contiguous()
+        npolys = rows.numel() // self.n
+        out = self.empty(npolys, nq + np_, self.n)
+        self._chk(self.lib.hcnn_from_signed(self.handle, _ptr(out), _ptr(rows), nq, np_, npolys, _stream()))
+        return out
+
+    def automorphism(self, a: torch.Tensor, g: int, nq: int, np_: int = 0, eval_domain: bool = True,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+        npolys = self._npolys(a, nq, np_, self.n)
+        if out is None:
+            out = torch.empty_like(a)
+        self._chk(self.lib.hcnn_automorphism(self.handle, _ptr(out), _ptr(a), int(g), 1 if eval_domain else 0,
+                                             nq, np_, npolys, _stream()))
+        return out
+
+    def base_convert(self, a: torch.Tensor, src_mods: Sequence[int], dst_mods: Sequence[int]) -> torch.Tensor:
+        """Centred FBC between arbitrary modulus-index lists (coefficient domain)."""
+        ns, nt = len(src_mods), len(dst_mods)
+        npolys = a.numel() // (ns * self.n)
+        out = self.empty(npolys, nt, self.n)
+        self._chk(self.lib.hcnn_base_convert(self.handle, _ptr(out), _ptr(a.contiguous()),
+                                             _native.u32_array(src_mods), ns, _native.u32_array(dst_mods), nt,
+                                             npolys, _stream()))
+        return out
+
+    # -- ckks.py level ops ----------------------------------------------------
+    def ks_workspace(self, level: int) -> torch.Tensor:
+        nbytes = int(self.lib.hcnn_ks_workspace_bytes(self.handle, level))
+        return self.empty(nbytes // 8)
+
+    def keyswitch(self, x_eval: torch.Tensor, level: int, key_b: torch.Tensor, key_a: torch.Tensor):
+        out = self.empty(2, level + 1, self.n)
+        ws = self.ks_workspace(level)
+        self._chk(self.lib.hcnn_keyswitch(self.handle, _ptr(out[0]), _ptr(out[1]), _ptr(x_eval), level,
+                                          _ptr(key_b), _ptr(key_a), _ptr(ws), _stream()))
+        return out
+
+    def hmult(self, a: torch.Tensor, b: torch.Tensor, level: int, key_b: torch.Tensor,
+              key_a: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        if out is None:
+            out = self.empty(2, level + 1, self.n)
+        ws = self.ks_workspace(level)
+        self._chk(self.lib.hcnn_hmult(self.handle, _ptr(out), _ptr(a), _ptr(b), level, _ptr(key_b),
+                                      _ptr(key_a), _ptr(ws), _stream()))
+        return out
+
+    def rotate_hoisted(self, ct: torch.Tensor, level: int, galois: Sequence[int],
+                       keys: Sequence[tuple[torch.Tensor, torch.Tensor]]) -> list[torch.Tensor]:
+        n_rot = len(galois)
+        outs = [self.empty(2, level + 1, self.n) for _ in range(n_rot)]
+        if n_rot == 0:
+            return outs
+        ws = self.ks_workspace(level)
+        P = ctypes.c_void_p * n_rot
+        outs_p = P(*[o.data_ptr() for o in outs])
+        kb = P(*[k[0].data_ptr() for k in keys])
+        ka = P(*[k[1].data_ptr() for k in keys])
+        self._chk(self.lib.hcnn_rotate_hoisted(self.handle, outs_p, _ptr(ct), level, n_rot,
+                                               _native.u64_array(galois), kb, ka, _ptr(ws), _stream()))
+        return outs
+
+    def rescale(self, a: torch.Tensor, level: int) -> torch.Tensor:
+        npolys = self._npolys(a, level + 1, 0, self.n)
+        out = self.empty(npolys, level, self.n)
+        ws = self.empty(npolys * self.n)
+        self._chk(self.lib.hcnn_rescale(self.handle, _ptr(out), _ptr(a), level, npolys, _ptr(ws), _stream()))
+        return out
+
+
+def context_for(n: int, q_list: Sequence[int], p_list: Sequence[int] = (), device: int = 0) -> DeviceContext:
+    key = (int(n), tuple(int(q) for q in q_list), tuple(int(p) for p in p_list), device)
+    ctx = _ctx_cache.get(key)
+    if ctx is None:
+        with _ctx_lock:
+            ctx = _ctx_cache.get(key)
+            if ctx is None:
+                ctx = DeviceContext(n, key[1], key[2], device)
+                _ctx_cache[key] = ctx
+    return ctx

@@ -1,0 +1,252 @@
+"""Generate the committed golden fixtures from the UNMODIFIED reference.
+
+Runs only in the build container, where /root/reference exists:
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py [small|deskA|bench16|layers ...]
+
+Outputs (all small enough to commit):
+  golden_small.npz      full residue arrays at a 256-ring (the reference's
+                        own small_setup params, test_ckks.py:46-52)
+  golden_hashes.json    sha256 of residue arrays at desk-A (cfg 1) and at
+                        N=2^16 (cfg 2, CkksParams.build("bench16",...)),
+                        plus layer-level outputs (conv / basic block /
+                        tiny-cnn) with their decrypted values
+A hash is sha256 over the C-contiguous little-endian uint64 bytes.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+os.environ.setdefault("HCNN_TEST_MODE", "1")
+sys.setrecursionlimit(10000)
+
+from hcnn import ckks, graph, packing, ring  # noqa: E402  (reference package)
+
+HERE = Path(__file__).resolve().parent
+
+
+def h(arr) -> str:
+    import hashlib
+    a = np.ascontiguousarray(np.asarray(arr, dtype=np.uint64))
+    return hashlib.sha256(a.astype("<u8").tobytes()).hexdigest()
+
+
+def ct_arr(ct) -> np.ndarray:
+    return np.stack([ct.c0.coeffs, ct.c1.coeffs])
+
+
+def key_arr(k) -> tuple[np.ndarray, np.ndarray]:
+    return np.stack(k.rows_b), np.stack(k.rows_a)
+
+
+def load_json():
+    p = HERE / "golden_hashes.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
+def save_json(obj):
+    (HERE / "golden_hashes.json").write_text(json.dumps(obj, indent=1, sort_keys=True) + "\n")
+
+
+def meta():
+    return {"numpy": np.__version__, "reference": "hcnn 0.1.0 @ /root/reference/pkg"}
+
+
+# ---------------------------------------------------------------------------
+def gen_small():
+    params = ckks.CkksParams.build("unit-small", 256, 50, 40, 4, 50, 2)
+    ext = params.q_mods + params.p_mods
+    out = {"q": np.array([m.q for m in params.q_mods], np.uint64),
+           "p": np.array([m.q for m in params.p_mods], np.uint64),
+           "psi": np.array([ring.get_twiddles(m, params.n).psi for m in ext], np.uint64)}
+    rng = np.random.default_rng(0)
+    coeff = np.stack([rng.integers(0, m.q, size=params.n, dtype=np.uint64) for m in ext])
+    p = ring.RnsPoly(ext, coeff.copy(), ring.Domain.COEFF)
+    out["ntt_in"] = coeff
+    out["ntt_out"] = ring.ntt_forward(p).coeffs
+    # base conversion q0..q2 -> specials + q3
+    src = params.q_mods[:3]
+    dst = params.p_mods + params.q_mods[3:4]
+    bc_in = ring.RnsPoly(src, coeff[:3].copy(), ring.Domain.COEFF)
+    out["bc_out"] = ring.base_convert(bc_in, dst).coeffs
+    # coefficient-domain automorphism
+    out["auto5"] = ring.automorphism(p, 5).coeffs
+    out["auto_g"] = ring.automorphism(p, ckks.galois_element(3, params.n)).coeffs
+
+    ks = ckks.keygen(params, np.random.default_rng(3), rotations=[1, 2, 4])
+    out["sk"] = ks.sk.coeffs
+    out["pk_b"], out["pk_a"] = ks.pk[0].coeffs, ks.pk[1].coeffs
+    out["rlk_b"], out["rlk_a"] = key_arr(ks.rlk)
+    for s in (1, 2, 4):
+        out[f"gk{s}_b"], out[f"gk{s}_a"] = key_arr(ks.gks[s])
+    vrng = np.random.default_rng(12345)
+    v1 = vrng.uniform(-1, 1, params.slots)
+    v2 = vrng.uniform(-1, 1, params.slots)
+    L = params.max_level
+    pt1 = ckks.encode(v1, params, L)
+    out["v1"], out["v2"] = v1, v2
+    out["pt1"] = pt1.poly.coeffs
+    ct1 = ckks.encrypt(pt1, ks, np.random.default_rng(77))
+    ct2 = ckks.encrypt(ckks.encode(v2, params, L), ks, np.random.default_rng(78))
+    out["ct1"], out["ct2"] = ct_arr(ct1), ct_arr(ct2)
+    hm = ckks.hmult(ct1, ct2, ks)
+    out["hmult"] = ct_arr(hm)
+    out["rescale"] = ct_arr(ckks.rescale(hm, params))
+    for k in (1, 3, -1, 4):
+        out[f"rot{k}"] = ct_arr(ckks.rotate(ct1, k, ks))
+    out["dec_hmult"] = ckks.decode(ckks.decrypt(ckks.rescale(hm, params), ks), params)
+    out["pmult"] = ct_arr(ckks.pmult(ct1, pt1))
+    out["hadd"] = ct_arr(ckks.hadd(ct1, ct2))
+    out["padd"] = ct_arr(ckks.padd(ct1, pt1))
+    np.savez_compressed(HERE / "golden_small.npz", **out)
+    print("small done")
+
+
+# ---------------------------------------------------------------------------
+def scheme_hashes(params, key_seed, rotations, rot_tests, tag):
+    t0 = time.time()
+    ks = ckks.keygen(params, np.random.default_rng(key_seed), rotations=rotations)
+    t_key = time.time() - t0
+    res = {"params": {"n": params.n, "q": [m.q for m in params.q_mods], "p": [m.q for m in params.p_mods]},
+           "key_seed": key_seed, "rotations": list(rotations)}
+    res["sk"] = h(ks.sk.coeffs)
+    res["pk"] = h(np.stack([ks.pk[0].coeffs, ks.pk[1].coeffs]))
+    b, a = key_arr(ks.rlk)
+    res["rlk"] = h(np.stack([b, a]))
+    res["gks"] = {}
+    for s in sorted(ks.gks):
+        b, a = key_arr(ks.gks[s])
+        res["gks"][str(s)] = h(np.stack([b, a]))
+    vrng = np.random.default_rng(12345)
+    v1 = vrng.uniform(-1, 1, params.slots)
+    v2 = vrng.uniform(-1, 1, params.slots)
+    L = params.max_level
+    pt1 = ckks.encode(v1, params, L)
+    res["pt1"] = h(pt1.poly.coeffs)
+    ct1 = ckks.encrypt(pt1, ks, np.random.default_rng(77))
+    ct2 = ckks.encrypt(ckks.encode(v2, params, L), ks, np.random.default_rng(78))
+    res["ct1"], res["ct2"] = h(ct_arr(ct1)), h(ct_arr(ct2))
+    coeff_rng = np.random.default_rng(0)
+    ext = params.q_mods + params.p_mods
+    coeff = np.stack([coeff_rng.integers(0, m.q, size=params.n, dtype=np.uint64) for m in ext])
+    res["ntt_in_seed0"] = h(coeff)
+    res["ntt_out_seed0"] = h(ring.ntt_forward(ring.RnsPoly(ext, coeff, ring.Domain.COEFF)).coeffs)
+    t0 = time.time()
+    hm = ckks.hmult(ct1, ct2, ks)
+    t_hm = time.time() - t0
+    res["hmult"] = h(ct_arr(hm))
+    t0 = time.time()
+    rs = ckks.rescale(hm, params)
+    t_rs = time.time() - t0
+    res["rescale"] = h(ct_arr(rs))
+    dec = ckks.decode(ckks.decrypt(rs, ks), params)
+    res["dec_hmult_err"] = float(np.max(np.abs(dec - v1 * v2)))
+    res["dec_hmult_head"] = [float(x) for x in dec[:8]]
+    res["rot"] = {}
+    t_rot = None
+    for k in rot_tests:
+        t0 = time.time()
+        r = ckks.rotate(ct1, k, ks)
+        if t_rot is None:
+            t_rot = time.time() - t0
+        res["rot"][str(k)] = h(ct_arr(r))
+    res["ref_cpu_seconds"] = {"keygen": t_key, "hmult": t_hm, "rescale": t_rs, "rotate_first": t_rot}
+    res["meta"] = meta()
+    print(tag, "done", res["ref_cpu_seconds"])
+    return res
+
+
+def gen_deska():
+    obj = load_json()
+    obj["deskA"] = scheme_hashes(ckks.desk_a(), 0xA11CE, [1 << i for i in range(12)], [1, 5, -1, 2048], "deskA")
+    save_json(obj)
+
+
+def gen_bench16():
+    obj = load_json()
+    p = ckks.CkksParams.build("bench16", 1 << 16, 59, 40, 24, 59, 4)
+    obj["bench16"] = scheme_hashes(p, 1, [1, 4], [1, 5], "bench16")
+    save_json(obj)
+
+
+# ---------------------------------------------------------------------------
+def gen_layers():
+    """Layer-level goldens: the acceptance suite's desk-A basic block (gate 4
+    setup, test_acceptance.py:73-93, 282-309) and one desk-B tiny-cnn
+    inference (gate 7 setup, test_acceptance.py:96-105, 415-449)."""
+    obj = load_json()
+    res = {}
+    params = ckks.desk_a()
+    stack_fx = graph.gen_fixture("basic-block-stack(1)", 21, params)
+    stack_g = graph.build_graph("basic-block-stack(1)", stack_fx, multiplex=8)
+    steps = sorted(graph.required_rotation_steps(stack_g, params.slots))
+    t0 = time.time()
+    ks = ckks.keygen(params, np.random.default_rng(0xACCE), rotations=steps)
+    plan = graph.plan_levels(stack_g, params.max_level)
+    x = np.asarray(stack_fx["golden"][0]["input"])
+    packed = packing.encrypt_tensor(x, stack_g.input_format, ks, np.random.default_rng(0xACC4),
+                                    plan.entry_levels[0])
+    t1 = time.time()
+    out, rep = graph.execute(stack_g, plan, packed, ks, "encrypted")
+    t_exec = time.time() - t1
+    dec = packing.decrypt_tensor(out, ks)
+    ref, _ = graph.execute(stack_g, plan, x, mode="plaintext-ref")
+    res["block"] = {
+        "steps": steps, "key_seed": 0xACCE, "enc_seed": 0xACC4,
+        "input": h(np.stack([ct_arr(c) for c in packed.cts])),
+        "output": h(np.stack([ct_arr(c) for c in out.cts])),
+        "entries": [r["entry_level"] for r in rep.per_layer],
+        "tally": rep.totals().as_dict(),
+        "per_layer_out": [],
+        "dec_max_err_vs_plain": float(np.max(np.abs(dec - ref))),
+        "dec_head": [float(v) for v in dec.ravel()[:16]],
+        "ref_cpu_seconds": t_exec,
+    }
+    # first conv alone
+    layer = stack_g.layers[0]
+    conv_out = packing.conv2d(packed, layer.spec, ks, None, {}, tag=layer.name)
+    res["block"]["conv1_out"] = h(np.stack([ct_arr(c) for c in conv_out.cts]))
+    print("block done", time.time() - t0)
+
+    # tiny-cnn at desk-B, one inference
+    params = ckks.desk_b()
+    fx = graph.gen_fixture("tiny-cnn", 42, params)
+    g = graph.build_graph("tiny-cnn", fx, multiplex=8)
+    plan = graph.plan_levels(g, params.max_level)
+    steps = sorted(graph.required_rotation_steps(g, params.slots))
+    ks = ckks.keygen(params, np.random.default_rng(0xB0B), rotations=steps)
+    rng = np.random.default_rng(0xACC7)
+    x = rng.uniform(-1.0, 1.0, (1, 8, 8))
+    packed = packing.encrypt_tensor(x, g.input_format, ks, rng, plan.entry_levels[0])
+    t1 = time.time()
+    out, rep = graph.execute(g, plan, packed, ks, "encrypted", cache={})
+    t_exec = time.time() - t1
+    logits = packing.read_logits(out, g.n_classes, g.formats[-1], ks)
+    ref, _ = graph.execute(g, plan, x, mode="plaintext-ref")
+    res["tiny"] = {
+        "steps": steps, "key_seed": 0xB0B, "input_seed": 0xACC7,
+        "plan": plan.as_dict(),
+        "output": h(ct_arr(out)),
+        "logits": [float(v) for v in logits],
+        "plain_logits": [float(v) for v in ref],
+        "tally": rep.totals().as_dict(),
+        "ref_cpu_seconds": t_exec,
+    }
+    res["meta"] = meta()
+    obj["layers"] = res
+    save_json(obj)
+    print("tiny done", time.time() - t0)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["small", "deskA", "bench16", "layers"]
+    for w in which:
+        {"small": gen_small, "deskA": gen_deska, "bench16": gen_bench16, "layers": gen_layers}[w]()

@@ -1,0 +1,141 @@
+"""Bit-exact parity of the CUDA engine against full residue arrays frozen
+from the unmodified reference at a 256-ring (tests/golden/make_golden.py,
+gen_small).  Every integer output must match with np.array_equal."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def small(golden_small):
+    from paper_2310_16530_b200 import ckks
+    params = ckks.CkksParams.build("unit-small", 256, 50, 40, 4, 50, 2)
+    assert [m.q for m in params.q_mods] == golden_small["q"].tolist()
+    assert [m.q for m in params.p_mods] == golden_small["p"].tolist()
+    ks = ckks.keygen(params, np.random.default_rng(3), rotations=[1, 2, 4])
+    return params, ks
+
+
+def _ct(ct):
+    c0, c1 = ct.host_residues()
+    return np.stack([c0, c1])
+
+
+def test_psi_matches_reference(small, golden_small):
+    params, _ = small
+    ctx = params.ctx
+    got = [ctx.psi(i) for i in range(ctx.Lq + ctx.K)]
+    assert got == golden_small["psi"].tolist()
+
+
+def test_ntt_forward_inverse(small, golden_small):
+    from paper_2310_16530_b200 import ring
+    params, _ = small
+    ext = params.q_mods + params.p_mods
+    p = ring.RnsPoly(ext, golden_small["ntt_in"].copy(), ring.Domain.COEFF, params.ctx)
+    f = ring.ntt_forward(p)
+    assert np.array_equal(f.coeffs, golden_small["ntt_out"])
+    back = ring.ntt_inverse(f)
+    assert np.array_equal(back.coeffs, golden_small["ntt_in"])
+
+
+def test_base_convert(small, golden_small):
+    from paper_2310_16530_b200 import ring
+    params, _ = small
+    src = params.q_mods[:3]
+    dst = params.p_mods + params.q_mods[3:4]
+    p = ring.RnsPoly(src, golden_small["ntt_in"][:3].copy(), ring.Domain.COEFF, params.ctx)
+    assert np.array_equal(ring.base_convert(p, dst).coeffs, golden_small["bc_out"])
+
+
+def test_automorphism_coeff(small, golden_small):
+    from paper_2310_16530_b200 import ckks, ring
+    params, _ = small
+    ext = params.q_mods + params.p_mods
+    p = ring.RnsPoly(ext, golden_small["ntt_in"].copy(), ring.Domain.COEFF, params.ctx)
+    assert np.array_equal(ring.automorphism(p, 5).coeffs, golden_small["auto5"])
+    g = ckks.galois_element(3, params.n)
+    assert np.array_equal(ring.automorphism(p, g).coeffs, golden_small["auto_g"])
+
+
+def test_automorphism_eval_is_permutation(small, golden_small):
+    from paper_2310_16530_b200 import ckks, ring
+    params, _ = small
+    ext = params.q_mods + params.p_mods
+    p = ring.RnsPoly(ext, golden_small["ntt_in"].copy(), ring.Domain.COEFF, params.ctx)
+    for g in (5, ckks.galois_element(3, params.n), 2 * params.n - 1):
+        lhs = ring.ntt_forward(ring.automorphism(p, g))
+        rhs = ring.automorphism_eval(ring.ntt_forward(p), g)
+        assert np.array_equal(lhs.coeffs, rhs.coeffs)
+
+
+def test_keygen_bit_exact(small, golden_small):
+    from paper_2310_16530_b200.engine import to_host_u64
+    _, ks = small
+    assert np.array_equal(ks.sk.coeffs, golden_small["sk"])
+    assert np.array_equal(ks.pk[0].coeffs, golden_small["pk_b"])
+    assert np.array_equal(ks.pk[1].coeffs, golden_small["pk_a"])
+    assert np.array_equal(to_host_u64(ks.rlk.rows_b), golden_small["rlk_b"])
+    assert np.array_equal(to_host_u64(ks.rlk.rows_a), golden_small["rlk_a"])
+    for s in (1, 2, 4):
+        assert np.array_equal(to_host_u64(ks.gks[s].rows_b), golden_small[f"gk{s}_b"])
+        assert np.array_equal(to_host_u64(ks.gks[s].rows_a), golden_small[f"gk{s}_a"])
+
+
+@pytest.fixture(scope="module")
+def cts(small, golden_small):
+    from paper_2310_16530_b200 import ckks
+    params, ks = small
+    L = params.max_level
+    pt1 = ckks.encode(golden_small["v1"], params, L)
+    ct1 = ckks.encrypt(pt1, ks, np.random.default_rng(77))
+    ct2 = ckks.encrypt(ckks.encode(golden_small["v2"], params, L), ks, np.random.default_rng(78))
+    return pt1, ct1, ct2
+
+
+def test_encode_encrypt(cts, golden_small):
+    pt1, ct1, ct2 = cts
+    assert np.array_equal(pt1.poly.coeffs, golden_small["pt1"])
+    assert np.array_equal(_ct(ct1), golden_small["ct1"])
+    assert np.array_equal(_ct(ct2), golden_small["ct2"])
+
+
+def test_hmult_rescale(small, cts, golden_small):
+    from paper_2310_16530_b200 import ckks
+    params, ks = small
+    _, ct1, ct2 = cts
+    hm = ckks.hmult(ct1, ct2, ks)
+    assert np.array_equal(_ct(hm), golden_small["hmult"])
+    rs = ckks.rescale(hm, params)
+    assert np.array_equal(_ct(rs), golden_small["rescale"])
+    dec = ckks.decode(ckks.decrypt(rs, ks), params)
+    np.testing.assert_array_equal(dec, golden_small["dec_hmult"])
+
+
+@pytest.mark.parametrize("k", [1, 3, -1, 4])
+def test_rotate(small, cts, golden_small, k):
+    from paper_2310_16530_b200 import ckks
+    _, ks = small
+    _, ct1, _ = cts
+    assert np.array_equal(_ct(ckks.rotate(ct1, k, ks)), golden_small[f"rot{k}"])
+
+
+def test_rotate_many_hoisted(small, cts, golden_small):
+    from paper_2310_16530_b200 import ckks
+    _, ks = small
+    _, ct1, _ = cts
+    outs = ckks.rotate_many(ct1, [1, 4, 3], ks)
+    assert np.array_equal(_ct(outs[0]), golden_small["rot1"])
+    assert np.array_equal(_ct(outs[1]), golden_small["rot4"])
+    assert np.array_equal(_ct(outs[2]), golden_small["rot3"])
+
+
+def test_elementwise(small, cts, golden_small):
+    from paper_2310_16530_b200 import ckks
+    _, ks = small
+    pt1, ct1, ct2 = cts
+    assert np.array_equal(_ct(ckks.pmult(ct1, pt1)), golden_small["pmult"])
+    assert np.array_equal(_ct(ckks.hadd(ct1, ct2)), golden_small["hadd"])
+    assert np.array_equal(_ct(ckks.padd(ct1, pt1)), golden_small["padd"])
