@@ -128,6 +128,15 @@ size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* ctx, uint32_t npolys);
 int hcnn_rescale(hcnn_ctx* ctx, uint64_t* out, const uint64_t* in, uint32_t level, uint32_t npolys, void* ws,
                  void* stream);
 
+/* ---- instrumentation ------------------------------------------------------ */
+/* count of engine kernels launched since load (all contexts) */
+unsigned long long hcnn_kernel_launches(void);
+/* when enabled, every launch is bracketed by CUDA events on its stream */
+void hcnn_profile_enable(int on);
+/* per-kernel totals as JSON {"name": [launches, ms, algorithmic_bytes, kernels]};
+ * returns the JSON length (buf may be NULL to size it) */
+int hcnn_profile_read(char* buf, size_t len, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,9 @@ SIGNATURES = {
                                    ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP, _VP]),
     "hcnn_rescale_workspace_bytes": (_SZ, [_VP, _U32]),
     "hcnn_rescale": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP, _VP]),
+    "hcnn_kernel_launches": (ctypes.c_ulonglong, []),
+    "hcnn_profile_enable": (None, [_INT]),
+    "hcnn_profile_read": (_INT, [ctypes.c_char_p, _SZ, _INT]),
 }
 
 _STATUS = {
@@ -105,6 +108,25 @@ def check(rc: int) -> None:
     msg = (load().hcnn_last_error() or b"").decode(errors="replace")
     cls = _STATUS.get(rc, NativeError)
     raise cls(f"hcnn-b200: {msg} (status {rc})")
+
+
+def kernel_launches() -> int:
+    return int(load().hcnn_kernel_launches())
+
+
+def profile_enable(on: bool) -> None:
+    load().hcnn_profile_enable(1 if on else 0)
+
+
+def profile_read(reset: bool = True) -> dict:
+    """{kernel: {"launches", "ms", "bytes", "kernels"}} accumulated since the last reset."""
+    import json
+    lib = load()
+    n = lib.hcnn_profile_read(None, 0, 0)
+    buf = ctypes.create_string_buffer(n + 1)
+    lib.hcnn_profile_read(buf, n + 1, 1 if reset else 0)
+    raw = json.loads(buf.value.decode())
+    return {k: {"launches": int(v[0]), "ms": v[1], "bytes": v[2], "kernels": int(v[3])} for k, v in raw.items()}
 
 
 def exported_symbols() -> list[str]:

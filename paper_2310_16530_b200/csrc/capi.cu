@@ -174,6 +174,44 @@ static int get_modup(hcnn_ctx* c, u32 level, ModupSet** out) {
   return HCNN_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// launch accounting + optional per-launch CUDA-event profiling
+// ---------------------------------------------------------------------------
+#include <atomic>
+#include <array>
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+  double bytes;
+  int nk;
+};
+static std::mutex g_pm;
+static std::atomic<bool> g_prof{false};
+static std::vector<ProfRec> g_pending;
+static std::map<std::string, std::array<double, 4>> g_acc;  // launches, ms, bytes, kernels
+static std::atomic<unsigned long long> g_kernels{0};
+
+#define PK(name, bytes, nk, st, expr)                                                 \
+  do {                                                                                \
+    cudaEvent_t _a = nullptr, _b = nullptr;                                           \
+    const bool _p = g_prof.load();                                                    \
+    if (_p) {                                                                         \
+      cudaEventCreate(&_a);                                                           \
+      cudaEventCreate(&_b);                                                           \
+      cudaEventRecord(_a, st);                                                        \
+    }                                                                                 \
+    CK(expr);                                                                         \
+    g_kernels += (nk);                                                                \
+    if (_p) {                                                                         \
+      cudaEventRecord(_b, st);                                                        \
+      std::lock_guard<std::mutex> _lk(g_pm);                                          \
+      g_pending.push_back(ProfRec{name, _a, _b, (double)(bytes), (int)(nk)});         \
+    }                                                                                 \
+  } while (0)
+
+static int ntt_nk(const hcnn_ctx* c) { return c->logN > 12 ? 2 : 1; }
+
 extern "C" {
 
 const char* hcnn_last_error(void) { return g_err.c_str(); }
@@ -345,7 +383,8 @@ static int ntt_common(hcnn_ctx* c, uint64_t* data, u32 nq, u32 np, u32 npolys, v
   m.base = data;
   m.poly_stride = (size_t)(nq + np) * c->n;
   m.basis = c->basis(nq, np);
-  CK(launch_ntt(c->tables(), m, nq + np, npolys, inv, STREAM(s)));
+  PK(inv ? "ntt_inv" : "ntt_fwd", 16.0 * (nq + np) * npolys * c->n, ntt_nk(c), STREAM(s),
+     launch_ntt(c->tables(), m, nq + np, npolys, inv, STREAM(s)));
   return HCNN_OK;
 }
 
@@ -360,7 +399,8 @@ static int binop(hcnn_ctx* c, int op, uint64_t* out, const uint64_t* a, const ui
                  u32 npolys, int bc, void* s) {
   int rc = check_basis(c, nq, np);
   if (rc) return rc;
-  CK(launch_ew_binary(op, out, a, b, c->basis(nq, np), c->logN, npolys, bc, c->d_mc, STREAM(s)));
+  PK("ew_binary", 24.0 * (nq + np) * npolys * c->n, 1, STREAM(s),
+     launch_ew_binary(op, out, a, b, c->basis(nq, np), c->logN, npolys, bc, c->d_mc, STREAM(s)));
   return HCNN_OK;
 }
 int hcnn_poly_add(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
@@ -387,7 +427,8 @@ int hcnn_poly_mac_mont(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint
 static int unop(hcnn_ctx* c, int op, uint64_t* out, const uint64_t* a, u32 nq, u32 np, u32 npolys, void* s) {
   int rc = check_basis(c, nq, np);
   if (rc) return rc;
-  CK(launch_ew_unary(op, out, a, c->basis(nq, np), c->logN, npolys, c->d_mc, nullptr, nullptr, STREAM(s)));
+  PK("ew_unary", 16.0 * (nq + np) * npolys * c->n, 1, STREAM(s),
+     launch_ew_unary(op, out, a, c->basis(nq, np), c->logN, npolys, c->d_mc, nullptr, nullptr, STREAM(s)));
   return HCNN_OK;
 }
 int hcnn_poly_neg(hcnn_ctx* c, uint64_t* out, const uint64_t* a, uint32_t nq, uint32_t np, uint32_t npolys,
@@ -419,7 +460,8 @@ int hcnn_scalar_mul(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_
   u64* d = nullptr;
   CK(cudaMallocAsync((void**)&d, 2 * nl * 8, STREAM(s)));
   CK(cudaMemcpyAsync(d, h.data(), 2 * nl * 8, cudaMemcpyHostToDevice, STREAM(s)));
-  CK(launch_ew_unary(EW_SCALAR, out, a, b, c->logN, npolys, c->d_mc, d, d + nl, STREAM(s)));
+  PK("ew_scalar", 16.0 * nl * npolys * c->n, 1, STREAM(s),
+     launch_ew_unary(EW_SCALAR, out, a, b, c->logN, npolys, c->d_mc, d, d + nl, STREAM(s)));
   CK(cudaFreeAsync(d, STREAM(s)));
   // the host vector must outlive the (pageable, synchronous-to-host) copy
   return HCNN_OK;
@@ -429,7 +471,8 @@ int hcnn_from_signed(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t nq,
                      void* s) {
   int rc = check_basis(c, nq, np);
   if (rc) return rc;
-  CK(launch_from_signed(out, (const long long*)in, c->basis(nq, np), c->logN, npolys, c->d_mc, STREAM(s)));
+  PK("from_signed", 8.0 * (nq + np + 1) * npolys * c->n, 1, STREAM(s),
+     launch_from_signed(out, (const long long*)in, c->basis(nq, np), c->logN, npolys, c->d_mc, STREAM(s)));
   return HCNN_OK;
 }
 
@@ -439,7 +482,8 @@ int hcnn_automorphism(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint64_t g
   if (rc) return rc;
   if ((g & 1) == 0) return fail(HCNN_E_PARAMETER, "automorphism exponent must be odd");
   g %= 2ull * c->n;
-  CK(launch_automorph(eval_domain, out, in, c->basis(nq, np), c->logN, npolys, g, c->d_mc, STREAM(s)));
+  PK("automorph", 16.0 * (nq + np) * npolys * c->n, 1, STREAM(s),
+     launch_automorph(eval_domain, out, in, c->basis(nq, np), c->logN, npolys, g, c->d_mc, STREAM(s)));
   return HCNN_OK;
 }
 
@@ -472,7 +516,8 @@ int hcnn_base_convert(hcnn_ctx* c, uint64_t* out, const uint64_t* in, const uint
     }
     st = &it->second;
   }
-  CK(launch_fbc(st->dev, c->d_mc, in, (size_t)n_src * c->n, out, (size_t)n_dst * c->n, c->logN, npolys, n_dst,
+  PK("fbc", 8.0 * (n_src + n_dst) * npolys * c->n, 1, STREAM(s),
+     launch_fbc(st->dev, c->d_mc, in, (size_t)n_src * c->n, out, (size_t)n_dst * c->n, c->logN, npolys, n_dst,
                 STREAM(s)));
   return HCNN_OK;
 }
@@ -512,14 +557,14 @@ static int ks_modup(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, cu
   m.base = w.xc;
   m.poly_stride = nq * N;
   m.basis = c->basis(nq, 0);
-  CK(launch_ntt(c->tables(), m, nq, 1, true, st));
-  CK(launch_modup(mu->d_tabs, nd, c->d_mc, w.xc, w.raised, c->alpha, n_ext, c->logN, st));
+  PK("ntt_inv", 16.0 * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), m, nq, 1, true, st));
+  PK("modup", 8.0 * (nq + (double)nd * (n_ext - c->alpha)) * N, 1, st, launch_modup(mu->d_tabs, nd, c->d_mc, w.xc, w.raised, c->alpha, n_ext, c->logN, st));
   LimbMap r{};
   r.base = w.raised;
   r.poly_stride = (size_t)n_ext * N;
   r.basis = c->basis(nq, c->K);
   r.skip_alpha = c->alpha;
-  CK(launch_ntt(c->tables(), r, n_ext, nd, false, st));
+  PK("ntt_fwd", 16.0 * ((double)nd * n_ext - nq) * N, ntt_nk(c), st, launch_ntt(c->tables(), r, n_ext, nd, false, st));
   return HCNN_OK;
 }
 
@@ -529,20 +574,20 @@ static int ks_finish(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, u
                      cudaStream_t st) {
   const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
   const size_t N = c->n;
-  CK(launch_ks_inner(w.acc, x_eval, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, g, c->d_mc, st));
+  PK("ks_inner", 8.0 * ((double)nd * n_ext * 3 + 2 * n_ext) * N, 1, st, launch_ks_inner(w.acc, x_eval, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, g, c->d_mc, st));
   LimbMap m{};
   m.base = w.acc + nq * N;
   m.poly_stride = (size_t)n_ext * N;
   m.basis = c->basis(nq, c->K);
   m.first_limb = nq;
-  CK(launch_ntt(c->tables(), m, c->K, 2, true, st));
-  CK(launch_fbc(c->moddown.dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N, c->logN, 2, nq, st));
+  PK("ntt_inv", 16.0 * 2 * c->K * N, ntt_nk(c), st, launch_ntt(c->tables(), m, c->K, 2, true, st));
+  PK("moddown_fbc", 8.0 * 2 * (c->K + nq) * N, 1, st, launch_fbc(c->moddown.dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N, c->logN, 2, nq, st));
   LimbMap l{};
   l.base = w.lift;
   l.poly_stride = nq * N;
   l.basis = c->basis(nq, 0);
-  CK(launch_ntt(c->tables(), l, nq, 2, false, st));
-  CK(launch_moddown_combine(out0, out1, w.acc, w.lift, add0, add1, g_add, nq, n_ext, c->logN, c->d_pinv,
+  PK("ntt_fwd", 16.0 * 2 * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), l, nq, 2, false, st));
+  PK("moddown_combine", 8.0 * 2 * (3 * nq + (add0 ? nq : 0)) * N, 1, st, launch_moddown_combine(out0, out1, w.acc, w.lift, add0, add1, g_add, nq, n_ext, c->logN, c->d_pinv,
                             c->d_pinv_sh, c->d_mc, st));
   return HCNN_OK;
 }
@@ -572,7 +617,7 @@ int hcnn_hmult(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b,
   const size_t N = c->n;
   KsWs w = ks_layout(c, level, ws);
   u64* d2 = w.lift;  // parked in the ModDown scratch until the inner product
-  CK(launch_tensor(out, out + nq * N, d2, a, b, nq, c->logN, c->d_mc, STREAM(s)));
+  PK("tensor", 8.0 * 7 * nq * N, 1, STREAM(s), launch_tensor(out, out + nq * N, d2, a, b, nq, c->logN, c->d_mc, STREAM(s)));
   rc = ks_modup(c, level, d2, w, STREAM(s));
   if (rc) return rc;
   return ks_finish(c, level, d2, w, 1, kb, ka, out, out + nq * N, out, out + nq * N, 1, STREAM(s));
@@ -607,22 +652,63 @@ int hcnn_rescale(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint32_t level,
   if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
   const u32 l = level;
   u64* top = (u64*)ws;
-  CK(launch_gather_limb(top, in, l, l + 1, c->logN, npolys, STREAM(s)));
+  PK("rescale_gather", 16.0 * npolys * c->n, 1, STREAM(s), launch_gather_limb(top, in, l, l + 1, c->logN, npolys, STREAM(s)));
   LimbMap m{};
   m.base = top;
   m.poly_stride = c->n;
   m.basis = c->basis(l + 1, 0);
   m.first_limb = l;
-  CK(launch_ntt(c->tables(), m, 1, npolys, true, STREAM(s)));
-  CK(launch_rescale_lift(out, top, l, c->logN, npolys, c->d_mc, STREAM(s)));
+  PK("ntt_inv", 16.0 * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), m, 1, npolys, true, STREAM(s)));
+  PK("rescale_lift", 8.0 * (l + 1) * npolys * c->n, 1, STREAM(s), launch_rescale_lift(out, top, l, c->logN, npolys, c->d_mc, STREAM(s)));
   LimbMap o{};
   o.base = out;
   o.poly_stride = (size_t)l * c->n;
   o.basis = c->basis(l, 0);
-  CK(launch_ntt(c->tables(), o, l, npolys, false, STREAM(s)));
-  CK(launch_rescale_combine(out, in, l, c->logN, npolys, c->d_rinv + (size_t)l * c->Lq,
+  PK("ntt_fwd", 16.0 * l * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), o, l, npolys, false, STREAM(s)));
+  PK("rescale_combine", 24.0 * l * npolys * c->n, 1, STREAM(s), launch_rescale_combine(out, in, l, c->logN, npolys, c->d_rinv + (size_t)l * c->Lq,
                             c->d_rinv_sh + (size_t)l * c->Lq, c->d_mc, STREAM(s)));
   return HCNN_OK;
+}
+
+
+void hcnn_profile_enable(int on) { g_prof.store(on != 0); }
+
+unsigned long long hcnn_kernel_launches(void) { return g_kernels.load(); }
+
+// Drain pending event pairs into per-name totals and render them as JSON:
+// {"name": [launches, total_ms, algorithmic_bytes, kernels], ...}
+int hcnn_profile_read(char* buf, size_t len, int reset) {
+  std::lock_guard<std::mutex> lk(g_pm);
+  for (auto& r : g_pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto& a = g_acc[r.name];
+    a[0] += 1;
+    a[1] += ms;
+    a[2] += r.bytes;
+    a[3] += r.nk;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_pending.clear();
+  std::string js = "{";
+  bool first = true;
+  for (auto& kv : g_acc) {
+    char tmp[256];
+    snprintf(tmp, sizeof tmp, "%s\"%s\": [%.0f, %.6f, %.0f, %.0f]", first ? "" : ", ", kv.first.c_str(),
+             kv.second[0], kv.second[1], kv.second[2], kv.second[3]);
+    js += tmp;
+    first = false;
+  }
+  js += "}";
+  if (reset) g_acc.clear();
+  if (buf && len) {
+    size_t n = js.size() < len - 1 ? js.size() : len - 1;
+    memcpy(buf, js.data(), n);
+    buf[n] = 0;
+  }
+  return (int)js.size();
 }
 
 }  // extern "C"

@@ -229,7 +229,12 @@ class DeviceContext:
         return out
 
 
-def context_for(n: int, q_list: Sequence[int], p_list: Sequence[int] = (), device: int = 0) -> DeviceContext:
+def context_for(n: int, q_list: Sequence[int], p_list: Sequence[int] = (),
+                device: int | None = None) -> DeviceContext:
+    """The (cached) context for a chain on `device` (default: torch's current device)."""
+    if device is None:
+        _require_cuda(0)
+        device = torch.cuda.current_device()
     key = (int(n), tuple(int(q) for q in q_list), tuple(int(p) for p in p_list), device)
     ctx = _ctx_cache.get(key)
     if ctx is None:
