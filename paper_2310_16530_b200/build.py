@@ -16,9 +16,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libhcnn_b200.so"
-SOURCES = ["ntt.cu", "arith.cu", "capi.cu"]
+SOURCES = ["ntt.cu", "ntt2.cu", "arith.cu", "capi.cu"]
 NVCC_FLAGS = [
-    "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    "-O3", "-std=c++17", "--extended-lambda", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
     "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-O3",
 ]
 

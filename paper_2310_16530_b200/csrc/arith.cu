@@ -212,6 +212,74 @@ __global__ void k_fbc(FbcDev T, const ModConsts* __restrict__ mc, const u64* __r
     fbc_point(T, mc, in + (size_t)z * in_pst, N, out + (size_t)z * out_pst, k, N, nt);
 }
 
+// Specialised centred FBC for NS <= 6 source limbs.  Per-target constants
+// (modulus, Montgomery inverse, output position, conversion row and the
+// sign-mask correction table) are staged in shared memory; each output is
+// one 128-bit sum of NS products of the raw y_i = x_i (Q/q_i)^-1 mod q_i,
+// one REDC, and one subtraction of corr[mask] = sum over the limbs whose
+// y_i exceeds q_i/2 of q_i (Q/q_i) mod t -- i.e. the centred lift of
+// ring.py:378-398 without per-limb branches.
+// z = blockIdx.y selects table tabs[z] (modup: one table per digit) or
+// tabs[0] (tab_per_z == 0).
+template <int NS>
+__global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, int tab_per_z,
+                                               const ModConsts* __restrict__ mc, const u64* __restrict__ in,
+                                               size_t in_pst, u64* __restrict__ out, size_t out_pst, u32 logN,
+                                               u32 nt_override, u32 z0) {
+  constexpr int NM = 1 << NS;
+  extern __shared__ u64 sh[];
+  const u32 N = 1u << logN, z = blockIdx.y + z0;
+  const FbcDev& T = tabs[tab_per_z ? z : 0];
+  const u32 nt = nt_override ? nt_override : T.nt;
+  u64* s_q = sh;
+  u64* s_ninv = s_q + nt;
+  u64* s_pos = s_ninv + nt;
+  u64* s_tm = s_pos + nt;        // [nt][NS]
+  u64* s_corr = s_tm + nt * NS;  // [nt][NM]
+  for (u32 t = threadIdx.x; t < nt; t += blockDim.x) {
+    const u32 m = T.dst_mod[t];
+    s_q[t] = mc[m].q;
+    s_ninv[t] = mc[m].ninv;
+    s_pos[t] = (u64)T.dst_pos[t] * N;
+  }
+  for (u32 e = threadIdx.x; e < nt * NS; e += blockDim.x) s_tm[e] = T.tmat[e];
+  for (u32 e = threadIdx.x; e < nt * NM; e += blockDim.x) s_corr[e] = T.corr[e];
+  u64 qi[NS], hq[NS], ip[NS], ips[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    qi[i] = mc[T.src_mod[i]].q;
+    hq[i] = qi[i] >> 1;
+    ip[i] = T.inv_punc[i];
+    ips[i] = T.inv_punc_sh[i];
+  }
+  __syncthreads();
+  const u64* src = in + (size_t)z * in_pst;
+  u64* dst = out + (size_t)z * out_pst;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    u64 y[NS];
+    u32 mask = 0;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      y[i] = shoup_mul(src[(size_t)i * N + k], ip[i], ips[i], qi[i]);
+      mask |= (y[i] > hq[i] ? 1u : 0u) << i;
+    }
+    for (u32 t = 0; t < nt; ++t) {
+      const u64 qt = s_q[t];
+      u64 hi = 0, lo = 0;
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {
+        const u64 b = s_tm[t * NS + i];
+        const u64 plo = y[i] * b;
+        const u64 phi = __umul64hi(y[i], b);
+        lo += plo;
+        hi += phi + (lo < plo ? 1ull : 0ull);
+      }
+      u64 v = redc128(hi, lo, qt, s_ninv[t]);
+      dst[s_pos[t] + k] = sub_mod(v, s_corr[t * NM + mask], qt);
+    }
+  }
+}
+
 // ModUp of every digit of a key-switch input (ckks.py:563-578):
 // digit j's limbs [j*alpha, ...) of xc are converted to the extended basis
 // minus the digit, written into raised[j] at their basis positions.
@@ -366,18 +434,66 @@ cudaError_t launch_tensor(u64* d0, u64* d1, u64* d2, const u64* a, const u64* b,
   return cudaGetLastError();
 }
 
-cudaError_t launch_fbc(const FbcDev& T, const ModConsts* mc, const u64* in, size_t in_pst, u64* out,
-                       size_t out_pst, u32 logN, u32 npolys, u32 nt, cudaStream_t st) {
+static size_t fbc_smem(u32 nt, int ns) { return (size_t)nt * (3 + ns + (1u << ns)) * 8; }
+
+template <int NS>
+static cudaError_t launch_fbc_t(const FbcDev* tabs, int tab_per_z, const ModConsts* mc, const u64* in,
+                                size_t in_pst, u64* out, size_t out_pst, u32 logN, u32 nz, u32 z0, u32 nt,
+                                u32 nt_override, cudaStream_t st) {
+  size_t sm = fbc_smem(nt, NS);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_fbc_t<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e) return e;
+  }
+  dim3 g = row_grid((1u << logN) / 2, nz, 256);
+  k_fbc_t<NS><<<g, 256, sm, st>>>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nt_override, z0);
+  return cudaGetLastError();
+}
+
+static cudaError_t dispatch_fbc_t(int ns, const FbcDev* tabs, int tab_per_z, const ModConsts* mc, const u64* in,
+                                  size_t in_pst, u64* out, size_t out_pst, u32 logN, u32 nz, u32 z0, u32 nt,
+                                  u32 nt_override, cudaStream_t st) {
+  switch (ns) {
+    case 1: return launch_fbc_t<1>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
+    case 2: return launch_fbc_t<2>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
+    case 3: return launch_fbc_t<3>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
+    case 4: return launch_fbc_t<4>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
+    case 5: return launch_fbc_t<5>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
+    case 6: return launch_fbc_t<6>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_fbc(const FbcDev& T, const FbcDev* dT, const ModConsts* mc, const u64* in, size_t in_pst,
+                       u64* out, size_t out_pst, u32 logN, u32 npolys, u32 nt, cudaStream_t st) {
+  if (dT && T.corr && T.nored && T.ns <= 6)
+    return dispatch_fbc_t(T.ns, dT, 0, mc, in, in_pst, out, out_pst, logN, npolys, 0, nt, nt, st);
   if (T.ns > FBC_MAX_SRC) return cudaErrorInvalidValue;
   k_fbc<<<row_grid(1u << logN, npolys, 128), 128, 0, st>>>(T, mc, in, in_pst, out, out_pst, logN, nt);
   return cudaGetLastError();
 }
 
-cudaError_t launch_modup(const FbcDev* tabs, u32 ndig, const ModConsts* mc, const u64* xc, u64* raised, u32 alpha,
-                         u32 n_ext, u32 logN, cudaStream_t st) {
+cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, const ModConsts* mc, const u64* xc,
+                         u64* raised, u32 alpha, u32 n_ext, u32 logN, cudaStream_t st) {
   if (alpha > FBC_MAX_SRC) return cudaErrorInvalidValue;
-  k_modup<<<row_grid(1u << logN, ndig, 128), 128, 0, st>>>(tabs, mc, xc, raised, alpha, n_ext, logN);
-  return cudaGetLastError();
+  bool fast = true;
+  for (u32 j = 0; j < ndig; ++j) fast = fast && htabs[j].corr && htabs[j].nored && htabs[j].ns <= 6;
+  if (!fast) {
+    k_modup<<<row_grid(1u << logN, ndig, 128), 128, 0, st>>>(tabs, mc, xc, raised, alpha, n_ext, logN);
+    return cudaGetLastError();
+  }
+  // full digits share one launch; a partial last digit gets its own
+  u32 nfull = ndig;
+  if (htabs[ndig - 1].ns != alpha) nfull = ndig - 1;
+  cudaError_t e = cudaSuccess;
+  if (nfull)
+    e = dispatch_fbc_t((int)alpha, tabs, 1, mc, xc, (size_t)alpha * (1u << logN), raised,
+                       (size_t)n_ext * (1u << logN), logN, nfull, 0, htabs[0].nt, 0, st);
+  if (e) return e;
+  if (nfull < ndig)
+    e = dispatch_fbc_t((int)htabs[ndig - 1].ns, tabs, 1, mc, xc, (size_t)alpha * (1u << logN), raised,
+                       (size_t)n_ext * (1u << logN), logN, 1, nfull, htabs[ndig - 1].nt, 0, st);
+  return e;
 }
 
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,

@@ -16,10 +16,13 @@ cudaError_t launch_automorph(int eval_domain, u64* out, const u64* in, Basis bas
                              const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_tensor(u64* d0, u64* d1, u64* d2, const u64* a, const u64* b, u32 nlimbs, u32 logN,
                           const ModConsts* mc, cudaStream_t st);
-cudaError_t launch_fbc(const FbcDev& T, const ModConsts* mc, const u64* in, size_t in_pst, u64* out,
-                       size_t out_pst, u32 logN, u32 npolys, u32 nt, cudaStream_t st);
-cudaError_t launch_modup(const FbcDev* tabs, u32 ndig, const ModConsts* mc, const u64* xc, u64* raised, u32 alpha,
-                         u32 n_ext, u32 logN, cudaStream_t st);
+// T: host copy of the table (pointers are device addresses); dT: the same
+// table in device memory (enables the specialised kernel), may be null
+cudaError_t launch_fbc(const FbcDev& T, const FbcDev* dT, const ModConsts* mc, const u64* in, size_t in_pst,
+                       u64* out, size_t out_pst, u32 logN, u32 npolys, u32 nt, cudaStream_t st);
+// tabs: device array of per-digit tables; htabs: host copies of the same
+cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, const ModConsts* mc, const u64* xc,
+                         u64* raised, u32 alpha, u32 n_ext, u32 logN, cudaStream_t st);
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
                             cudaStream_t st);

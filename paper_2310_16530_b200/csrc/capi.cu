@@ -31,12 +31,14 @@ static int fail(int code, const std::string& msg) {
 
 // host-resident FBC table with its device copy
 struct FbcStore {
-  FbcDev dev{};
+  FbcDev dev{};            // host copy (pointers into `mem`)
+  FbcDev* d_dev = nullptr;  // the same struct in device memory
   void* mem = nullptr;
 };
 
 struct ModupSet {
   std::vector<FbcStore> digits;
+  std::vector<FbcDev> host;  // host copies, one per digit
   FbcDev* d_tabs = nullptr;  // device array of FbcDev, one per digit
 };
 
@@ -47,6 +49,7 @@ struct hcnn_ctx {
   std::vector<ModConsts> hmc;
   ModConsts* d_mc = nullptr;
   u64 *d_tw = nullptr, *d_twp = nullptr, *d_itw = nullptr, *d_itwp = nullptr;
+  ulonglong2 *d_ctw = nullptr, *d_ictw = nullptr;
   FbcStore moddown;                  // P -> q_0..q_{Lq-1}
   u64 *d_pinv = nullptr, *d_pinv_sh = nullptr;  // P^-1 mod q_i
   u64 *d_rinv = nullptr, *d_rinv_sh = nullptr;  // [l][i] q_l^-1 mod q_i
@@ -61,6 +64,8 @@ struct hcnn_ctx {
     T.twp = d_twp;
     T.itw = d_itw;
     T.itwp = d_itwp;
+    T.ctw = d_ctw;
+    T.ictw = d_ictw;
     return T;
   }
   Basis basis(u32 nq, u32 np) const {
@@ -103,7 +108,8 @@ static int build_fbc(hcnn_ctx* c, const std::vector<u32>& src, const std::vector
   u32buf.insert(u32buf.end(), dst.begin(), dst.end());
   u32buf.insert(u32buf.end(), dst_pos.begin(), dst_pos.end());
   while (u32buf.size() % 2) u32buf.push_back(0);
-  std::vector<u64> u64buf(2 * ns + (size_t)nt * ns);
+  const bool with_corr = ns <= 6;
+  std::vector<u64> u64buf(2 * ns + (size_t)nt * ns + (with_corr ? (size_t)nt << ns : 0));
   for (u32 i = 0; i < ns; ++i) {
     u64 qi = c->mods[src[i]];
     u64 prod = 1;
@@ -121,7 +127,24 @@ static int build_fbc(hcnn_ctx* c, const std::vector<u32>& src, const std::vector
         if (j != i) prod = h_mulmod(prod, c->mods[src[j]] % qt, qt);
       u64buf[2 * ns + (size_t)t * ns + i] = h_to_mont(prod, qt);
     }
+    if (with_corr) {
+      // corr[t][mask] = sum_{i in mask} q_i * (Q/q_i) mod t: the centred
+      // lift subtracts q_i for every limb whose y_i exceeds q_i/2
+      for (u32 mask = 0; mask < (1u << ns); ++mask) {
+        u64 acc = 0;
+        for (u32 i = 0; i < ns; ++i) {
+          if (!((mask >> i) & 1)) continue;
+          u64 prod = c->mods[src[i]] % qt;
+          for (u32 j = 0; j < ns; ++j)
+            if (j != i) prod = h_mulmod(prod, c->mods[src[j]] % qt, qt);
+          acc = (acc + prod) % qt;
+        }
+        u64buf[2 * ns + (size_t)nt * ns + ((size_t)t << ns) + mask] = acc;
+      }
+    }
   }
+  unsigned __int128 bound = 0;
+  for (u32 i = 0; i < ns; ++i) bound += c->mods[src[i]];
   size_t b32 = u32buf.size() * 4, b64 = u64buf.size() * 8;
   CK(cudaMalloc(&st->mem, b32 + b64));
   CK(cudaMemcpy(st->mem, u32buf.data(), b32, cudaMemcpyHostToDevice));
@@ -136,6 +159,10 @@ static int build_fbc(hcnn_ctx* c, const std::vector<u32>& src, const std::vector
   st->dev.inv_punc = d64;
   st->dev.inv_punc_sh = d64 + ns;
   st->dev.tmat = d64 + 2 * ns;
+  st->dev.corr = with_corr ? d64 + 2 * ns + (size_t)nt * ns : nullptr;
+  st->dev.nored = bound < ((unsigned __int128)1 << 64) ? 1 : 0;
+  CK(cudaMalloc(&st->d_dev, sizeof(FbcDev)));
+  CK(cudaMemcpy(st->d_dev, &st->dev, sizeof(FbcDev), cudaMemcpyHostToDevice));
   return HCNN_OK;
 }
 
@@ -166,6 +193,7 @@ static int get_modup(hcnn_ctx* c, u32 level, ModupSet** out) {
     if (rc) return rc;
     set.digits.push_back(st);
     devs.push_back(st.dev);
+    set.host.push_back(st.dev);
   }
   CK(cudaMalloc(&set.d_tabs, sizeof(FbcDev) * devs.size()));
   CK(cudaMemcpy(set.d_tabs, devs.data(), sizeof(FbcDev) * devs.size(), cudaMemcpyHostToDevice));
@@ -301,6 +329,32 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
   CK(cudaMemcpy(c->d_twp, twp.data(), tb, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_itw, itw.data(), tb, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_itwp, itwp.data(), tb, cudaMemcpyHostToDevice));
+  if (ntt2_supported(c->logN)) {
+    // per-chunk twiddles for the radix-16 chunk pass (ntt2.cu): chunk g of
+    // 256 owns 255 Shoup pairs, forward e = 2^s-1+i -> tw[(N1+g)*2^s + i],
+    // inverse e = nb-1+i -> itw[nb*(N1+g) + i] (nb = 128>>u blocks)
+    const u32 N1 = n >> 8;
+    std::vector<ulonglong2> ctw((size_t)c->nmods * N), ictw((size_t)c->nmods * N);
+    for (u32 m = 0; m < c->nmods; ++m)
+      for (u32 g = 0; g < N1; ++g) {
+        ulonglong2* F = &ctw[((size_t)m * N1 + g) * 256];
+        ulonglong2* I = &ictw[((size_t)m * N1 + g) * 256];
+        F[255] = make_ulonglong2(0, 0);
+        I[255] = make_ulonglong2(0, 0);
+        for (u32 s = 0; s < 8; ++s)
+          for (u32 i = 0; i < (1u << s); ++i) {
+            size_t src = (size_t)(N1 + g) * (1u << s) + i;
+            F[(1u << s) - 1 + i] = make_ulonglong2(tw[m * N + src], twp[m * N + src]);
+            u32 nb = 1u << s;  // inverse stage with nb blocks
+            size_t isrc = (size_t)nb * (N1 + g) + i;
+            I[nb - 1 + i] = make_ulonglong2(itw[m * N + isrc], itwp[m * N + isrc]);
+          }
+      }
+    CK(cudaMalloc(&c->d_ctw, ctw.size() * sizeof(ulonglong2)));
+    CK(cudaMalloc(&c->d_ictw, ictw.size() * sizeof(ulonglong2)));
+    CK(cudaMemcpy(c->d_ctw, ctw.data(), ctw.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_ictw, ictw.data(), ictw.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice));
+  }
   // rescale table: q_l^-1 mod q_i
   std::vector<u64> rinv((size_t)n_q * n_q, 0), rinv_sh((size_t)n_q * n_q, 0);
   for (u32 l = 1; l < n_q; ++l)
@@ -348,16 +402,25 @@ void hcnn_ctx_destroy(hcnn_ctx* c) {
   cudaFree(c->d_twp);
   cudaFree(c->d_itw);
   cudaFree(c->d_itwp);
+  cudaFree(c->d_ctw);
+  cudaFree(c->d_ictw);
   cudaFree(c->d_pinv);
   cudaFree(c->d_pinv_sh);
   cudaFree(c->d_rinv);
   cudaFree(c->d_rinv_sh);
   cudaFree(c->moddown.mem);
+  cudaFree(c->moddown.d_dev);
   for (auto& kv : c->modup) {
-    for (auto& d : kv.second.digits) cudaFree(d.mem);
+    for (auto& d : kv.second.digits) {
+      cudaFree(d.mem);
+      cudaFree(d.d_dev);
+    }
     cudaFree(kv.second.d_tabs);
   }
-  for (auto& kv : c->generic) cudaFree(kv.second.mem);
+  for (auto& kv : c->generic) {
+    cudaFree(kv.second.mem);
+    cudaFree(kv.second.d_dev);
+  }
   delete c;
 }
 
@@ -517,7 +580,7 @@ int hcnn_base_convert(hcnn_ctx* c, uint64_t* out, const uint64_t* in, const uint
     st = &it->second;
   }
   PK("fbc", 8.0 * (n_src + n_dst) * npolys * c->n, 1, STREAM(s),
-     launch_fbc(st->dev, c->d_mc, in, (size_t)n_src * c->n, out, (size_t)n_dst * c->n, c->logN, npolys, n_dst,
+     launch_fbc(st->dev, st->d_dev, c->d_mc, in, (size_t)n_src * c->n, out, (size_t)n_dst * c->n, c->logN, npolys, n_dst,
                 STREAM(s)));
   return HCNN_OK;
 }
@@ -558,7 +621,7 @@ static int ks_modup(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, cu
   m.poly_stride = nq * N;
   m.basis = c->basis(nq, 0);
   PK("ntt_inv", 16.0 * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), m, nq, 1, true, st));
-  PK("modup", 8.0 * (nq + (double)nd * (n_ext - c->alpha)) * N, 1, st, launch_modup(mu->d_tabs, nd, c->d_mc, w.xc, w.raised, c->alpha, n_ext, c->logN, st));
+  PK("modup", 8.0 * (nq + (double)nd * (n_ext - c->alpha)) * N, 1, st, launch_modup(mu->d_tabs, mu->host.data(), nd, c->d_mc, w.xc, w.raised, c->alpha, n_ext, c->logN, st));
   LimbMap r{};
   r.base = w.raised;
   r.poly_stride = (size_t)n_ext * N;
@@ -581,7 +644,7 @@ static int ks_finish(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, u
   m.basis = c->basis(nq, c->K);
   m.first_limb = nq;
   PK("ntt_inv", 16.0 * 2 * c->K * N, ntt_nk(c), st, launch_ntt(c->tables(), m, c->K, 2, true, st));
-  PK("moddown_fbc", 8.0 * 2 * (c->K + nq) * N, 1, st, launch_fbc(c->moddown.dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N, c->logN, 2, nq, st));
+  PK("moddown_fbc", 8.0 * 2 * (c->K + nq) * N, 1, st, launch_fbc(c->moddown.dev, c->moddown.d_dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N, c->logN, 2, nq, st));
   LimbMap l{};
   l.base = w.lift;
   l.poly_stride = nq * N;

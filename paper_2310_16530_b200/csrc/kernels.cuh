@@ -23,12 +23,17 @@ struct NttTables {
   const u64* twp;   // Shoup companions
   const u64* itw;   // [mod][N] psi^-brv(j)
   const u64* itwp;
+  const ulonglong2* ctw;   // [mod][N/256][256] per-chunk forward twiddles (ntt2.cu)
+  const ulonglong2* ictw;  // [mod][N/256][256] per-chunk inverse twiddles
 };
 
 void ntt_split(u32 logN, u32* logN1);
 cudaError_t launch_ntt(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 npolys, bool inverse,
                        cudaStream_t st);
 cudaError_t ntt_configure_smem();
+bool ntt2_supported(u32 logN);
+cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 npolys, bool inverse,
+                        cudaStream_t st);
 
 // --------------------------------------------------------------------------
 // fast base conversion tables (ring.py:343-375): for one source set and a
@@ -44,6 +49,8 @@ struct FbcDev {
   const u64* inv_punc;    // [ns]
   const u64* inv_punc_sh; // [ns]
   const u64* tmat;        // [nt][ns] Montgomery form of (Q/q_i) mod t
+  const u64* corr;        // [nt][1<<ns] sum_{i in mask} q_i*(Q/q_i) mod t, or null (ns > 6)
+  int nored;              // ns * max(q_i) < 2^64: 128-bit sums need no interim reduction
 };
 
 }  // namespace hcnn

@@ -250,6 +250,7 @@ void ntt_split(u32 logN, u32* logN1) {
 cudaError_t launch_ntt(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 npolys, bool inverse,
                        cudaStream_t st) {
   if (nlimbs == 0 || npolys == 0) return cudaSuccess;
+  if (T.ctw && ntt2_supported(T.logN)) return launch_ntt2(T, map, nlimbs, npolys, inverse, st);
   u32 logN = T.logN, logN1;
   ntt_split(logN, &logN1);
   const u32 N = 1u << logN;

@@ -1,0 +1,85 @@
+"""NTT / iNTT parity over every ring size the engine dispatches (single-pass
+smem kernels for small N, radix-16 register passes for 2^12..2^16) against
+the C oracle (restated reference kernels.py:232-281), plus acceptance gate 1
+(test_acceptance.py:128-156): transform products equal schoolbook negacyclic
+products, run through the GPU."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _mods(n, bits=(59, 40, 45)):
+    from paper_2310_16530_b200.ring import find_ntt_primes
+    out = []
+    for b in bits:
+        out += find_ntt_primes(n, b, 1, avoid=out)
+    return out
+
+
+@pytest.mark.parametrize("logn", list(range(2, 17)))
+def test_ntt_matches_oracle(logn):
+    from oracle import ckks_oracle as O
+    from paper_2310_16530_b200.engine import context_for, to_device_u64, to_host_u64
+    n = 1 << logn
+    qs = _mods(n)
+    rng = np.random.default_rng(logn)
+    rows = np.stack([rng.integers(0, q, size=(3, n), dtype=np.uint64) for q in qs], axis=1)  # [3 polys, 3 limbs, n]
+    ctx = context_for(n, qs)
+    d = to_device_u64(rows)
+    ctx.ntt(d, len(qs))
+    got = to_host_u64(d)
+    for z in range(3):
+        assert np.array_equal(got[z], O.ntt(rows[z], qs)), f"poly {z}"
+    ctx.ntt(d, len(qs), inverse=True)
+    assert np.array_equal(to_host_u64(d), rows)
+
+
+@pytest.mark.parametrize("logn", [12, 13, 14, 16])
+def test_ntt_ext_basis_and_skip(logn):
+    """Ext-basis NTT (q prefix + specials) equals per-limb oracle transforms."""
+    from oracle import ckks_oracle as O
+    from paper_2310_16530_b200.engine import context_for, to_device_u64, to_host_u64
+    n = 1 << logn
+    qs = _mods(n, (59, 40, 41, 42))
+    ps = _mods(n, (58, 57))
+    ps = [p for p in ps if p not in qs]
+    ctx = context_for(n, qs, ps)
+    rng = np.random.default_rng(7)
+    basis = qs[:2] + ps
+    rows = np.stack([rng.integers(0, q, size=n, dtype=np.uint64) for q in basis])
+    d = to_device_u64(rows)
+    ctx.ntt(d, 2, len(ps))
+    assert np.array_equal(to_host_u64(d), O.ntt(rows, basis))
+
+
+def _schoolbook(a, b, q):
+    n = len(a)
+    out = [0] * n
+    for i, ai in enumerate(a):
+        for j, bj in enumerate(b):
+            k = i + j
+            if k < n:
+                out[k] = (out[k] + ai * bj) % q
+            else:
+                out[k - n] = (out[k - n] - ai * bj) % q
+    return out
+
+
+@pytest.mark.parametrize("n", [4, 8, 16, 32])
+def test_gate1_schoolbook(n):
+    from paper_2310_16530_b200 import ring
+    from paper_2310_16530_b200.ring import Modulus, find_ntt_primes
+    qs = find_ntt_primes(n, 59, 1) + find_ntt_primes(n, 45, 1)
+    mods = tuple(Modulus.make(q) for q in qs)
+    rng = np.random.default_rng(0xACC1)
+    for _ in range(50):
+        a = rng.integers(-(1 << 61), 1 << 61, size=n).tolist()
+        b = rng.integers(-(1 << 61), 1 << 61, size=n).tolist()
+        pa = ring.from_int_coeffs(a, mods, n)
+        pb = ring.from_int_coeffs(b, mods, n)
+        got = ring.ntt_inverse(ring.poly_mul_pointwise(ring.ntt_forward(pa), ring.ntt_forward(pb))).coeffs
+        for li, m in enumerate(mods):
+            want = _schoolbook([v % m.q for v in a], [v % m.q for v in b], m.q)
+            assert got[li].tolist() == want
