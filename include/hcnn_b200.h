@@ -128,6 +128,13 @@ size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* ctx, uint32_t npolys);
 int hcnn_rescale(hcnn_ctx* ctx, uint64_t* out, const uint64_t* in, uint32_t level, uint32_t npolys, void* ws,
                  void* stream);
 
+/* plane MAC of the HyPHEN convolution (packing.py:600-604, 520-525):
+ * out = [accumulate ? out : 0] + sum_t cts[t] (.) masks[t], ciphertexts at
+ * `level` (2 polys each), masks Montgomery-form [level+1][N] like the
+ * reference's _mask_pt rows; cts/masks are host arrays of device pointers */
+int hcnn_mac_terms(hcnn_ctx* ctx, uint64_t* out_ct, const uint64_t* const* cts, const uint64_t* const* masks_mont,
+                   uint32_t n_terms, uint32_t level, int accumulate, void* stream);
+
 /* ---- instrumentation ------------------------------------------------------ */
 /* count of engine kernels launched since load (all contexts) */
 unsigned long long hcnn_kernel_launches(void);

@@ -9,6 +9,13 @@
 
 namespace hcnn {
 
+static inline dim3 row_grid(u32 work_per_row, u32 rows, u32 threads) {
+  u32 x = (work_per_row + threads - 1) / threads;
+  if (x == 0) x = 1;
+  if (x > 1024) x = 1024;
+  return dim3(x, rows, 1);
+}
+
 // ---------------------------------------------------------------------------
 // element-wise (ring.py:264-314, kernels.py:190-230)
 // grid: x over N/(2*blockDim), y over rows = npolys*nlimbs
@@ -346,6 +353,35 @@ __global__ void k_moddown_combine(u64* __restrict__ out0, u64* __restrict__ out1
 }
 
 // ---------------------------------------------------------------------------
+// plane MAC of the HyPHEN conv (packing.py:600-604 / :520-525):
+// out_z = sum_t ct_t,z (.) mask_t over up to kMacMax terms, masks in
+// Montgomery form -> one 128-bit sum and one REDC per residue (bit-exact
+// with the reference's hadd(pmult_mont) chain since every partial result
+// is canonical).  accumulate: out += sum.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __restrict__ out, u32 nq, u32 logN,
+                                                   int accumulate, const ModConsts* __restrict__ mc) {
+  const u32 N = 1u << logN, r = blockIdx.y, z = blockIdx.z;
+  const u64 q = mc[r].q, ninv = mc[r].ninv;
+  const size_t off = ((size_t)z * nq + r) * N, moff = (size_t)r * N;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    u64 hi = 0, lo = 0;
+    for (int t = 0; t < nt; ++t) mac128(hi, lo, T.ct[t][off + k], T.mask[t][moff + k], q);
+    u64 v = redc128(hi, lo, q, ninv);
+    if (accumulate) v = add_mod(v, out[off + k], q);
+    out[off + k] = v;
+  }
+}
+
+cudaError_t launch_mac_terms(const MacTerms& T, int nt, u64* out, u32 nq, u32 logN, int accumulate,
+                             const ModConsts* mc, cudaStream_t st) {
+  dim3 g = row_grid(1u << logN, nq, 256);
+  g.z = 2;
+  k_mac_terms<<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // rescale (ckks.py:506-528)
 // ---------------------------------------------------------------------------
 // centred lift of the (coefficient-domain) top limb into limbs 0..l-1
@@ -387,12 +423,6 @@ __global__ void k_gather_limb(u64* __restrict__ out, const u64* __restrict__ in,
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
-static inline dim3 row_grid(u32 work_per_row, u32 rows, u32 threads) {
-  u32 x = (work_per_row + threads - 1) / threads;
-  if (x == 0) x = 1;
-  if (x > 1024) x = 1024;
-  return dim3(x, rows, 1);
-}
 
 cudaError_t launch_ew_binary(int op, u64* out, const u64* a, const u64* b, Basis basis, u32 logN, u32 npolys,
                              int b_bcast, const ModConsts* mc, cudaStream_t st) {

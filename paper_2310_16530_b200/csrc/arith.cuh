@@ -33,6 +33,13 @@ cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 n
                                 cudaStream_t st);
 cudaError_t launch_rescale_combine(u64* out, const u64* in, u32 l, u32 logN, u32 npolys, const u64* inv,
                                    const u64* inv_sh, const ModConsts* mc, cudaStream_t st);
+constexpr int kMacMax = 64;
+struct MacTerms {
+  const u64* ct[kMacMax];
+  const u64* mask[kMacMax];
+};
+cudaError_t launch_mac_terms(const MacTerms& T, int nt, u64* out, u32 nq, u32 logN, int accumulate,
+                             const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_gather_limb(u64* out, const u64* in, u32 limb, u32 nlimbs, u32 logN, u32 npolys,
                                cudaStream_t st);
 

@@ -706,6 +706,28 @@ int hcnn_rotate_hoisted(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* ct, 
   return HCNN_OK;
 }
 
+int hcnn_mac_terms(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const uint64_t* const* masks,
+                   uint32_t n_terms, uint32_t level, int accumulate, void* s) {
+  if (!c) return fail(HCNN_E_PARAMETER, "null context");
+  if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
+  const u32 nq = level + 1;
+  if (n_terms == 0) {
+    if (!accumulate) CK(cudaMemsetAsync(out, 0, 2ull * nq * c->n * 8, STREAM(s)));
+    return HCNN_OK;
+  }
+  for (u32 t0 = 0; t0 < n_terms; t0 += kMacMax) {
+    MacTerms T;
+    u32 nt = std::min<u32>(kMacMax, n_terms - t0);
+    for (u32 t = 0; t < nt; ++t) {
+      T.ct[t] = cts[t0 + t];
+      T.mask[t] = masks[t0 + t];
+    }
+    PK("mac_terms", 8.0 * (3.0 * nt + 2 + (accumulate || t0 ? 2 : 0)) * nq * c->n, 1, STREAM(s),
+       launch_mac_terms(T, (int)nt, out, nq, c->logN, accumulate || t0 > 0, c->d_mc, STREAM(s)));
+  }
+  return HCNN_OK;
+}
+
 size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* c, uint32_t npolys) { return (size_t)npolys * c->n * 8; }
 
 int hcnn_rescale(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint32_t level, uint32_t npolys, void* ws,

@@ -221,6 +221,19 @@ class DeviceContext:
                                                _native.u64_array(galois), kb, ka, _ptr(ws), _stream()))
         return outs
 
+    def mac_terms(self, cts: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], level: int,
+                  out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+        """out (+)= sum_t cts[t] (.) masks[t] (Montgomery masks), one fused kernel."""
+        if out is None:
+            out = self.empty(2, level + 1, self.n)
+        n = len(cts)
+        P = ctypes.c_void_p * max(n, 1)
+        cp = P(*[c.data_ptr() for c in cts])
+        mp = P(*[m.data_ptr() for m in masks])
+        self._chk(self.lib.hcnn_mac_terms(self.handle, _ptr(out), cp, mp, n, level, 1 if accumulate else 0,
+                                          _stream()))
+        return out
+
     def rescale(self, a: torch.Tensor, level: int) -> torch.Tensor:
         npolys = self._npolys(a, level + 1, 0, self.n)
         out = self.empty(npolys, level, self.n)
