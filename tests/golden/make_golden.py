@@ -246,7 +246,66 @@ def gen_layers():
     print("tiny done", time.time() - t0)
 
 
+def hf(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(a, dtype=np.float64)).astype("<f8").tobytes()).hexdigest()
+
+
+def gen_host():
+    """Host-side goldens (CPU tests): fixtures, folds, plans, rotation-step
+    sets, layouts -- everything the GPU path consumes as plaintext input."""
+    from hcnn import aespa
+    obj = load_json()
+    res = {"hermite2": list(aespa.hermite_coeffs(2).f_hat), "hermite4": list(aespa.hermite_coeffs(4).f_hat)}
+    fixtures = {}
+    for topo, seed, pname in (("tiny-cnn", 42, "desk-B"), ("basic-block-stack(1)", 21, "desk-A"),
+                              ("basic-block-stack(2)", 7, "desk-A")):
+        params = ckks.params_by_name(pname)
+        fx = graph.gen_fixture(topo, seed, params, golden_count=2)
+        g = graph.build_graph(topo, fx, multiplex=8)
+        ent = {"digest": graph.weights_digest(fx), "golden": fx["golden"],
+               "plan": graph.plan_levels(g, params.max_level).as_dict(),
+               "plan_t5": graph.plan_levels(g, 7, 5).as_dict(),
+               "steps": sorted(graph.required_rotation_steps(g, params.slots)),
+               "steps_fixed": sorted(graph.required_rotation_steps(g, params.slots, include_fixed=True)),
+               "layers": []}
+        for L in g.layers:
+            row = {"kind": L.kind, "fold_forward": L.fold_forward}
+            if L.kind == "conv":
+                row["eff_w"] = hf(L.spec.effective_weights())
+                row["bias_map"] = None if L.spec.bias_map is None else hf(L.spec.bias_map)
+                row["low_scale_out"] = L.spec.low_scale_out
+            if L.kind == "act":
+                row["quads"] = [[q.a, q.b, q.c] for q in L.quads]
+            ent["layers"].append(row)
+        x = np.asarray(fx["golden"][0]["input"])
+        plan = graph.plan_levels(g, params.max_level)
+        ent["plain_out"] = hf(graph.execute(g, plan, x, mode="plaintext-ref")[0])
+        fixtures[f"{topo}|{seed}|{pname}"] = ent
+    res["fixtures"] = fixtures
+    lay = {}
+    rng = np.random.default_rng(11)
+    for fa, shape, slots in ((("B", 4, 1, 4), (4, 2, 2), 32), (("A", 4, 1, 16), (4, 4, 4), 256),
+                             (("B", 2, 2, 16), (3, 2, 2), 256), (("B", 8, 2, 64), (12, 4, 4), 1024)):
+        fmt = packing.PackingFormat(*fa)
+        t = rng.uniform(-1, 1, shape)
+        L = packing.Layout(fmt, packing.TensorShape(*shape), slots)
+        lay["|".join(map(str, fa + shape + (slots,)))] = {
+            "input": t.tolist(),
+            "pack": [hf(v) for v in packing.pack(t, fmt, slots)],
+            "occ": [hf(L.occupancy(i)) for i in range(L.n_cts)],
+            "pool_fc_steps": sorted(packing.pool_fc_rotation_steps(packing.TensorShape(*shape), fmt, slots,
+                                                                   shape[0], 3)),
+        }
+    res["layouts"] = lay
+    res["meta"] = meta()
+    obj["host"] = res
+    save_json(obj)
+    print("host done")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "deskA", "bench16", "layers"]
+    which = sys.argv[1:] or ["small", "deskA", "bench16", "layers", "host"]
     for w in which:
-        {"small": gen_small, "deskA": gen_deska, "bench16": gen_bench16, "layers": gen_layers}[w]()
+        {"small": gen_small, "deskA": gen_deska, "bench16": gen_bench16, "layers": gen_layers,
+         "host": gen_host}[w]()
