@@ -93,6 +93,10 @@ int hcnn_from_mont(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, uint32_t nq,
 /* _scalar_mul_rows ckks.py:350-356: limb i times consts[i] (host array, any value, reduced here) */
 int hcnn_scalar_mul(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* consts, uint32_t nq,
                     uint32_t np, uint32_t npolys, void* stream);
+/* + consts[i] on every residue of limb i: adds the constant polynomial
+ * (evaluation domain), used for exact constant terms in polynomial evaluation */
+int hcnn_scalar_add(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* consts, uint32_t nq,
+                    uint32_t np, uint32_t npolys, void* stream);
 /* signed int64 coefficient rows [npolys][N] (device) -> residues in every limb:
  * sample_poly replication ring.py:463-467, encode reduction ckks.py:284-288 */
 int hcnn_from_signed(hcnn_ctx* ctx, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np, uint32_t npolys,

@@ -52,6 +52,7 @@ SIGNATURES = {
     "hcnn_to_mont": (_INT, [_VP, _VP, _VP, _U32, _U32, _U32, _VP]),
     "hcnn_from_mont": (_INT, [_VP, _VP, _VP, _U32, _U32, _U32, _VP]),
     "hcnn_scalar_mul": (_INT, [_VP, _VP, _VP, _PU64, _U32, _U32, _U32, _VP]),
+    "hcnn_scalar_add": (_INT, [_VP, _VP, _VP, _PU64, _U32, _U32, _U32, _VP]),
     "hcnn_from_signed": (_INT, [_VP, _VP, _VP, _U32, _U32, _U32, _VP]),
     "hcnn_automorphism": (_INT, [_VP, _VP, _VP, _U64, _INT, _U32, _U32, _U32, _VP]),
     "hcnn_base_convert": (_INT, [_VP, _VP, _VP, _PU32, _U32, _PU32, _U32, _U32, _VP]),

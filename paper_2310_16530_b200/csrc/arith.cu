@@ -83,7 +83,7 @@ __global__ void k_ew_unary(int op, u64* __restrict__ out, const u64* __restrict_
   const ulonglong2* A = reinterpret_cast<const ulonglong2*>(a + off);
   ulonglong2* O = reinterpret_cast<ulonglong2*>(out + off);
   u64 w = 0, wp = 0;
-  if (op == EW_SCALAR) {
+  if (op == EW_SCALAR || op == EW_SCALAR_ADD) {
     w = consts[rc.r];
     wp = consts_sh[rc.r];
   }
@@ -101,6 +101,10 @@ __global__ void k_ew_unary(int op, u64* __restrict__ out, const u64* __restrict_
       case EW_FROM_MONT:
         o.x = mont_mul(x.x, 1ull, C.q, C.ninv);
         o.y = mont_mul(x.y, 1ull, C.q, C.ninv);
+        break;
+      case EW_SCALAR_ADD:  // + per-limb constant (constant polynomial in the eval domain)
+        o.x = add_mod(x.x, w, C.q);
+        o.y = add_mod(x.y, w, C.q);
         break;
       default:  // EW_SCALAR
         o.x = shoup_mul(x.x, w, wp, C.q);

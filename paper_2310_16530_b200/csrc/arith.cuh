@@ -4,7 +4,7 @@
 namespace hcnn {
 
 enum { EW_ADD = 0, EW_SUB = 1, EW_MUL_MONT = 2, EW_MUL = 3, EW_MAC_MONT = 4 };
-enum { EW_NEG = 0, EW_TO_MONT = 1, EW_FROM_MONT = 2, EW_SCALAR = 3 };
+enum { EW_NEG = 0, EW_TO_MONT = 1, EW_FROM_MONT = 2, EW_SCALAR = 3, EW_SCALAR_ADD = 4 };
 
 cudaError_t launch_ew_binary(int op, u64* out, const u64* a, const u64* b, Basis basis, u32 logN, u32 npolys,
                              int b_bcast, const ModConsts* mc, cudaStream_t st);

@@ -507,8 +507,21 @@ int hcnn_from_mont(hcnn_ctx* c, uint64_t* out, const uint64_t* a, uint32_t nq, u
   return unop(c, EW_FROM_MONT, out, a, nq, np, npolys, s);
 }
 
+static int scalar_op(hcnn_ctx* c, int op, uint64_t* out, const uint64_t* a, const uint64_t* consts, uint32_t nq,
+                     uint32_t np, uint32_t npolys, void* s);
+
 int hcnn_scalar_mul(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* consts, uint32_t nq,
                     uint32_t np, uint32_t npolys, void* s) {
+  return scalar_op(c, EW_SCALAR, out, a, consts, nq, np, npolys, s);
+}
+
+int hcnn_scalar_add(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* consts, uint32_t nq,
+                    uint32_t np, uint32_t npolys, void* s) {
+  return scalar_op(c, EW_SCALAR_ADD, out, a, consts, nq, np, npolys, s);
+}
+
+static int scalar_op(hcnn_ctx* c, int op, uint64_t* out, const uint64_t* a, const uint64_t* consts, uint32_t nq,
+                     uint32_t np, uint32_t npolys, void* s) {
   int rc = check_basis(c, nq, np);
   if (rc) return rc;
   Basis b = c->basis(nq, np);
@@ -524,7 +537,7 @@ int hcnn_scalar_mul(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_
   CK(cudaMallocAsync((void**)&d, 2 * nl * 8, STREAM(s)));
   CK(cudaMemcpyAsync(d, h.data(), 2 * nl * 8, cudaMemcpyHostToDevice, STREAM(s)));
   PK("ew_scalar", 16.0 * nl * npolys * c->n, 1, STREAM(s),
-     launch_ew_unary(EW_SCALAR, out, a, b, c->logN, npolys, c->d_mc, d, d + nl, STREAM(s)));
+     launch_ew_unary(op, out, a, b, c->logN, npolys, c->d_mc, d, d + nl, STREAM(s)));
   CK(cudaFreeAsync(d, STREAM(s)));
   // the host vector must outlive the (pageable, synchronous-to-host) copy
   return HCNN_OK;

@@ -148,14 +148,15 @@ class DeviceContext:
         return out
 
     def scalar_mul(self, a: torch.Tensor, consts: Sequence[int], nq: int, np_: int = 0,
-                   out: torch.Tensor | None = None) -> torch.Tensor:
+                   out: torch.Tensor | None = None, add: bool = False) -> torch.Tensor:
+        """limb i times consts[i] (or, with add=True, plus consts[i])."""
         npolys = self._npolys(a, nq, np_, self.n)
         if len(consts) != nq + np_:
             raise BasisError("one constant per limb required")
         if out is None:
             out = torch.empty_like(a)
-        self._chk(self.lib.hcnn_scalar_mul(self.handle, _ptr(out), _ptr(a), _native.u64_array(consts),
-                                           nq, np_, npolys, _stream()))
+        fn = self.lib.hcnn_scalar_add if add else self.lib.hcnn_scalar_mul
+        self._chk(fn(self.handle, _ptr(out), _ptr(a), _native.u64_array(consts), nq, np_, npolys, _stream()))
         return out
 
     def from_signed(self, rows: torch.Tensor, nq: int, np_: int = 0) -> torch.Tensor:

@@ -1,0 +1,80 @@
+"""Plaintext simulation of every bootstrapping stage (CPU).  Bootstrapping
+has no reference implementation (parity unpinned); these checks pin the
+linear algebra and the EvalMod polynomial before any homomorphic run."""
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_2310_16530_b200 import bootstrap as bt
+
+
+@pytest.mark.parametrize("n_ring", [16, 32, 256])
+def test_special_fft_factorises_embedding(n_ring):
+    n = n_ring // 2
+    u0 = bt.embedding_matrix(n_ring)
+    prod = np.eye(n, dtype=complex)
+    for s in range(1, n.bit_length()):
+        prod = bt.special_fft_stage(n, 1 << s).toarray() @ prod
+    br = bt.bit_reverse_perm(n)
+    perm = np.zeros((n, n))
+    perm[np.arange(n), br] = 1
+    assert np.allclose(prod @ perm, u0)
+
+
+def test_embedding_matches_reference_encoding():
+    """slot j = m(zeta^(5^j)): decode of the engine's encode is U0 applied to
+    (t_lo + i t_hi)/scale (ckks.py:241-308 conventions)."""
+    from paper_2310_16530_b200 import ckks
+    params = ckks.CkksParams.build("t", 64, 50, 40, 2, 50, 2)
+    rng = np.random.default_rng(0)
+    vals = rng.uniform(-1, 1, params.slots)
+    t = ckks.encode_coeffs(vals, params, 0, 2.0 ** 30).astype(float)
+    n = params.slots
+    u = (t[:n] + 1j * t[n:]) / 2.0 ** 30
+    assert np.max(np.abs(bt.embedding_matrix(params.n) @ u - vals)) < 1e-6
+
+
+@pytest.mark.parametrize("n_ring,stages", [(64, (2, 3)), (256, (3, 2, 2)), (1 << 12, (4, 4, 3))])
+def test_cts_stc_round_trip_and_cts_output(n_ring, stages):
+    n = n_ring // 2
+    rng = np.random.default_rng(1)
+    t = rng.normal(size=2 * n)
+    coeffs = t[:n] + 1j * t[n:]
+    w = bt.embedding_matrix(n_ring) @ coeffs
+    cts = [bt.diag_plan(m) for m in bt.cts_groups(n, stages, 0.5)]
+    stc = [bt.diag_plan(m) for m in bt.stc_groups(n, stages[::-1], 2.0 / n)]
+    u = bt.apply_plain(cts, w)
+    br = bt.bit_reverse_perm(n)
+    assert np.allclose(u, 0.5 * n * coeffs[br])
+    assert np.allclose(bt.apply_plain(stc, u), w)
+    # unit-magnitude diagonal entries (precision of the plaintext products)
+    for plans, c0 in ((cts, 0.5), (stc, 2.0 / n)):
+        for i, p in enumerate(plans):
+            mags = np.concatenate([np.abs(pre) for terms in p.giants.values() for _, pre in terms])
+            nz = mags[mags > 1e-12]
+            assert np.allclose(nz, c0 if i == 0 else 1.0)
+    # BSGS uses few rotations per level
+    for p in cts:
+        assert len(p.babies) + len(p.giants) <= 2 * (1 << max(stages)) + 2
+
+
+def test_evalmod_polynomial_accuracy():
+    cfg = bt.BootConfig()
+    rng = np.random.default_rng(2)
+    I = rng.integers(-cfg.k_bound + 1, cfg.k_bound, size=4000)
+    eps = rng.uniform(-2.0 ** -10, 2.0 ** -10, size=4000)
+    x = I + eps
+    got = bt.evalmod_plain(cfg, x / (cfg.k_bound + 1))
+    assert np.max(np.abs(got - np.sin(2 * np.pi * x))) < 1e-9
+    # sin(2 pi eps)/(2 pi) ~ eps to the cubic term
+    assert np.max(np.abs(got / (2 * np.pi) - eps)) < 1e-7
+
+
+def test_depth_budget_and_chain():
+    cfg = bt.BootConfig()
+    assert cfg.depth() == 3 + (math.ceil(math.log2(cfg.degree)) + 1) + cfg.double_angle + 3
+    p = bt.boot_params("b", 1 << 12, 4, bt.BootConfig(cts_stages=(4, 4, 3), stc_stages=(3, 4, 4)))
+    assert p.max_level == 4 + 3 + cfg.evalmod_depth() + 3
+    assert all(m.q.bit_length() <= 61 for m in p.q_mods + p.p_mods)

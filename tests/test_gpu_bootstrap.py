@@ -1,0 +1,59 @@
+"""Homomorphic bootstrapping on the B200 (BASELINE config 3).
+No reference exists (parity unpinned): checked by decrypt-and-compare
+against the input slot values, stage by stage."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def boot12():
+    from paper_2310_16530_b200 import bootstrap as bt, ckks
+    cfg = bt.BootConfig(cts_stages=(4, 4, 3), stc_stages=(3, 4, 4))
+    params = bt.boot_params("boot12", 1 << 12, 4, cfg)
+    b = bt.Bootstrapper(params, cfg)
+    ks = b.keygen(np.random.default_rng(7), rotations=[1])
+    return params, cfg, b, ks
+
+
+def test_mod_raise_and_cts(boot12):
+    """After ModRaise + CoeffToSlot the slots hold (t_lo + i t_hi)/(2 q0 B)
+    with t = m + q0*I, I small integers."""
+    from paper_2310_16530_b200 import bootstrap as bt, ckks
+    params, cfg, b, ks = boot12
+    rng = np.random.default_rng(1)
+    vals = rng.uniform(-1, 1, params.slots)
+    ct = ckks.encrypt(ckks.encode(vals, params, 0), ks, rng)
+    u, delta1 = b.coeff_to_slot(ct, ks)
+    assert u.level == params.max_level - len(cfg.cts_stages)
+    got = ckks.decode(ckks.decrypt(u, ks), params, imag_tol=None)  # real parts only
+    # plaintext expectation from the coefficient vector of m' (scaled-up message)
+    t = ckks.encode_coeffs(vals, params, 0, delta1).astype(float)
+    n = params.slots
+    br = bt.bit_reverse_perm(n)
+    frac = (t[:n] / b.q0)[br]
+    # real part of slot = (t_lo + q0 I)/(2 q0 B): the fractional offset must match mod 1/(2B)
+    r = got * 2 * b.B
+    assert np.max(np.abs((r - frac) - np.round(r - frac))) < 1e-6
+    assert np.max(np.abs(np.round(r - frac))) <= cfg.k_bound
+
+
+def test_bootstrap_round_trip(boot12):
+    from paper_2310_16530_b200 import ckks
+    params, cfg, b, ks = boot12
+    rng = np.random.default_rng(2)
+    vals = rng.uniform(-1, 1, params.slots)
+    ct = ckks.encrypt(ckks.encode(vals, params, 2), ks, rng)
+    out = b.bootstrap(ct, ks)
+    assert out.level == b.output_level == params.max_level - cfg.depth()
+    assert abs(out.scale - ct.scale) < 1e-6 * ct.scale
+    got = ckks.decode(ckks.decrypt(out, ks), params, imag_tol=None)
+    err = float(np.max(np.abs(got - vals)))
+    print("bootstrap max abs error", err)
+    assert err < 1e-3
+    # the refreshed ciphertext keeps computing: square it
+    sq = ckks.rescale(ckks.hmult(out, out, ks), params)
+    got2 = ckks.decode(ckks.decrypt(sq, ks), params, imag_tol=None)
+    assert np.max(np.abs(got2 - vals * vals)) < 2e-3
