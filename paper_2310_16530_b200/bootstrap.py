@@ -363,15 +363,18 @@ class Bootstrapper:
 
     def _apply(self, ct: Ciphertext, plans: list[DiagPlan], ks: KeySet, tag,
                final_scale: float | None = None) -> Ciphertext:
-        """Apply the level matrices; all but the last keep the scale (plaintext
-        scale = q_l), the last lands on final_scale (None: keep)."""
+        """Apply the level matrices.  The scale moves geometrically from the
+        input scale to final_scale (None: keep) so every level's plaintext
+        scale stays close to its prime -- the precision of the product."""
         ctx = self.params.ctx
+        nlev = len(plans)
+        ratio = 1.0 if final_scale is None else (final_scale / ct.scale) ** (1.0 / nlev)
         for li, p in enumerate(plans):
             lvl = ct.level
             if lvl < 1:
                 raise LevelError("linear transform ran out of levels")
             q = self.params.q_mods[lvl].q
-            tgt = final_scale if (li == len(plans) - 1 and final_scale is not None) else ct.scale
+            tgt = final_scale if (li == nlev - 1 and final_scale is not None) else ct.scale * ratio
             s_d = tgt * q / ct.scale
             rots = dict(zip(p.babies, ckks.rotate_many(ct, p.babies, ks)))
             acc = None

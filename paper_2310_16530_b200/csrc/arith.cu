@@ -390,11 +390,11 @@ cudaError_t launch_mac_terms(const MacTerms& T, int nt, u64* out, u32 nq, u32 lo
 // ---------------------------------------------------------------------------
 // centred lift of the (coefficient-domain) top limb into limbs 0..l-1
 __global__ void k_rescale_lift(u64* __restrict__ out, const u64* __restrict__ top, u32 l, u32 logN,
-                               const ModConsts* __restrict__ mc) {
+                               const u64* __restrict__ qtop_mod, const ModConsts* __restrict__ mc) {
   const u32 N = 1u << logN, i = blockIdx.y, z = blockIdx.z;
   const ModConsts C = mc[i];
   const u64 qt = mc[l].q;
-  const u64 qt_mod = qt % C.q;  // uniform
+  const u64 qt_mod = qtop_mod[i];  // q_l mod q_i (host table)
   const u64* T = top + (size_t)z * N;
   u64* O = out + ((size_t)z * l + i) * N;
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
@@ -548,11 +548,11 @@ cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u
   return cudaGetLastError();
 }
 
-cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 npolys, const ModConsts* mc,
-                                cudaStream_t st) {
+cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 npolys, const u64* qtop_mod,
+                                const ModConsts* mc, cudaStream_t st) {
   dim3 g = row_grid(1u << logN, l, 256);
   g.z = npolys;
-  k_rescale_lift<<<g, 256, 0, st>>>(out, top, l, logN, mc);
+  k_rescale_lift<<<g, 256, 0, st>>>(out, top, l, logN, qtop_mod, mc);
   return cudaGetLastError();
 }
 

@@ -29,8 +29,8 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
 cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,
                                    const u64* add1, u64 g_add, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
                                    const u64* pinv_sh, const ModConsts* mc, cudaStream_t st);
-cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 npolys, const ModConsts* mc,
-                                cudaStream_t st);
+cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 npolys, const u64* qtop_mod,
+                                const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_rescale_combine(u64* out, const u64* in, u32 l, u32 logN, u32 npolys, const u64* inv,
                                    const u64* inv_sh, const ModConsts* mc, cudaStream_t st);
 constexpr int kMacMax = 64;

@@ -53,6 +53,7 @@ struct hcnn_ctx {
   FbcStore moddown;                  // P -> q_0..q_{Lq-1}
   u64 *d_pinv = nullptr, *d_pinv_sh = nullptr;  // P^-1 mod q_i
   u64 *d_rinv = nullptr, *d_rinv_sh = nullptr;  // [l][i] q_l^-1 mod q_i
+  u64* d_qmod = nullptr;                         // [l][i] q_l mod q_i
   std::mutex mu;
   std::map<u32, ModupSet> modup;
   std::map<std::vector<u32>, FbcStore> generic;
@@ -356,14 +357,17 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
     CK(cudaMemcpy(c->d_ictw, ictw.data(), ictw.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice));
   }
   // rescale table: q_l^-1 mod q_i
-  std::vector<u64> rinv((size_t)n_q * n_q, 0), rinv_sh((size_t)n_q * n_q, 0);
+  std::vector<u64> rinv((size_t)n_q * n_q, 0), rinv_sh((size_t)n_q * n_q, 0), qmod((size_t)n_q * n_q, 0);
   for (u32 l = 1; l < n_q; ++l)
     for (u32 i = 0; i < l; ++i) {
       u64 qi = c->mods[i];
       u64 v = h_invmod(c->mods[l] % qi, qi);
       rinv[(size_t)l * n_q + i] = v;
       rinv_sh[(size_t)l * n_q + i] = h_shoup(v, qi);
+      qmod[(size_t)l * n_q + i] = c->mods[l] % qi;
     }
+  CK(cudaMalloc(&c->d_qmod, qmod.size() * 8));
+  CK(cudaMemcpy(c->d_qmod, qmod.data(), qmod.size() * 8, cudaMemcpyHostToDevice));
   CK(cudaMalloc(&c->d_rinv, rinv.size() * 8));
   CK(cudaMalloc(&c->d_rinv_sh, rinv.size() * 8));
   CK(cudaMemcpy(c->d_rinv, rinv.data(), rinv.size() * 8, cudaMemcpyHostToDevice));
@@ -408,6 +412,7 @@ void hcnn_ctx_destroy(hcnn_ctx* c) {
   cudaFree(c->d_pinv_sh);
   cudaFree(c->d_rinv);
   cudaFree(c->d_rinv_sh);
+  cudaFree(c->d_qmod);
   cudaFree(c->moddown.mem);
   cudaFree(c->moddown.d_dev);
   for (auto& kv : c->modup) {
@@ -757,7 +762,7 @@ int hcnn_rescale(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint32_t level,
   m.basis = c->basis(l + 1, 0);
   m.first_limb = l;
   PK("ntt_inv", 16.0 * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), m, 1, npolys, true, STREAM(s)));
-  PK("rescale_lift", 8.0 * (l + 1) * npolys * c->n, 1, STREAM(s), launch_rescale_lift(out, top, l, c->logN, npolys, c->d_mc, STREAM(s)));
+  PK("rescale_lift", 8.0 * (l + 1) * npolys * c->n, 1, STREAM(s), launch_rescale_lift(out, top, l, c->logN, npolys, c->d_qmod + (size_t)l * c->Lq, c->d_mc, STREAM(s)));
   LimbMap o{};
   o.base = out;
   o.poly_stride = (size_t)l * c->n;
