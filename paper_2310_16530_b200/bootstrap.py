@@ -343,8 +343,10 @@ class Bootstrapper:
 
     def keygen(self, rng: np.random.Generator, rotations=()) -> KeySet:
         steps = sorted(set(rotations) | self.rotation_steps())
-        return ckks.keygen(self.params, rng, rotations=steps, secret_weight=self.cfg.secret_weight,
-                           conjugation=True)
+        ks = ckks.keygen(self.params, rng, rotations=steps, secret_weight=self.cfg.secret_weight,
+                         conjugation=True)
+        ks.bootstrapper = self
+        return ks
 
     # -- linear transforms ----------------------------------------------------
     def _scale_bits(self, in_scale: float) -> int:

@@ -57,3 +57,27 @@ def test_bootstrap_round_trip(boot12):
     sq = ckks.rescale(ckks.hmult(out, out, ks), params)
     got2 = ckks.decode(ckks.decrypt(sq, ks), params, imag_tol=None)
     assert np.max(np.abs(got2 - vals * vals)) < 2e-3
+
+
+def test_graph_refresh_slot_bootstraps():
+    """Two stacked basic blocks need a refresh between them (6 levels each):
+    the executor's refresh slot bootstraps (no decryption), and the result
+    matches the plaintext mirror."""
+    from paper_2310_16530_b200 import bootstrap as bt, graph, packing
+    cfg = bt.BootConfig(cts_stages=(4, 4, 4), stc_stages=(4, 4, 4))
+    params = bt.boot_params("boot13", 1 << 13, 6, cfg)
+    b = bt.Bootstrapper(params, cfg)
+    fx = graph.gen_fixture("basic-block-stack(2)", 5, params)
+    g = graph.build_graph("basic-block-stack(2)", fx, multiplex=8)
+    plan = graph.plan_levels(g, b.output_level, refresh_target=b.output_level)
+    assert plan.refresh_points
+    ks = b.keygen(np.random.default_rng(9), rotations=sorted(graph.required_rotation_steps(g, params.slots)))
+    x = np.asarray(fx["golden"][0]["input"])
+    packed = packing.encrypt_tensor(x, g.input_format, ks, np.random.default_rng(4), plan.entry_levels[0])
+    out, rep = graph.execute(g, plan, packed, ks, "encrypted")
+    assert rep.totals().refreshes > 0
+    dec = packing.decrypt_tensor(out, ks)
+    ref, _ = graph.execute(g, plan, x, mode="plaintext-ref")
+    err = float(np.max(np.abs(dec - ref)))
+    print("stack(2) with bootstrapping: max abs err", err)
+    assert err < 1e-3
