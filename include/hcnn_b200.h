@@ -142,6 +142,10 @@ int hcnn_mac_terms(hcnn_ctx* ctx, uint64_t* out_ct, const uint64_t* const* cts, 
 /* ---- instrumentation ------------------------------------------------------ */
 /* count of engine kernels launched since load (all contexts) */
 unsigned long long hcnn_kernel_launches(void);
+/* process-wide tuning knobs: "ntt_group_limbs" (NTT pass pairs run on groups
+ * of this many limbs so the inter-pass data stays in L2; 0 = whole batch),
+ * "ntt_hints" (1 = evict-last twiddles / streaming data loads) */
+int hcnn_set_option(const char* name, long long value);
 /* when enabled, every launch is bracketed by CUDA events on its stream */
 void hcnn_profile_enable(int on);
 /* per-kernel totals as JSON {"name": [launches, ms, algorithmic_bytes, kernels]};

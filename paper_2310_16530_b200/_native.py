@@ -66,6 +66,7 @@ SIGNATURES = {
     "hcnn_mac_terms": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _U32, _U32, _INT, _VP]),
     "hcnn_kernel_launches": (ctypes.c_ulonglong, []),
     "hcnn_profile_enable": (None, [_INT]),
+    "hcnn_set_option": (_INT, [ctypes.c_char_p, ctypes.c_longlong]),
     "hcnn_profile_read": (_INT, [ctypes.c_char_p, _SZ, _INT]),
 }
 
@@ -114,6 +115,10 @@ def check(rc: int) -> None:
 
 def kernel_launches() -> int:
     return int(load().hcnn_kernel_launches())
+
+
+def set_option(name: str, value: int) -> None:
+    check(load().hcnn_set_option(name.encode(), int(value)))
 
 
 def profile_enable(on: bool) -> None:

@@ -180,6 +180,7 @@ __global__ void k_tensor(u64* __restrict__ d0, u64* __restrict__ d1, u64* __rest
 // centred fast base conversion (ring.py:378-398, kernels.py:283-301)
 // ---------------------------------------------------------------------------
 #define FBC_MAX_SRC 64
+constexpr u32 kFbcTG = 128;  // targets per CTA in k_fbc_t (splitting measured slower)
 
 __device__ __forceinline__ void fbc_point(const FbcDev& T, const ModConsts* __restrict__ mc,
                                           const u64* __restrict__ src, size_t src_limb_stride,
@@ -241,20 +242,24 @@ __global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, 
   extern __shared__ u64 sh[];
   const u32 N = 1u << logN, z = blockIdx.y + z0;
   const FbcDev& T = tabs[tab_per_z ? z : 0];
-  const u32 nt = nt_override ? nt_override : T.nt;
+  const u32 nt_all = nt_override ? nt_override : T.nt;
+  // blockIdx.z selects a group of kFbcTG targets (more CTAs; y recomputed)
+  const u32 t0 = blockIdx.z * kFbcTG;
+  if (t0 >= nt_all) return;
+  const u32 nt = nt_all - t0 < kFbcTG ? nt_all - t0 : kFbcTG;
   u64* s_q = sh;
   u64* s_ninv = s_q + nt;
   u64* s_pos = s_ninv + nt;
   u64* s_tm = s_pos + nt;        // [nt][NS]
   u64* s_corr = s_tm + nt * NS;  // [nt][NM]
   for (u32 t = threadIdx.x; t < nt; t += blockDim.x) {
-    const u32 m = T.dst_mod[t];
+    const u32 m = T.dst_mod[t0 + t];
     s_q[t] = mc[m].q;
     s_ninv[t] = mc[m].ninv;
-    s_pos[t] = (u64)T.dst_pos[t] * N;
+    s_pos[t] = (u64)T.dst_pos[t0 + t] * N;
   }
-  for (u32 e = threadIdx.x; e < nt * NS; e += blockDim.x) s_tm[e] = T.tmat[e];
-  for (u32 e = threadIdx.x; e < nt * NM; e += blockDim.x) s_corr[e] = T.corr[e];
+  for (u32 e = threadIdx.x; e < nt * NS; e += blockDim.x) s_tm[e] = T.tmat[(size_t)t0 * NS + e];
+  for (u32 e = threadIdx.x; e < nt * NM; e += blockDim.x) s_corr[e] = T.corr[(size_t)t0 * NM + e];
   u64 qi[NS], hq[NS], ip[NS], ips[NS];
 #pragma unroll
   for (int i = 0; i < NS; ++i) {
@@ -274,6 +279,7 @@ __global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, 
       y[i] = shoup_mul(src[(size_t)i * N + k], ip[i], ips[i], qi[i]);
       mask |= (y[i] > hq[i] ? 1u : 0u) << i;
     }
+#pragma unroll 4
     for (u32 t = 0; t < nt; ++t) {
       const u64 qt = s_q[t];
       u64 hi = 0, lo = 0;
@@ -309,36 +315,52 @@ __global__ void k_modup(const FbcDev* __restrict__ tabs, const ModConsts* __rest
 // (key rows are Montgomery form, so the 128-bit sum REDCs straight to the
 // ordinary residue).  g != 1 applies the eval-domain Galois permutation to
 // the raised digits on the fly (hoisted rotation).
-__global__ void k_ks_inner(u64* __restrict__ acc, const u64* __restrict__ x_eval, const u64* __restrict__ raised,
-                           const u64* __restrict__ key_b, const u64* __restrict__ key_a, Basis basis, u32 alpha,
-                           u32 ndig, u32 logN, u64 g, const ModConsts* __restrict__ mc) {
+__global__ void __launch_bounds__(256) k_ks_inner(u64* __restrict__ acc, const u64* __restrict__ x_eval,
+                                                  const u64* __restrict__ raised, const u64* __restrict__ key_b,
+                                                  const u64* __restrict__ key_a, Basis basis, u32 alpha, u32 ndig,
+                                                  u32 logN, u64 g, const ModConsts* __restrict__ mc) {
   const u32 N = 1u << logN, r = blockIdx.y;
   const u32 n_ext = basis.nlimbs();
   const u32 mod = basis.mod_of(r);
-  const ModConsts C = mc[mod];
+  const u64 q = mc[mod].q, ninv = mc[mod].ninv;
   const size_t key_dst = (size_t)(basis.Lq + basis.np) * N;  // per-digit key stride
-  // digit owning limb r (only q limbs belong to digits)
-  const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;
-  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
-    const u32 ks = g == 1 ? k : galois_src(k, g, logN);
-    u64 bhi = 0, blo = 0, ahi = 0, alo = 0;
+  const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;     // digit owning limb r
+  // two adjacent coefficients per thread: 16-byte key / raised / acc accesses
+  for (u32 k2 = blockIdx.x * blockDim.x + threadIdx.x; k2 < N / 2; k2 += gridDim.x * blockDim.x) {
+    const u32 k = 2 * k2;
+    u64 bh0 = 0, bl0 = 0, ah0 = 0, al0 = 0, bh1 = 0, bl1 = 0, ah1 = 0, al1 = 0;
+#pragma unroll 2
     for (u32 j = 0; j < ndig; ++j) {
-      u64 v = (j == own) ? x_eval[(size_t)r * N + ks] : raised[((size_t)j * n_ext + r) * N + ks];
+      const u64* src = (j == own) ? x_eval + (size_t)r * N : raised + ((size_t)j * n_ext + r) * N;
+      ulonglong2 v;
+      if (g == 1) {
+        v = *reinterpret_cast<const ulonglong2*>(src + k);
+      } else {
+        v.x = src[galois_src(k, g, logN)];
+        v.y = src[galois_src(k + 1, g, logN)];
+      }
       const size_t kofs = (size_t)j * key_dst + (size_t)mod * N + k;
-      mac128(bhi, blo, v, key_b[kofs], C.q);
-      mac128(ahi, alo, v, key_a[kofs], C.q);
+      const ulonglong2 kb = *reinterpret_cast<const ulonglong2*>(key_b + kofs);
+      const ulonglong2 ka = *reinterpret_cast<const ulonglong2*>(key_a + kofs);
+      mac128(bh0, bl0, v.x, kb.x, q);
+      mac128(bh1, bl1, v.y, kb.y, q);
+      mac128(ah0, al0, v.x, ka.x, q);
+      mac128(ah1, al1, v.y, ka.y, q);
     }
-    acc[(size_t)r * N + k] = redc128(bhi, blo, C.q, C.ninv);
-    acc[((size_t)n_ext + r) * N + k] = redc128(ahi, alo, C.q, C.ninv);
+    *reinterpret_cast<ulonglong2*>(acc + (size_t)r * N + k) =
+        make_ulonglong2(redc128(bh0, bl0, q, ninv), redc128(bh1, bl1, q, ninv));
+    *reinterpret_cast<ulonglong2*>(acc + ((size_t)n_ext + r) * N + k) =
+        make_ulonglong2(redc128(ah0, al0, q, ninv), redc128(ah1, al1, q, ninv));
   }
 }
 
 // ModDown combine (ckks.py:593-601): out_z[r] = add_z[perm(k)] + (acc_z[r] - lift_z[r]) * P^-1
-__global__ void k_moddown_combine(u64* __restrict__ out0, u64* __restrict__ out1, const u64* __restrict__ acc,
-                                  const u64* __restrict__ lift, const u64* __restrict__ add0,
-                                  const u64* __restrict__ add1, u64 g_add, u32 nq, u32 n_ext, u32 logN,
-                                  const u64* __restrict__ pinv, const u64* __restrict__ pinv_sh,
-                                  const ModConsts* __restrict__ mc) {
+__global__ void __launch_bounds__(256) k_moddown_combine(u64* __restrict__ out0, u64* __restrict__ out1,
+                                                         const u64* __restrict__ acc, const u64* __restrict__ lift,
+                                                         const u64* __restrict__ add0, const u64* __restrict__ add1,
+                                                         u64 g_add, u32 nq, u32 n_ext, u32 logN,
+                                                         const u64* __restrict__ pinv, const u64* __restrict__ pinv_sh,
+                                                         const ModConsts* __restrict__ mc) {
   const u32 N = 1u << logN, r = blockIdx.y, z = blockIdx.z;
   const u64 q = mc[r].q;
   const u64 w = pinv[r], wp = pinv_sh[r];
@@ -346,13 +368,24 @@ __global__ void k_moddown_combine(u64* __restrict__ out0, u64* __restrict__ out1
   const u64* L = lift + ((size_t)z * nq + r) * N;
   const u64* ADD = z == 0 ? add0 : add1;
   u64* O = (z == 0 ? out0 : out1) + (size_t)r * N;
-  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
-    u64 v = shoup_mul(sub_mod(A[k], L[k], q), w, wp, q);
+  for (u32 k2 = blockIdx.x * blockDim.x + threadIdx.x; k2 < N / 2; k2 += gridDim.x * blockDim.x) {
+    const u32 k = 2 * k2;
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(A + k);
+    const ulonglong2 l = *reinterpret_cast<const ulonglong2*>(L + k);
+    u64 v0 = shoup_mul(sub_mod(a.x, l.x, q), w, wp, q);
+    u64 v1 = shoup_mul(sub_mod(a.y, l.y, q), w, wp, q);
     if (ADD) {
-      u32 ks = g_add == 1 ? k : galois_src(k, g_add, logN);
-      v = add_mod(v, ADD[(size_t)r * N + ks], q);
+      const u64* ar = ADD + (size_t)r * N;
+      if (g_add == 1) {
+        const ulonglong2 d = *reinterpret_cast<const ulonglong2*>(ar + k);
+        v0 = add_mod(v0, d.x, q);
+        v1 = add_mod(v1, d.y, q);
+      } else {
+        v0 = add_mod(v0, ar[galois_src(k, g_add, logN)], q);
+        v1 = add_mod(v1, ar[galois_src(k + 1, g_add, logN)], q);
+      }
     }
-    O[k] = v;
+    *reinterpret_cast<ulonglong2*>(O + k) = make_ulonglong2(v0, v1);
   }
 }
 
@@ -468,7 +501,10 @@ cudaError_t launch_tensor(u64* d0, u64* d1, u64* d2, const u64* a, const u64* b,
   return cudaGetLastError();
 }
 
-static size_t fbc_smem(u32 nt, int ns) { return (size_t)nt * (3 + ns + (1u << ns)) * 8; }
+static size_t fbc_smem(u32 nt, int ns) {
+  if (nt > kFbcTG) nt = kFbcTG;
+  return (size_t)nt * (3 + ns + (1u << ns)) * 8;
+}
 
 template <int NS>
 static cudaError_t launch_fbc_t(const FbcDev* tabs, int tab_per_z, const ModConsts* mc, const u64* in,
@@ -480,6 +516,7 @@ static cudaError_t launch_fbc_t(const FbcDev* tabs, int tab_per_z, const ModCons
     if (e) return e;
   }
   dim3 g = row_grid((1u << logN) / 2, nz, 256);
+  g.z = (nt + kFbcTG - 1) / kFbcTG;
   k_fbc_t<NS><<<g, 256, sm, st>>>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nt_override, z0);
   return cudaGetLastError();
 }
@@ -533,15 +570,15 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
                             cudaStream_t st) {
-  k_ks_inner<<<row_grid(1u << logN, basis.nlimbs(), 256), 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis,
-                                                                        alpha, ndig, logN, g, mc);
+  k_ks_inner<<<row_grid((1u << logN) / 2, basis.nlimbs(), 256), 256, 0, st>>>(acc, x_eval, raised, key_b, key_a,
+                                                                              basis, alpha, ndig, logN, g, mc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,
                                    const u64* add1, u64 g_add, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
                                    const u64* pinv_sh, const ModConsts* mc, cudaStream_t st) {
-  dim3 g = row_grid(1u << logN, nq, 256);
+  dim3 g = row_grid((1u << logN) / 2, nq, 256);
   g.z = 2;
   k_moddown_combine<<<g, 256, 0, st>>>(out0, out1, acc, lift, add0, add1, g_add, nq, n_ext, logN, pinv, pinv_sh,
                                        mc);

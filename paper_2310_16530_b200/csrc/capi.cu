@@ -50,6 +50,8 @@ struct hcnn_ctx {
   ModConsts* d_mc = nullptr;
   u64 *d_tw = nullptr, *d_twp = nullptr, *d_itw = nullptr, *d_itwp = nullptr;
   ulonglong2 *d_ctw = nullptr, *d_ictw = nullptr;
+  bool ntt2_ok = false;
+  std::vector<unsigned char> small;  // q < 2^47
   FbcStore moddown;                  // P -> q_0..q_{Lq-1}
   u64 *d_pinv = nullptr, *d_pinv_sh = nullptr;  // P^-1 mod q_i
   u64 *d_rinv = nullptr, *d_rinv_sh = nullptr;  // [l][i] q_l^-1 mod q_i
@@ -67,6 +69,7 @@ struct hcnn_ctx {
     T.itwp = d_itwp;
     T.ctw = d_ctw;
     T.ictw = d_ictw;
+    T.small = small.data();
     return T;
   }
   Basis basis(u32 nq, u32 np) const {
@@ -314,6 +317,8 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
     mc.ninvN = h_invmod(n % q, q);
     mc.ninvN_sh = h_shoup(mc.ninvN, q);
     mc.two_q = 2 * q;
+    mc.four_q = 4 * q;
+    mc.one_sh = h_shoup(1, q);
     u64 w1 = itw[m * N + (N > 1 ? 1 : 0)];
     mc.ilast = h_mulmod(w1, mc.ninvN, q);
     mc.ilast_sh = h_shoup(mc.ilast, q);
@@ -330,7 +335,13 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
   CK(cudaMemcpy(c->d_twp, twp.data(), tb, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_itw, itw.data(), tb, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_itwp, itwp.data(), tb, cudaMemcpyHostToDevice));
-  if (ntt2_supported(c->logN)) {
+  u64 qmax = 0;
+  for (u64 q : c->mods) {
+    qmax = q > qmax ? q : qmax;
+    c->small.push_back(q < (1ull << 47) ? 1 : 0);
+  }
+  c->ntt2_ok = ntt2_supported(c->logN) && qmax < (1ull << 61);  // 8q < 2^64 (approximate-quotient NTT)
+  if (c->ntt2_ok) {
     // per-chunk twiddles for the radix-16 chunk pass (ntt2.cu): chunk g of
     // 256 owns 255 Shoup pairs, forward e = 2^s-1+i -> tw[(N1+g)*2^s + i],
     // inverse e = nb-1+i -> itw[nb*(N1+g) + i] (nb = 128>>u blocks)
@@ -775,6 +786,16 @@ int hcnn_rescale(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint32_t level,
 
 
 void hcnn_profile_enable(int on) { g_prof.store(on != 0); }
+
+int hcnn_set_option(const char* name, long long value) {
+  std::string k = name ? name : "";
+  if (k == "ntt_group_limbs") g_ntt_tuning.group_limbs = (int)value;
+  else if (k == "ntt_hints") g_ntt_tuning.hints = (int)value;
+  else if (k == "ntt_occupancy") g_ntt_tuning.occupancy = (int)value;
+  else if (k == "ntt_split") g_ntt_tuning.split = (int)value;
+  else return fail(HCNN_E_PARAMETER, "unknown option " + k);
+  return HCNN_OK;
+}
 
 unsigned long long hcnn_kernel_launches(void) { return g_kernels.load(); }
 

@@ -31,7 +31,8 @@ struct ModConsts {
   u64 two_q;
   u64 ilast;    // inverse twiddle itw[1] * N^-1 mod q (last GS stage, N^-1 folded)
   u64 ilast_sh;
-  u64 pad;
+  u64 four_q;   // lazy bound of the approximate-quotient NTT (ntt2.cu)
+  u64 one_sh;   // floor(2^64 / q): Shoup companion of 1 (exact reduction of any u64)
 };
 
 // A basis is (nq, np): limbs 0..nq-1 live over q_0..q_{nq-1}, limbs
@@ -81,6 +82,19 @@ __device__ __forceinline__ u64 shoup_lazy(u64 a, u64 w, u64 wp, u64 q) {
 __device__ __forceinline__ u64 shoup_mul(u64 a, u64 w, u64 wp, u64 q) {
   u64 r = shoup_lazy(a, w, wp, q);
   return r >= q ? r - q : r;
+}
+
+// floor(a*b / 2^64) - e, e in {0,1,2}: the lo*lo partial product and the
+// middle carries are dropped (3 IMAD.WIDE instead of 4 plus carry chain).
+__device__ __forceinline__ u64 mulhi_approx(u64 a, u64 b) {
+  const u32 alo = (u32)a, ahi = (u32)(a >> 32), blo = (u32)b, bhi = (u32)(b >> 32);
+  const u64 m1 = (u64)alo * bhi, m2 = (u64)ahi * blo, hh = (u64)ahi * bhi;
+  return hh + (m1 >> 32) + (m2 >> 32);
+}
+// Shoup product with the approximate quotient: a*w - qhat*q lies in [0, 4q)
+// for any a < 2^64, w < q (qhat is at most 2 below the true quotient).
+__device__ __forceinline__ u64 shoup_approx(u64 a, u64 w, u64 wp, u64 q) {
+  return a * w - mulhi_approx(a, wp) * q;
 }
 
 // 128-bit accumulate of a*b into (hi:lo), keeping hi < q so the total stays

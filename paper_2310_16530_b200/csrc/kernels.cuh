@@ -14,7 +14,18 @@ struct LimbMap {
   Basis basis;
   u32 skip_alpha;
   u32 first_limb;     // basis position of the first processed limb
+  u32 r0, z0;         // sub-batch offsets (limb / poly) added to blockIdx.y / blockIdx.z
 };
+
+// tuning knobs (hcnn_set_option): NTT sub-batch size in limbs (0 = one
+// launch pair for the whole batch) and L2 cache-policy hints
+struct NttTuning {
+  int group_limbs = 0;
+  int hints = 1;
+  int occupancy = 0;  // 1: register-capped kernels (more resident warps)
+  int split = 0;      // 1: separate launches per modulus class
+};
+extern NttTuning g_ntt_tuning;
 
 struct NttTables {
   u32 logN;
@@ -25,6 +36,7 @@ struct NttTables {
   const u64* itwp;
   const ulonglong2* ctw;   // [mod][N/256][256] per-chunk forward twiddles (ntt2.cu)
   const ulonglong2* ictw;  // [mod][N/256][256] per-chunk inverse twiddles
+  const unsigned char* small;  // host: per modulus index, q < 2^47 (unreduced fast path)
 };
 
 void ntt_split(u32 logN, u32* logN1);

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(256) ntt_fwd_cols(LimbMap map, const ModConsts
                                                     const u64* __restrict__ tw, const u64* __restrict__ twp,
                                                     u32 logN, u32 logN1) {
   extern __shared__ u64 sm[];
-  const u32 r = blockIdx.y, z = blockIdx.z;
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
   if (limb_skipped(map, r, z)) return;
   const u32 N = 1u << logN, N1 = 1u << logN1, N2 = N >> logN1;
   const u32 mod = map.basis.mod_of(r + map.first_limb);
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) ntt_fwd_chunks(LimbMap map, const ModCons
                                                       const u64* __restrict__ tw, const u64* __restrict__ twp,
                                                       u32 logN, u32 logN1, u32 CH) {
   extern __shared__ u64 sm[];
-  const u32 r = blockIdx.y, z = blockIdx.z;
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
   if (limb_skipped(map, r, z)) return;
   const u32 N = 1u << logN, N1 = 1u << logN1;
   const u32 logM = logN - logN1, M = 1u << logM;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) ntt_inv_chunks(LimbMap map, const ModCons
                                                       const u64* __restrict__ itw, const u64* __restrict__ itwp,
                                                       u32 logN, u32 logN1, u32 CH) {
   extern __shared__ u64 sm[];
-  const u32 r = blockIdx.y, z = blockIdx.z;
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
   if (limb_skipped(map, r, z)) return;
   const u32 N = 1u << logN, N1 = 1u << logN1;
   const u32 logM = logN - logN1, M = 1u << logM;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) ntt_inv_cols(LimbMap map, const ModConsts
                                                     const u64* __restrict__ itw, const u64* __restrict__ itwp,
                                                     u32 logN, u32 logN1) {
   extern __shared__ u64 sm[];
-  const u32 r = blockIdx.y, z = blockIdx.z;
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
   if (limb_skipped(map, r, z)) return;
   const u32 N = 1u << logN, N1 = 1u << logN1, N2 = N >> logN1;
   const u32 mod = map.basis.mod_of(r + map.first_limb);
@@ -250,7 +250,7 @@ void ntt_split(u32 logN, u32* logN1) {
 cudaError_t launch_ntt(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 npolys, bool inverse,
                        cudaStream_t st) {
   if (nlimbs == 0 || npolys == 0) return cudaSuccess;
-  if (T.ctw && ntt2_supported(T.logN)) return launch_ntt2(T, map, nlimbs, npolys, inverse, st);
+  if (T.ctw) return launch_ntt2(T, map, nlimbs, npolys, inverse, st);
   u32 logN = T.logN, logN1;
   ntt_split(logN, &logN1);
   const u32 N = 1u << logN;

@@ -21,19 +21,65 @@
 
 namespace hcnn {
 
-__device__ __forceinline__ void ct_bfly(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 q2) {
-  u64 x = X >= q2 ? X - q2 : X;
-  u64 t = shoup_lazy(Y, w, wp, q);
-  X = x + t;
-  Y = x - t + q2;
+NttTuning g_ntt_tuning;
+
+// L2 policy: keep twiddle tables resident (evict_last), stream the data
+__device__ __forceinline__ u64 keep_policy() {
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <bool HINT>
+__device__ __forceinline__ ulonglong2 ld_tw(const ulonglong2* p, u64 pol) {
+  if constexpr (HINT) {
+    ulonglong2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
+    return v;
+  } else {
+    return __ldg(p);
+  }
+}
+template <bool HINT>
+__device__ __forceinline__ u64 ld_last(const u64* p) {  // data read for the last time
+  if constexpr (HINT) return __ldcs(p);
+  else return *p;
 }
 
-__device__ __forceinline__ void gs_bfly(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 q2) {
+// Harvey butterflies with the approximate Shoup quotient.  Forward keeps
+// values in [0, 8q) (qb = 4q): X is folded to [0,4q), T in [0,4q).
+// Inverse keeps [0, 4q).  Requires q < 2^61.
+__device__ __forceinline__ void ct_bfly(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 qb) {
+  u64 x = X >= qb ? X - qb : X;
+  u64 t = shoup_approx(Y, w, wp, q);
+  X = x + t;
+  Y = x - t + qb;
+}
+
+__device__ __forceinline__ void gs_bfly(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 qb) {
   u64 s = X + Y;
-  s = s >= q2 ? s - q2 : s;
-  u64 t = X - Y + q2;
+  s = s >= qb ? s - qb : s;
+  u64 t = X - Y + qb;
   X = s;
-  Y = shoup_lazy(t, w, wp, q);
+  Y = shoup_approx(t, w, wp, q);
+}
+
+// Unreduced butterflies for q < 2^47 (24 of the 29 moduli of config 2): the
+// 64-bit word has room for the growth, so the per-stage conditional
+// subtractions (the ALU-pipe bottleneck) disappear.  Forward: values grow by
+// < 4q per stage (T = Shoup output in [0,4q)), < 65q after 16 stages.
+// Inverse: the sum doubles per stage, values < q 2^(s+1) after stage s;
+// C_s = q 2^(s+1) keeps X - Y + C_s positive.
+__device__ __forceinline__ void ct_bfly_fast(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 q4) {
+  u64 t = shoup_approx(Y, w, wp, q);
+  u64 x = X;
+  X = x + t;
+  Y = x + q4 - t;
+}
+__device__ __forceinline__ void gs_bfly_fast(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 c) {
+  u64 x = X, y = Y;
+  X = x + y;
+  Y = shoup_approx(x - y + c, w, wp, q);
 }
 
 // One CT stage d of a 16-point network held in x[0..15]: pairs k with
@@ -50,13 +96,31 @@ __device__ __forceinline__ void ct_stage(u64 (&x)[16], u64 q, u64 q2, TW& tw) {
   }
 }
 
-// CT stages d in [D0,4)
-template <int D0, class TW>
+template <int d, class TW>
+__device__ __forceinline__ void ct_stage_fast(u64 (&x)[16], u64 q, u64 q4, TW& tw) {
+  constexpr int h = 8 >> d;
+#pragma unroll
+  for (int b = 0; b < (1 << d); ++b) {
+    ulonglong2 W = tw(d, b);
+#pragma unroll
+    for (int r = 0; r < h; ++r) ct_bfly_fast(x[2 * h * b + r], x[2 * h * b + r + h], W.x, W.y, q, q4);
+  }
+}
+
+// CT stages d in [D0,4); FAST selects the unreduced butterflies (q < 2^47)
+template <int D0, bool FAST = false, class TW>
 __device__ __forceinline__ void ct16(u64 (&x)[16], u64 q, u64 q2, TW tw) {
-  if constexpr (D0 <= 0) ct_stage<0>(x, q, q2, tw);
-  if constexpr (D0 <= 1) ct_stage<1>(x, q, q2, tw);
-  if constexpr (D0 <= 2) ct_stage<2>(x, q, q2, tw);
-  if constexpr (D0 <= 3) ct_stage<3>(x, q, q2, tw);
+  if constexpr (FAST) {
+    if constexpr (D0 <= 0) ct_stage_fast<0>(x, q, q2, tw);
+    if constexpr (D0 <= 1) ct_stage_fast<1>(x, q, q2, tw);
+    if constexpr (D0 <= 2) ct_stage_fast<2>(x, q, q2, tw);
+    if constexpr (D0 <= 3) ct_stage_fast<3>(x, q, q2, tw);
+  } else {
+    if constexpr (D0 <= 0) ct_stage<0>(x, q, q2, tw);
+    if constexpr (D0 <= 1) ct_stage<1>(x, q, q2, tw);
+    if constexpr (D0 <= 2) ct_stage<2>(x, q, q2, tw);
+    if constexpr (D0 <= 3) ct_stage<3>(x, q, q2, tw);
+  }
 }
 
 struct Fold {
@@ -75,21 +139,42 @@ __device__ __forceinline__ void gs_stage(u64 (&x)[16], u64 q, u64 q2, TW& tw) {
   }
 }
 
+template <int d, class TW>
+__device__ __forceinline__ void gs_stage_fast(u64 (&x)[16], u64 q, u64 c, TW& tw) {
+  constexpr int h = 1 << d;
+#pragma unroll
+  for (int b = 0; b < (8 >> d); ++b) {
+    ulonglong2 W = tw(d, b);
+#pragma unroll
+    for (int r = 0; r < h; ++r) gs_bfly_fast(x[2 * h * b + r], x[2 * h * b + r + h], W.x, W.y, q, c);
+  }
+}
+
 // GS stages d in [D0,4).  FOLD: stage 3 is the transform's last one
-// (twiddle itw[1]) and also applies N^-1.
-template <int D0, bool FOLD, class TW>
-__device__ __forceinline__ void gs16(u64 (&x)[16], u64 q, u64 q2, TW tw, Fold C) {
-  if constexpr (D0 <= 0) gs_stage<0>(x, q, q2, tw);
-  if constexpr (D0 <= 1) gs_stage<1>(x, q, q2, tw);
-  if constexpr (D0 <= 2) gs_stage<2>(x, q, q2, tw);
+// (twiddle itw[1]) and also applies N^-1.  FAST: unreduced butterflies;
+// s0 is the global index of stage d = 0 (sets C_s = q 2^(s+1)).
+template <int D0, bool FOLD, bool FAST = false, class TW>
+__device__ __forceinline__ void gs16(u64 (&x)[16], u64 q, u64 q2, TW tw, Fold C, u32 s0 = 0) {
+  if constexpr (FAST) {
+    if constexpr (D0 <= 0) gs_stage_fast<0>(x, q, q << (s0 + 1), tw);
+    if constexpr (D0 <= 1) gs_stage_fast<1>(x, q, q << (s0 + 2), tw);
+    if constexpr (D0 <= 2) gs_stage_fast<2>(x, q, q << (s0 + 3), tw);
+  } else {
+    if constexpr (D0 <= 0) gs_stage<0>(x, q, q2, tw);
+    if constexpr (D0 <= 1) gs_stage<1>(x, q, q2, tw);
+    if constexpr (D0 <= 2) gs_stage<2>(x, q, q2, tw);
+  }
   if constexpr (FOLD) {
+    const u64 c3 = FAST ? (q << (s0 + 4)) : q2;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       u64 s = x[r] + x[r + 8];
-      u64 t = x[r] - x[r + 8] + q2;
+      u64 t = x[r] - x[r + 8] + c3;
       x[r] = shoup_mul(s, C.ninvN, C.ninvN_sh, q);
       x[r + 8] = shoup_mul(t, C.ilast, C.ilast_sh, q);
     }
+  } else if constexpr (FAST) {
+    gs_stage_fast<3>(x, q, q << (s0 + 4), tw);
   } else {
     gs_stage<3>(x, q, q2, tw);
   }
@@ -108,33 +193,38 @@ __device__ __forceinline__ bool limb_skipped2(const LimbMap& m, u32 r, u32 z) {
 // column pass (N1 = 2^LOGN1 points, 16 <= N1 <= 256), 256 threads,
 // COLS = 256/T1 columns per CTA, T1 = N1/16 threads per column
 // ---------------------------------------------------------------------------
-template <int LOGN1>
-__global__ void __launch_bounds__(256) ntt2_fwd_cols(LimbMap map, const ModConsts* __restrict__ mc,
+template <int LOGN1, bool HINT, int MINB, int MODE>
+__global__ void __launch_bounds__(256, MINB) ntt2_fwd_cols(LimbMap map, const ModConsts* __restrict__ mc,
                                                      const u64* __restrict__ tw, const u64* __restrict__ twp,
                                                      u32 logN) {
   constexpr int N1 = 1 << LOGN1, T1 = N1 / 16, COLS = 256 / T1, NSB = LOGN1 - 4;
   __shared__ u64 tile[N1 * COLS];
   __shared__ ulonglong2 sw[N1];
-  const u32 r = blockIdx.y, z = blockIdx.z;
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
   if (limb_skipped2(map, r, z)) return;
   const u32 N = 1u << logN, N2 = N >> LOGN1;
   const u32 mod = map.basis.mod_of(r + map.first_limb);
-  const u64 q = mc[mod].q, q2 = mc[mod].two_q;
+  const u64 q = mc[mod].q, q2 = mc[mod].four_q;
   u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + blockIdx.x * COLS;
   const int tid = threadIdx.x, c = tid % COLS, j = tid / COLS;
   for (int i = tid; i < N1; i += 256) sw[i] = make_ulonglong2(tw[(size_t)mod * N + i], twp[(size_t)mod * N + i]);
   u64 x[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) x[k] = a[(size_t)(j + T1 * k) * N2 + c];
+  for (int k = 0; k < 16; ++k) x[k] = ld_last<HINT>(&a[(size_t)(j + T1 * k) * N2 + c]);
   __syncthreads();
-  ct16<0>(x, q, q2, [&](int d, int b) { return sw[(1 << d) + b]; });
+  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
+  auto twA = [&](int d, int b) { return sw[(1 << d) + b]; };
+  if (fast) ct16<0, true>(x, q, q2, twA);
+  else ct16<0, false>(x, q, q2, twA);
   if (NSB > 0) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[(j + T1 * k) * COLS + c] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 16; ++k) x[k] = tile[(16 * j + k) * COLS + c];
-    ct16<4 - NSB>(x, q, q2, [&](int d, int b) { return sw[(1 << (d + NSB)) + (j << d) + b]; });
+    auto twB = [&](int d, int b) { return sw[(1 << (d + NSB)) + (j << d) + b]; };
+    if (fast) ct16<4 - NSB, true>(x, q, q2, twB);
+    else ct16<4 - NSB, false>(x, q, q2, twB);
 #pragma unroll
     for (int k = 0; k < 16; ++k) a[(size_t)(16 * j + k) * N2 + c] = x[k];
   } else {
@@ -143,40 +233,46 @@ __global__ void __launch_bounds__(256) ntt2_fwd_cols(LimbMap map, const ModConst
   }
 }
 
-template <int LOGN1>
-__global__ void __launch_bounds__(256) ntt2_inv_cols(LimbMap map, const ModConsts* __restrict__ mc,
+template <int LOGN1, bool HINT, int MINB, int MODE>
+__global__ void __launch_bounds__(256, MINB) ntt2_inv_cols(LimbMap map, const ModConsts* __restrict__ mc,
                                                      const u64* __restrict__ itw, const u64* __restrict__ itwp,
                                                      u32 logN) {
   constexpr int N1 = 1 << LOGN1, T1 = N1 / 16, COLS = 256 / T1, NSA = LOGN1 - 4;
   __shared__ u64 tile[N1 * COLS];
   __shared__ ulonglong2 sw[N1];
-  const u32 r = blockIdx.y, z = blockIdx.z;
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
   if (limb_skipped2(map, r, z)) return;
   const u32 N = 1u << logN, N2 = N >> LOGN1;
   const u32 mod = map.basis.mod_of(r + map.first_limb);
-  const u64 q = mc[mod].q, q2 = mc[mod].two_q;
+  const u64 q = mc[mod].q, q2 = mc[mod].four_q;
   const Fold C{mc[mod].ninvN, mc[mod].ninvN_sh, mc[mod].ilast, mc[mod].ilast_sh};
   u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + blockIdx.x * COLS;
   const int tid = threadIdx.x, c = tid % COLS, j = tid / COLS;
   for (int i = tid; i < N1; i += 256) sw[i] = make_ulonglong2(itw[(size_t)mod * N + i], itwp[(size_t)mod * N + i]);
   u64 x[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) x[k] = a[(size_t)(16 * j + k) * N2 + c];
+  for (int k = 0; k < 16; ++k) x[k] = ld_last<HINT>(&a[(size_t)(16 * j + k) * N2 + c]);
   __syncthreads();
   // stages t = 1..8 rows: contiguous groups of 16 rows; twiddle itw[H + i],
   // H = N1 >> (d+1) blocks, i = j*(8>>d) + b
+  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
+  auto twB = [&](int d, int b) { return sw[(N1 >> (d + 1)) + j * (8 >> d) + b]; };
+  auto twA = [&](int d, int b) { return sw[(8 >> d) + b]; };
   if (NSA == 0) {
-    gs16<0, true>(x, q, q2, [&](int d, int b) { return sw[(N1 >> (d + 1)) + j * (8 >> d) + b]; }, C);
+    if (fast) gs16<0, true, true>(x, q, q2, twB, C, 8);
+    else gs16<0, true, false>(x, q, q2, twB, C);
 #pragma unroll
     for (int k = 0; k < 16; ++k) a[(size_t)(16 * j + k) * N2 + c] = x[k];
   } else {
-    gs16<0, false>(x, q, q2, [&](int d, int b) { return sw[(N1 >> (d + 1)) + j * (8 >> d) + b]; }, C);
+    if (fast) gs16<0, false, true>(x, q, q2, twB, C, 8);
+    else gs16<0, false, false>(x, q, q2, twB, C);
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[(16 * j + k) * COLS + c] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 16; ++k) x[k] = tile[(j + T1 * k) * COLS + c];
-    gs16<4 - NSA, true>(x, q, q2, [&](int d, int b) { return sw[(8 >> d) + b]; }, C);
+    if (fast) gs16<4 - NSA, true, true>(x, q, q2, twA, C, 8 + NSA);
+    else gs16<4 - NSA, true, false>(x, q, q2, twA, C);
 #pragma unroll
     for (int k = 0; k < 16; ++k) a[(size_t)(j + T1 * k) * N2 + c] = x[k];
   }
@@ -191,43 +287,57 @@ __global__ void __launch_bounds__(256) ntt2_inv_cols(LimbMap map, const ModConst
 // ---------------------------------------------------------------------------
 constexpr int kChunksPerCta = 8;
 
-__global__ void __launch_bounds__(128) ntt2_fwd_chunks(LimbMap map, const ModConsts* __restrict__ mc,
+template <bool HINT, int MINB, int MODE>
+__global__ void __launch_bounds__(128, MINB) ntt2_fwd_chunks(LimbMap map, const ModConsts* __restrict__ mc,
                                                        const ulonglong2* __restrict__ ctw, u32 logN) {
   __shared__ u64 tile[kChunksPerCta][16 * 17];
   __shared__ ulonglong2 twa[kChunksPerCta][16];
-  const u32 r = blockIdx.y, z = blockIdx.z;
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
   if (limb_skipped2(map, r, z)) return;
   const u32 N = 1u << logN, N1 = N >> 8;
   const u32 mod = map.basis.mod_of(r + map.first_limb);
-  const u64 q = mc[mod].q, q2 = mc[mod].two_q;
+  const u64 q = mc[mod].q, q2 = mc[mod].four_q;
   const int tid = threadIdx.x, cc = tid >> 4, j = tid & 15;
   const u32 g = blockIdx.x * kChunksPerCta + cc;
   u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + (size_t)g * 256;
   const ulonglong2* T = ctw + ((size_t)mod * N1 + g) * 256;
   u64* tl = tile[cc];
+  const u64 pol = HINT ? keep_policy() : 0;
   u64 x[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) x[k] = a[j + 16 * k];
-  if (j < 15) twa[cc][j] = __ldg(&T[j]);
+  for (int k = 0; k < 16; ++k) x[k] = ld_last<HINT>(&a[j + 16 * k]);
+  if (j < 15) twa[cc][j] = ld_tw<HINT>(&T[j], pol);
   // second-group twiddles: stage 4+d, block (j<<d)+b -> e = (16<<d)-1+(j<<d)+b
   ulonglong2 tb[15];
 #pragma unroll
   for (int d = 0; d < 4; ++d)
 #pragma unroll
-    for (int b = 0; b < (1 << d); ++b) tb[(1 << d) - 1 + b] = __ldg(&T[(16 << d) - 1 + (j << d) + b]);
+    for (int b = 0; b < (1 << d); ++b) tb[(1 << d) - 1 + b] = ld_tw<HINT>(&T[(16 << d) - 1 + (j << d) + b], pol);
   __syncwarp();
-  ct16<0>(x, q, q2, [&](int d, int b) { return twa[cc][(1 << d) - 1 + b]; });
+  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
+  auto twA = [&](int d, int b) { return twa[cc][(1 << d) - 1 + b]; };
+  if (fast) ct16<0, true>(x, q, q2, twA);
+  else ct16<0, false>(x, q, q2, twA);
 #pragma unroll
   for (int k = 0; k < 16; ++k) tl[17 * k + j] = x[k];
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 16; ++k) x[k] = tl[17 * j + k];
-  ct16<0>(x, q, q2, [&](int d, int b) { return tb[(1 << d) - 1 + b]; });
+  auto twB = [&](int d, int b) { return tb[(1 << d) - 1 + b]; };
+  if (fast) {
+    ct16<0, true>(x, q, q2, twB);
+    const u64 one_sh = mc[mod].one_sh;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    u64 v = x[k];
-    v = v >= q2 ? v - q2 : v;
-    x[k] = v >= q ? v - q : v;
+    for (int k = 0; k < 16; ++k) x[k] = shoup_mul(x[k], 1, one_sh, q);  // < 65q -> [0, q)
+  } else {
+    ct16<0, false>(x, q, q2, twB);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      u64 v = x[k];
+      v = v >= q2 ? v - q2 : v;              // [0, 4q)
+      v = v >= 2 * q ? v - 2 * q : v;        // [0, 2q)
+      x[k] = v >= q ? v - q : v;
+    }
   }
   __syncwarp();
 #pragma unroll
@@ -237,45 +347,53 @@ __global__ void __launch_bounds__(128) ntt2_fwd_chunks(LimbMap map, const ModCon
   for (int k = 0; k < 16; ++k) a[j + 16 * k] = tl[17 * k + j];
 }
 
-__global__ void __launch_bounds__(128) ntt2_inv_chunks(LimbMap map, const ModConsts* __restrict__ mc,
+template <bool HINT, int MINB, int MODE>
+__global__ void __launch_bounds__(128, MINB) ntt2_inv_chunks(LimbMap map, const ModConsts* __restrict__ mc,
                                                        const ulonglong2* __restrict__ ctw, u32 logN) {
   __shared__ u64 tile[kChunksPerCta][16 * 17];
   __shared__ ulonglong2 twa[kChunksPerCta][16];
-  const u32 r = blockIdx.y, z = blockIdx.z;
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
   if (limb_skipped2(map, r, z)) return;
   const u32 N = 1u << logN, N1 = N >> 8;
   const u32 mod = map.basis.mod_of(r + map.first_limb);
-  const u64 q = mc[mod].q, q2 = mc[mod].two_q;
+  const u64 q = mc[mod].q, q2 = mc[mod].four_q;
   const Fold C{0, 0, 0, 0};
   const int tid = threadIdx.x, cc = tid >> 4, j = tid & 15;
   const u32 g = blockIdx.x * kChunksPerCta + cc;
   u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + (size_t)g * 256;
   const ulonglong2* T = ctw + ((size_t)mod * N1 + g) * 256;
   u64* tl = tile[cc];
+  const u64 pol = HINT ? keep_policy() : 0;
   u64 x[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) x[k] = a[j + 16 * k];
+  for (int k = 0; k < 16; ++k) x[k] = ld_last<HINT>(&a[j + 16 * k]);
   // first group (local stages 0..3): nb = 128>>d blocks, i = j*(8>>d)+b
   ulonglong2 tb[15];
 #pragma unroll
   for (int d = 0; d < 4; ++d)
 #pragma unroll
-    for (int b = 0; b < (8 >> d); ++b) tb[16 - (16 >> d) + b] = __ldg(&T[(128 >> d) - 1 + j * (8 >> d) + b]);
+    for (int b = 0; b < (8 >> d); ++b)
+      tb[16 - (16 >> d) + b] = ld_tw<HINT>(&T[(128 >> d) - 1 + j * (8 >> d) + b], pol);
   // second group (local stages 4..7): nb = 8>>d, i = b -> e = (8>>d)-1+b, shared
-  if (j < 15) twa[cc][j] = __ldg(&T[j]);
+  if (j < 15) twa[cc][j] = ld_tw<HINT>(&T[j], pol);
 #pragma unroll
   for (int k = 0; k < 16; ++k) tl[17 * k + j] = x[k];
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 16; ++k) x[k] = tl[17 * j + k];
-  gs16<0, false>(x, q, q2, [&](int d, int b) { return tb[16 - (16 >> d) + b]; }, C);
+  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
+  auto twB = [&](int d, int b) { return tb[16 - (16 >> d) + b]; };
+  if (fast) gs16<0, false, true>(x, q, q2, twB, C, 0);
+  else gs16<0, false, false>(x, q, q2, twB, C);
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 16; ++k) tl[17 * j + k] = x[k];
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 16; ++k) x[k] = tl[17 * k + j];
-  gs16<0, false>(x, q, q2, [&](int d, int b) { return twa[cc][(8 >> d) - 1 + b]; }, C);
+  auto twA = [&](int d, int b) { return twa[cc][(8 >> d) - 1 + b]; };
+  if (fast) gs16<0, false, true>(x, q, q2, twA, C, 4);
+  else gs16<0, false, false>(x, q, q2, twA, C);
 #pragma unroll
   for (int k = 0; k < 16; ++k) a[j + 16 * k] = x[k];
 }
@@ -283,41 +401,92 @@ __global__ void __launch_bounds__(128) ntt2_inv_chunks(LimbMap map, const ModCon
 // ---------------------------------------------------------------------------
 bool ntt2_supported(u32 logN) { return logN >= 12 && logN <= 16; }
 
-template <int L>
-static void launch_cols(bool inv, dim3 g, const LimbMap& map, const NttTables& T, cudaStream_t st) {
-  if (inv) ntt2_inv_cols<L><<<g, 256, 0, st>>>(map, T.mc, T.itw, T.itwp, T.logN);
-  else ntt2_fwd_cols<L><<<g, 256, 0, st>>>(map, T.mc, T.tw, T.twp, T.logN);
+template <int L, bool H, int OCC, int F>
+static void launch_cols_t(bool inv, dim3 g, const LimbMap& map, const NttTables& T, cudaStream_t st) {
+  if (inv) ntt2_inv_cols<L, H, OCC ? 3 : 1, F><<<g, 256, 0, st>>>(map, T.mc, T.itw, T.itwp, T.logN);
+  else ntt2_fwd_cols<L, H, OCC ? 3 : 1, F><<<g, 256, 0, st>>>(map, T.mc, T.tw, T.twp, T.logN);
 }
 
+template <bool H, int OCC, int F>
+static cudaError_t launch_pair(const NttTables& T, const LimbMap& map, u32 ny, u32 nz, bool inverse,
+                               cudaStream_t st) {
+  const u32 logN = T.logN, logN1 = logN - 8, N1 = 1u << logN1;
+  const u32 cols = 256 / (N1 / 16);
+  dim3 gc(256 / cols, ny, nz);
+  dim3 gk(N1 / kChunksPerCta, ny, nz);
+  auto cols_launch = [&](bool inv) -> bool {
+    switch (logN1) {
+      case 4: launch_cols_t<4, H, OCC, F>(inv, gc, map, T, st); return true;
+      case 5: launch_cols_t<5, H, OCC, F>(inv, gc, map, T, st); return true;
+      case 6: launch_cols_t<6, H, OCC, F>(inv, gc, map, T, st); return true;
+      case 7: launch_cols_t<7, H, OCC, F>(inv, gc, map, T, st); return true;
+      case 8: launch_cols_t<8, H, OCC, F>(inv, gc, map, T, st); return true;
+      default: return false;
+    }
+  };
+  if (!inverse) {
+    if (!cols_launch(false)) return cudaErrorInvalidValue;
+    ntt2_fwd_chunks<H, OCC ? 5 : 1, F><<<gk, 128, 0, st>>>(map, T.mc, T.ctw, logN);
+  } else {
+    ntt2_inv_chunks<H, OCC ? 5 : 1, F><<<gk, 128, 0, st>>>(map, T.mc, T.ictw, logN);
+    if (!cols_launch(true)) return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// The two passes of a batch run back to back on L2-sized groups of limbs so
+// the intermediate between passes is re-read from L2, not HBM.
 cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 npolys, bool inverse,
                         cudaStream_t st) {
   if (nlimbs == 0 || npolys == 0) return cudaSuccess;
-  const u32 logN = T.logN, logN1 = logN - 8, N1 = 1u << logN1;
-  const u32 cols = 256 / (N1 / 16);
-  dim3 gc(256 / cols, nlimbs, npolys);
-  dim3 gk(N1 / kChunksPerCta, nlimbs, npolys);
-  if (!inverse) {
-    switch (logN1) {
-      case 4: launch_cols<4>(false, gc, map, T, st); break;
-      case 5: launch_cols<5>(false, gc, map, T, st); break;
-      case 6: launch_cols<6>(false, gc, map, T, st); break;
-      case 7: launch_cols<7>(false, gc, map, T, st); break;
-      case 8: launch_cols<8>(false, gc, map, T, st); break;
-      default: return cudaErrorInvalidValue;
+  const bool hint = g_ntt_tuning.hints != 0;
+  const bool occ = g_ntt_tuning.occupancy != 0;
+  // split: one launch pair per run of limbs of one modulus class (uniform
+  // kernels); otherwise one launch pair dispatching per limb at run time
+  const bool split = g_ntt_tuning.split != 0;
+  auto one = [&](const LimbMap& m, u32 ny, u32 nz, int mode) -> cudaError_t {
+    if (mode == 0) return occ ? launch_pair<true, 1, 0>(T, m, ny, nz, inverse, st)
+                              : launch_pair<true, 0, 0>(T, m, ny, nz, inverse, st);
+    if (mode == 1) return occ ? launch_pair<true, 1, 1>(T, m, ny, nz, inverse, st)
+                              : launch_pair<true, 0, 1>(T, m, ny, nz, inverse, st);
+    return occ ? launch_pair<true, 1, 2>(T, m, ny, nz, inverse, st) : launch_pair<true, 0, 2>(T, m, ny, nz, inverse, st);
+  };
+  auto pair = [&](const LimbMap& m, u32 ny, u32 nz) -> cudaError_t {
+    if (!split || !T.small) return one(m, ny, nz, 2);
+    u32 r = 0;
+    while (r < ny) {
+      const bool f = T.small[m.basis.mod_of(m.r0 + r + m.first_limb)];
+      u32 e = r + 1;
+      while (e < ny && (bool)T.small[m.basis.mod_of(m.r0 + e + m.first_limb)] == f) ++e;
+      LimbMap mm = m;
+      mm.r0 = m.r0 + r;
+      cudaError_t err = one(mm, e - r, nz, f ? 1 : 0);
+      if (err) return err;
+      r = e;
     }
-    ntt2_fwd_chunks<<<gk, 128, 0, st>>>(map, T.mc, T.ctw, logN);
+    return cudaSuccess;
+  };
+  (void)hint;
+  const u32 G = g_ntt_tuning.group_limbs > 0 ? (u32)g_ntt_tuning.group_limbs : 0;
+  if (G == 0 || nlimbs * npolys <= G) return pair(map, nlimbs, npolys);
+  cudaError_t e = cudaSuccess;
+  if (nlimbs <= G) {
+    const u32 gp = G / nlimbs;
+    for (u32 z0 = 0; z0 < npolys && !e; z0 += gp) {
+      LimbMap m = map;
+      m.z0 = map.z0 + z0;
+      e = pair(m, nlimbs, npolys - z0 < gp ? npolys - z0 : gp);
+    }
   } else {
-    ntt2_inv_chunks<<<gk, 128, 0, st>>>(map, T.mc, T.ictw, logN);
-    switch (logN1) {
-      case 4: launch_cols<4>(true, gc, map, T, st); break;
-      case 5: launch_cols<5>(true, gc, map, T, st); break;
-      case 6: launch_cols<6>(true, gc, map, T, st); break;
-      case 7: launch_cols<7>(true, gc, map, T, st); break;
-      case 8: launch_cols<8>(true, gc, map, T, st); break;
-      default: return cudaErrorInvalidValue;
-    }
+    for (u32 z = 0; z < npolys && !e; ++z)
+      for (u32 r0 = 0; r0 < nlimbs && !e; r0 += G) {
+        LimbMap m = map;
+        m.z0 = map.z0 + z;
+        m.r0 = map.r0 + r0;
+        e = pair(m, nlimbs - r0 < G ? nlimbs - r0 : G, 1);
+      }
   }
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace hcnn
