@@ -114,6 +114,38 @@ __global__ void k_ew_unary(int op, u64* __restrict__ out, const u64* __restrict_
   }
 }
 
+// per-limb scalar multiply / add with the constants passed by value
+// (capture-safe: no host->device copy), up to kScalarMax limbs
+__global__ void k_scalar(int add, u64* __restrict__ out, const u64* __restrict__ a, Basis basis, u32 logN,
+                         const ModConsts* __restrict__ mc, ScalarArgs args) {
+  RowCtx rc = row_ctx(basis);
+  const u32 N = 1u << logN;
+  const u64 q = mc[rc.mod].q;
+  const u64 w = args.w[rc.r], wp = args.wp[rc.r];
+  const size_t off = (size_t)rc.row * N;
+  const ulonglong2* A = reinterpret_cast<const ulonglong2*>(a + off);
+  ulonglong2* O = reinterpret_cast<ulonglong2*>(out + off);
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < N / 2; i += gridDim.x * blockDim.x) {
+    ulonglong2 x = A[i], o;
+    if (add) {
+      o.x = add_mod(x.x, w, q);
+      o.y = add_mod(x.y, w, q);
+    } else {
+      o.x = shoup_mul(x.x, w, wp, q);
+      o.y = shoup_mul(x.y, w, wp, q);
+    }
+    O[i] = o;
+  }
+}
+
+cudaError_t launch_scalar(int add, u64* out, const u64* a, Basis basis, u32 logN, u32 npolys, const ModConsts* mc,
+                          const ScalarArgs& args, cudaStream_t st) {
+  u32 rows = npolys * basis.nlimbs();
+  if (!rows) return cudaSuccess;
+  k_scalar<<<row_grid((1u << logN) / 2, rows, 256), 256, 0, st>>>(add, out, a, basis, logN, mc, args);
+  return cudaGetLastError();
+}
+
 // signed int64 coefficients (one row of N per poly) -> residues in every
 // limb (ring.py:446-468 replication, ckks.py:284-288 encode reduction)
 __global__ void k_from_signed(u64* __restrict__ out, const long long* __restrict__ in, Basis basis, u32 logN,

@@ -33,6 +33,14 @@ cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 n
                                 const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_rescale_combine(u64* out, const u64* in, u32 l, u32 logN, u32 npolys, const u64* inv,
                                    const u64* inv_sh, const ModConsts* mc, cudaStream_t st);
+constexpr int kScalarMax = 128;
+struct ScalarArgs {
+  u64 w[kScalarMax];
+  u64 wp[kScalarMax];
+};
+cudaError_t launch_scalar(int add, u64* out, const u64* a, Basis basis, u32 logN, u32 npolys, const ModConsts* mc,
+                          const ScalarArgs& args, cudaStream_t st);
+
 constexpr int kMacMax = 64;
 struct MacTerms {
   const u64* ct[kMacMax];

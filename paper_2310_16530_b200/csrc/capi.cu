@@ -541,21 +541,16 @@ static int scalar_op(hcnn_ctx* c, int op, uint64_t* out, const uint64_t* a, cons
   int rc = check_basis(c, nq, np);
   if (rc) return rc;
   Basis b = c->basis(nq, np);
-  u32 nl = nq + np;
-  // constants travel in a small device scratch owned by the context stream-ordered
-  std::vector<u64> h(2 * nl);
+  const u32 nl = nq + np;
+  if (nl > (u32)kScalarMax) return fail(HCNN_E_BASIS, "too many limbs for a scalar op");
+  ScalarArgs args;  // by value: capture-safe, no host->device copy
   for (u32 r = 0; r < nl; ++r) {
     u64 q = c->mods[b.mod_of(r)];
-    h[r] = consts[r] % q;
-    h[nl + r] = h_shoup(h[r], q);
+    args.w[r] = consts[r] % q;
+    args.wp[r] = h_shoup(args.w[r], q);
   }
-  u64* d = nullptr;
-  CK(cudaMallocAsync((void**)&d, 2 * nl * 8, STREAM(s)));
-  CK(cudaMemcpyAsync(d, h.data(), 2 * nl * 8, cudaMemcpyHostToDevice, STREAM(s)));
-  PK("ew_scalar", 16.0 * nl * npolys * c->n, 1, STREAM(s),
-     launch_ew_unary(op, out, a, b, c->logN, npolys, c->d_mc, d, d + nl, STREAM(s)));
-  CK(cudaFreeAsync(d, STREAM(s)));
-  // the host vector must outlive the (pageable, synchronous-to-host) copy
+  PK(op == EW_SCALAR ? "ew_scalar" : "ew_scalar_add", 16.0 * nl * npolys * c->n, 1, STREAM(s),
+     launch_scalar(op == EW_SCALAR_ADD ? 1 : 0, out, a, b, c->logN, npolys, c->d_mc, args, STREAM(s)));
   return HCNN_OK;
 }
 

@@ -39,7 +39,7 @@ def infer(g, plan, ks, x, cache, rng):
     return logits, rep
 
 
-def main(images: int = 2, app_levels: int = 14):
+def main(images: int = 2, app_levels: int = 14, use_graph: int = 1):
     packing.set_mask_mode("compact")
     t0 = time.time()
     params, cfg, b, fx, g, plan, ks = build(app_levels)
@@ -52,6 +52,16 @@ def main(images: int = 2, app_levels: int = 14):
     logits0, rep0 = infer(g, plan, ks, x0, cache, rng)
     torch.cuda.synchronize()
     t_first = time.time() - t0
+    runner = None
+    t_capture = None
+    if use_graph:
+        t0 = time.time()
+        example = packing.encrypt_tensor(x0, g.input_format, ks, rng, plan.entry_levels[0])
+        runner = graph.CapturedInference(g, plan, ks, example, cache)
+        t_capture = time.time() - t0
+        eager_out, _ = graph.execute(g, plan, example, ks, "encrypted", cache=cache)
+        replay_out = runner.run(example)
+        assert torch.equal(eager_out.data, replay_out.data), "graph replay differs from eager execution"
     errs, agree, times = [], 0, []
     kinds: dict = {}
     refreshes = 0
@@ -59,7 +69,13 @@ def main(images: int = 2, app_levels: int = 14):
         x = rng.uniform(-1.0, 1.0, (3, 32, 32))
         torch.cuda.synchronize()
         t0 = time.time()
-        logits, rep = infer(g, plan, ks, x, cache, rng)
+        if runner is not None:
+            packed = packing.encrypt_tensor(x, g.input_format, ks, rng, plan.entry_levels[0])
+            out = runner.run(packed)
+            logits = packing.read_logits(out, g.n_classes, g.formats[-1], ks)
+            rep = runner.report
+        else:
+            logits, rep = infer(g, plan, ks, x, cache, rng)
         torch.cuda.synchronize()
         times.append(time.time() - t0)
         ref, _ = graph.execute(g, plan, x, mode="plaintext-ref")
@@ -84,6 +100,7 @@ def main(images: int = 2, app_levels: int = 14):
         "q_limbs": len(params.q_mods), "special_limbs": len(params.p_mods), "app_levels": app_levels,
         "refresh_points": list(plan.refresh_points), "bootstraps_per_image": refreshes,
         "rotation_keys": len(ks.gks), "setup_s": round(t_setup, 1), "first_image_s": round(t_first, 2),
+        "cuda_graph": bool(use_graph), "capture_s": None if t_capture is None else round(t_capture, 1),
         "s_per_image": round(float(np.median(times)), 3), "images": images,
         "max_logit_err_vs_plain": max(errs), "argmax_agree": f"{agree}/{images}",
         "tally": tot, "layer_ms_by_kind": {k: round(v, 1) for k, v in kinds.items()},
