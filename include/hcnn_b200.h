@@ -139,6 +139,16 @@ int hcnn_rescale(hcnn_ctx* ctx, uint64_t* out, const uint64_t* in, uint32_t leve
 int hcnn_mac_terms(hcnn_ctx* ctx, uint64_t* out_ct, const uint64_t* const* cts, const uint64_t* const* masks_mont,
                    uint32_t n_terms, uint32_t level, int accumulate, void* stream);
 
+/* out[npolys][nq][N] (+)= sum_t consts[t][r] * srcs[t] limb-wise (integer
+ * constants, reduced per limb).  srcs[t] has src_limbs[t] >= nq limbs per
+ * poly (a longer ciphertext is read as its level-dropped prefix).  Replaces
+ * the per-coefficient mul_const / add chain of a Chebyshev evaluation
+ * (no reference counterpart: the reference has no bootstrapping,
+ * ckks.py:667-690 debug_refresh); any number of terms (batched by 16). */
+int hcnn_scalar_mac(hcnn_ctx* ctx, uint64_t* out, const uint64_t* const* srcs, const uint32_t* src_limbs,
+                    const uint64_t* consts, uint32_t n_terms, uint32_t nq, uint32_t npolys, int accumulate,
+                    void* stream);
+
 /* ---- instrumentation ------------------------------------------------------ */
 /* count of engine kernels launched since load (all contexts) */
 unsigned long long hcnn_kernel_launches(void);

@@ -63,6 +63,8 @@ SIGNATURES = {
                                    ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP, _VP]),
     "hcnn_rescale_workspace_bytes": (_SZ, [_VP, _U32]),
     "hcnn_rescale": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP, _VP]),
+    "hcnn_scalar_mac": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_U32), _PU64, _U32, _U32, _U32, _INT,
+                               _VP]),
     "hcnn_mac_terms": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _U32, _U32, _INT, _VP]),
     "hcnn_kernel_launches": (ctypes.c_ulonglong, []),
     "hcnn_profile_enable": (None, [_INT]),

@@ -268,10 +268,10 @@ class _Exact:
     def _int_consts(self, k: int, level: int) -> list[int]:
         return [k % m.q for m in self.params.mods_at(level)]
 
-    def add_const(self, a: Ciphertext, c: float) -> Ciphertext:
+    def add_const(self, a: Ciphertext, c: float, inplace: bool = False) -> Ciphertext:
         k = int(round(c * a.scale))
-        out = a.data.clone()
-        self.ctx.scalar_mul(a.data[0].contiguous(), self._int_consts(k, a.level), a.level + 1, out=out[0], add=True)
+        out = a.data if inplace else a.data.clone()
+        self.ctx.scalar_mul(out[0], self._int_consts(k, a.level), a.level + 1, out=out[0], add=True)
         return Ciphertext(out, a.scale, a.n, a.params)
 
     def mul_const(self, a: Ciphertext, c: float, target_scale: float) -> Ciphertext:
@@ -285,26 +285,127 @@ class _Exact:
         return ckks.rescale(Ciphertext(out, a.scale * s_c, a.n, a.params), self.params)
 
 
-def eval_chebyshev(ev: _Exact, y: Ciphertext, coeffs: np.ndarray, target_scale: float,
-                   tol: float = 1e-14) -> Ciphertext:
-    """p(y) = sum c_i T_i(y) with T_2k = 2T_k^2 - 1, T_2k+1 = 2T_kT_k+1 - T_1."""
-    d = len(coeffs) - 1
-    T: dict[int, Ciphertext] = {1: y}
-    for i in range(2, d + 1):
-        a, b = i // 2, i - i // 2
-        p = ev.double(ev.mul(T[a], T[b]))
-        if a == b:
-            p = ev.add_const(p, -1.0)
+    def cheb_product(self, a: Ciphertext, b: Ciphertext, t1: Ciphertext | None) -> Ciphertext:
+        """T_{i+j} = 2 T_i T_j - T_{|i-j|} with |i-j| in {0, 1}: the doubling
+        and the T_1 (or constant) correction are folded into one scalar-MAC
+        before the single rescale."""
+        lvl = min(a.level, b.level)
+        if lvl < 1:
+            raise LevelError("bootstrap evaluator ran out of levels")
+        p = ckks.hmult(self.drop(a, lvl), self.drop(b, lvl), self.ks)
+        two = [2] * (lvl + 1)
+        if t1 is None:
+            d = self.ctx.scalar_mac([p.data], [two], lvl)
         else:
-            t1 = ev.mul_const(T[1], 1.0, p.scale)
-            p = ev.add(p, t1, sub=True)
-        T[i] = p
-    terms = [ev.mul_const(T[i], float(coeffs[i]), target_scale) for i in range(1, d + 1) if abs(coeffs[i]) > tol]
-    lvl = min(t.level for t in terms)
-    acc = ev.drop(terms[0], lvl)
-    for t in terms[1:]:
-        acc = ev.add(acc, t)
-    return ev.add_const(acc, float(coeffs[0]))
+            k = int(round(p.scale / t1.scale))
+            d = self.ctx.scalar_mac([p.data, t1.data], [two, [-k] * (lvl + 1)], lvl)
+        out = ckks.rescale(Ciphertext(d, p.scale, p.n, p.params), self.params)
+        return self.add_const(out, -1.0, inplace=True) if t1 is None else out
+
+    def lincomb(self, terms: list[tuple[Ciphertext, float]], c0: float, level: int, scale: float) -> Ciphertext:
+        """c0 + sum c_i t_i landing exactly on (level, scale): one scalar-MAC
+        over the level-dropped prefixes at level+1, one rescale."""
+        lvl = level + 1
+        q = self.params.q_mods[lvl].q
+        srcs = [t.data for t, _ in terms]
+        consts = [[int(round(c * scale * q / t.scale))] * (lvl + 1) for t, c in terms]
+        acc = self.ctx.scalar_mac(srcs, consts, lvl)
+        out = ckks.rescale(Ciphertext(acc, scale * q, terms[0][0].n, terms[0][0].params), self.params)
+        return self.add_const(Ciphertext(out.data, scale, out.n, out.params), c0, inplace=True)
+
+
+def cheb_divide(c: np.ndarray, m: int) -> tuple[np.ndarray, np.ndarray]:
+    """p = r + T_m q for deg p < 2m (T_m T_j = (T_{m+j} + T_{m-j})/2)."""
+    d = len(c) - 1
+    q = np.zeros(d - m + 1)
+    q[0] = c[m]
+    q[1:] = 2.0 * c[m + 1:]
+    r = np.array(c[:m], dtype=np.float64)
+    for i in range(1, m):
+        if 2 * m - i <= d:
+            r[i] -= c[2 * m - i]
+    return q, r
+
+
+def _trim(c: np.ndarray, tol: float) -> np.ndarray:
+    d = len(c) - 1
+    while d > 0 and abs(c[d]) <= tol:
+        d -= 1
+    return np.asarray(c[: d + 1], dtype=np.float64)
+
+
+def bsgs_split(c: np.ndarray, baby: int, tol: float = 1e-14):
+    """The recursion tree of the baby-step giant-step evaluation: a leaf is
+    the coefficient vector itself (degree < baby), a node is
+    (m, q_tree, r_tree) with p = r + T_m q."""
+    c = _trim(c, tol)
+    d = len(c) - 1
+    if d < baby:
+        return c
+    m = baby
+    while 2 * m <= d:
+        m *= 2
+    q, r = cheb_divide(c, m)
+    return (m, bsgs_split(q, baby, tol), bsgs_split(r, baby, tol))
+
+
+def bsgs_eval_plain(tree, y: np.ndarray) -> np.ndarray:
+    """Host mirror of the homomorphic evaluation order (tests)."""
+    if isinstance(tree, np.ndarray):
+        return npcheb.chebval(y, tree)
+    m, q, r = tree
+    tm = npcheb.chebval(y, np.eye(m + 1)[m])
+    return bsgs_eval_plain(r, y) + tm * bsgs_eval_plain(q, y)
+
+
+def bsgs_powers(tree, baby: int) -> set[int]:
+    if isinstance(tree, np.ndarray):
+        return set(range(1, len(tree)))
+    m, q, r = tree
+    return {m} | bsgs_powers(q, baby) | bsgs_powers(r, baby)
+
+
+def eval_chebyshev(ev: _Exact, y: Ciphertext, coeffs: np.ndarray, target_scale: float,
+                   baby: int = 8, tol: float = 1e-14) -> Ciphertext:
+    """p(y) = sum c_i T_i(y) by baby-step giant-step: T_1..T_{baby-1} and the
+    giants T_{baby 2^j} (each T one hmult with the 2x and T_1 correction
+    fused), then p = r + T_m q recursively; every leaf is one scalar-MAC and
+    one rescale, every split one hmult.  Depth ceil(log2(d+1)) + 1, about
+    2 sqrt(d) + log d ciphertext products instead of d."""
+    tree = bsgs_split(coeffs, baby, tol)
+    T: dict[int, Ciphertext] = {1: y}
+
+    def power(i: int) -> Ciphertext:
+        if i not in T:
+            a, b = i // 2, i - i // 2
+            T[i] = ev.cheb_product(power(a), power(b), None if a == b else T[1])
+        return T[i]
+
+    for i in sorted(bsgs_powers(tree, baby)):
+        power(i)
+
+    def top(t) -> int:  # highest output level the subtree can land on
+        if isinstance(t, np.ndarray):
+            return min((T[i].level for i in range(1, len(t))), default=y.level) - 1
+        m, q, r = t
+        return min(T[m].level - 1, top(q) - 1, top(r))
+
+    def run(t, level: int, scale: float) -> Ciphertext:
+        if isinstance(t, np.ndarray):
+            terms = [(T[i], float(t[i])) for i in range(1, len(t))] or [(T[1], 0.0)]
+            return ev.lincomb(terms, float(t[0]), level, scale)
+        m, q, r = t
+        lvl = level + 1
+        qp = ev.params.q_mods[lvl].q
+        tm = T[m]
+        qv = run(q, lvl, scale * qp / tm.scale)
+        prod = ckks.rescale(ckks.hmult(ev.drop(tm, lvl), qv, ev.ks), ev.params)
+        return ev.add(Ciphertext(prod.data, scale, prod.n, prod.params), run(r, level, scale))
+
+    level = top(tree)
+    if level < 0:
+        raise LevelError("bootstrap evaluator ran out of levels")
+    return run(tree, level, target_scale)
 
 
 # ---------------------------------------------------------------------------
@@ -413,7 +514,7 @@ class Bootstrapper:
         ev = _Exact(self.params, ks)
         c = eval_chebyshev(ev, y, self.cheb, self.eval_scale)
         for _ in range(self.cfg.double_angle):
-            c = ev.add_const(ev.double(ev.mul(c, c)), -1.0)
+            c = ev.cheb_product(c, c, None)  # cos(2t) = 2 cos(t)^2 - 1
         return c
 
     # -- the pipeline -----------------------------------------------------------

@@ -146,6 +146,35 @@ cudaError_t launch_scalar(int add, u64* out, const u64* a, Basis basis, u32 logN
   return cudaGetLastError();
 }
 
+// linear combination with per-limb integer constants (bootstrapping's
+// Chebyshev leaves and fused T_{a+b} = 2 T_a T_b - T_{a-b}): one pass over
+// the sources, fully reduced Shoup products summed mod q
+__global__ void __launch_bounds__(256) k_scalar_mac(int nt, u64* __restrict__ out, u32 nl, u32 logN, int accumulate,
+                                                    const ModConsts* __restrict__ mc, ScalarMacArgs A) {
+  const u32 N = 1u << logN;
+  const u32 r = blockIdx.y % nl, z = blockIdx.y / nl;
+  const u64 q = mc[r].q;
+  ulonglong2* O = reinterpret_cast<ulonglong2*>(out + ((size_t)z * nl + r) * N);
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < N / 2; i += gridDim.x * blockDim.x) {
+    ulonglong2 acc = accumulate ? O[i] : make_ulonglong2(0, 0);
+    for (int t = 0; t < nt; ++t) {
+      const ulonglong2 x =
+          reinterpret_cast<const ulonglong2*>(A.src[t] + ((size_t)z * A.src_limbs[t] + r) * N)[i];
+      const u64 w = A.w[t][r], wp = A.wp[t][r];
+      acc.x = add_mod(acc.x, shoup_mul(x.x, w, wp, q), q);
+      acc.y = add_mod(acc.y, shoup_mul(x.y, w, wp, q), q);
+    }
+    O[i] = acc;
+  }
+}
+
+cudaError_t launch_scalar_mac(const ScalarMacArgs& A, int nt, u64* out, u32 nl, u32 logN, u32 npolys,
+                              int accumulate, const ModConsts* mc, cudaStream_t st) {
+  if (!nl || !npolys) return cudaSuccess;
+  k_scalar_mac<<<row_grid((1u << logN) / 2, nl * npolys, 256), 256, 0, st>>>(nt, out, nl, logN, accumulate, mc, A);
+  return cudaGetLastError();
+}
+
 // signed int64 coefficients (one row of N per poly) -> residues in every
 // limb (ring.py:446-468 replication, ckks.py:284-288 encode reduction)
 __global__ void k_from_signed(u64* __restrict__ out, const long long* __restrict__ in, Basis basis, u32 logN,

@@ -41,6 +41,19 @@ struct ScalarArgs {
 cudaError_t launch_scalar(int add, u64* out, const u64* a, Basis basis, u32 logN, u32 npolys, const ModConsts* mc,
                           const ScalarArgs& args, cudaStream_t st);
 
+// out (+)= sum_t k_t[limb] * src_t over q-limbs; sources may be level-dropped
+// views of longer ciphertexts (per-source poly stride in limbs)
+constexpr int kSMacTerms = 16;
+constexpr int kSMacLimbs = 48;
+struct ScalarMacArgs {
+  const u64* src[kSMacTerms];
+  u32 src_limbs[kSMacTerms];
+  u64 w[kSMacTerms][kSMacLimbs];
+  u64 wp[kSMacTerms][kSMacLimbs];
+};
+cudaError_t launch_scalar_mac(const ScalarMacArgs& A, int nt, u64* out, u32 nl, u32 logN, u32 npolys,
+                              int accumulate, const ModConsts* mc, cudaStream_t st);
+
 constexpr int kMacMax = 64;
 struct MacTerms {
   const u64* ct[kMacMax];

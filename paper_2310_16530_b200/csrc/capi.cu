@@ -554,6 +554,31 @@ static int scalar_op(hcnn_ctx* c, int op, uint64_t* out, const uint64_t* a, cons
   return HCNN_OK;
 }
 
+int hcnn_scalar_mac(hcnn_ctx* c, uint64_t* out, const uint64_t* const* srcs, const uint32_t* src_limbs,
+                    const uint64_t* consts, uint32_t nterms, uint32_t nq, uint32_t npolys, int accumulate, void* s) {
+  int rc = check_basis(c, nq, 0);
+  if (rc) return rc;
+  if (nq > (u32)kSMacLimbs) return fail(HCNN_E_BASIS, "too many limbs for scalar_mac");
+  ScalarMacArgs A;  // by value: capture-safe
+  for (u32 t0 = 0; t0 < nterms || (t0 == 0 && !accumulate); t0 += kSMacTerms) {
+    const u32 nt = nterms - t0 < (u32)kSMacTerms ? nterms - t0 : (u32)kSMacTerms;
+    for (u32 t = 0; t < nt; ++t) {
+      if (src_limbs[t0 + t] < nq) return fail(HCNN_E_BASIS, "scalar_mac source has fewer limbs than the output");
+      A.src[t] = srcs[t0 + t];
+      A.src_limbs[t] = src_limbs[t0 + t];
+      for (u32 r = 0; r < nq; ++r) {
+        const u64 q = c->mods[r];
+        A.w[t][r] = consts[(size_t)(t0 + t) * nq + r] % q;
+        A.wp[t][r] = h_shoup(A.w[t][r], q);
+      }
+    }
+    PK("scalar_mac", 8.0 * (nt + 1 + ((accumulate || t0) ? 1 : 0)) * nq * npolys * c->n, 1, STREAM(s),
+       launch_scalar_mac(A, (int)nt, out, nq, c->logN, npolys, accumulate || t0 > 0, c->d_mc, STREAM(s)));
+    if (nterms == 0) break;
+  }
+  return HCNN_OK;
+}
+
 int hcnn_from_signed(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np, uint32_t npolys,
                      void* s) {
   int rc = check_basis(c, nq, np);

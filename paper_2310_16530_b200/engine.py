@@ -235,6 +235,29 @@ class DeviceContext:
                                           _stream()))
         return out
 
+    def scalar_mac(self, srcs: Sequence[torch.Tensor], consts: Sequence[Sequence[int]], level: int,
+                   out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+        """out[2, level+1, N] (+)= sum_t consts[t][r] * srcs[t] per limb r;
+        srcs[t] are contiguous [2, >=level+1, N] ciphertext tensors (a longer
+        one is read as its level-dropped prefix)."""
+        nq = level + 1
+        if out is None:
+            out = self.empty(2, nq, self.n)
+        n = len(srcs)
+        for s in srcs:
+            if not s.is_contiguous() or s.dim() != 3 or s.shape[0] != 2 or s.shape[1] < nq:
+                raise BasisError("scalar_mac sources must be contiguous [2, >=level+1, N]")
+        flat = [int(v) % self.q_list[r] for row in consts for r, v in enumerate(row[:nq])]
+        if any(len(row) < nq for row in consts) or len(consts) != n:
+            raise BasisError("scalar_mac needs one constant per limb per source")
+        P = ctypes.c_void_p * max(n, 1)
+        L = ctypes.c_uint32 * max(n, 1)
+        sp = P(*[s.data_ptr() for s in srcs])
+        sl = L(*[s.shape[1] for s in srcs])
+        self._chk(self.lib.hcnn_scalar_mac(self.handle, _ptr(out), sp, sl, _native.u64_array(flat or [0]), n, nq, 2,
+                                           1 if accumulate else 0, _stream()))
+        return out
+
     def rescale(self, a: torch.Tensor, level: int) -> torch.Tensor:
         npolys = self._npolys(a, level + 1, 0, self.n)
         out = self.empty(npolys, level, self.n)

@@ -78,3 +78,45 @@ def test_depth_budget_and_chain():
     p = bt.boot_params("b", 1 << 12, 4, bt.BootConfig(cts_stages=(4, 4, 3), stc_stages=(3, 4, 4)))
     assert p.max_level == 4 + 3 + cfg.evalmod_depth() + 3
     assert all(m.q.bit_length() <= 61 for m in p.q_mods + p.p_mods)
+
+
+def _levels(tree, baby, top_level):
+    """level simulation of eval_chebyshev: T_i at top - ceil(log2 i)"""
+    lv = {i: top_level - math.ceil(math.log2(i)) if i > 1 else top_level for i in bt.bsgs_powers(tree, baby)}
+
+    def top(t):
+        if isinstance(t, np.ndarray):
+            return min((lv[i] for i in range(1, len(t))), default=top_level) - 1
+        m, q, r = t
+        return min(lv[m] - 1, top(q) - 1, top(r))
+    return top(tree)
+
+
+def _products(tree):
+    if isinstance(tree, np.ndarray):
+        return 0
+    return 1 + _products(tree[1]) + _products(tree[2])
+
+
+@pytest.mark.parametrize("baby", [4, 8])
+def test_bsgs_chebyshev_matches_direct_evaluation(baby):
+    cfg = bt.BootConfig()
+    c = bt.evalmod_coeffs(cfg)
+    tree = bt.bsgs_split(c, baby)
+    y = np.linspace(-1, 1, 2001)
+    assert np.max(np.abs(bt.bsgs_eval_plain(tree, y) - np.polynomial.chebyshev.chebval(y, c))) < 1e-12
+    # depth within the evalmod budget, far fewer ciphertext products than degree
+    assert 40 - _levels(tree, baby, 40) <= math.ceil(math.log2(cfg.degree)) + 1
+    powers = bt.bsgs_powers(tree, baby)
+    assert len(powers) + _products(tree) <= 2 * int(math.sqrt(cfg.degree)) + 10
+
+
+def test_cheb_divide_identity():
+    rng = np.random.default_rng(4)
+    for d, m in [(7, 4), (15, 8), (59, 32), (33, 32)]:
+        c = rng.standard_normal(d + 1)
+        q, r = bt.cheb_divide(c, m)
+        y = np.linspace(-1, 1, 101)
+        tm = np.polynomial.chebyshev.chebval(y, np.eye(m + 1)[m])
+        ch = np.polynomial.chebyshev.chebval
+        assert np.allclose(ch(y, r) + tm * ch(y, q), ch(y, c), atol=1e-12)

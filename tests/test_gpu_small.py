@@ -139,3 +139,25 @@ def test_elementwise(small, cts, golden_small):
     assert np.array_equal(_ct(ckks.pmult(ct1, pt1)), golden_small["pmult"])
     assert np.array_equal(_ct(ckks.hadd(ct1, ct2)), golden_small["hadd"])
     assert np.array_equal(_ct(ckks.padd(ct1, pt1)), golden_small["padd"])
+
+
+def test_scalar_mac_exact(small, cts):
+    """sum_t k_t * src_t per limb (prefix read of a longer source), checked
+    with Python integers; > 16 terms exercises the batched launches."""
+    params, _ = small
+    _, ct1, ct2 = cts
+    ctx = params.ctx
+    lvl = ct1.level - 1
+    srcs = [ct1.data, ct2.data] * 9
+    rng = np.random.default_rng(9)
+    consts = [[int(v) for v in rng.integers(-(1 << 62), 1 << 62, size=lvl + 1)] for _ in srcs]
+    out = ctx.scalar_mac(srcs, consts, lvl).cpu().numpy().astype(object)
+    hs = [s.cpu().numpy().astype(object) for s in srcs]
+    for r in range(lvl + 1):
+        q = params.q_mods[r].q
+        want = sum(h[:, r, :] * (c[r] % q) for h, c in zip(hs, consts)) % q
+        assert np.array_equal(out[:, r, :], want)
+    acc = ctx.scalar_mac(srcs[:1], consts[:1], lvl, out=ctx.scalar_mac(srcs[1:2], consts[1:2], lvl),
+                         accumulate=True).cpu().numpy().astype(object)
+    q0 = params.q_mods[0].q
+    assert np.array_equal(acc[:, 0, :], (hs[0][:, 0, :] * (consts[0][0] % q0) + hs[1][:, 0, :] * (consts[1][0] % q0)) % q0)
