@@ -101,6 +101,11 @@ int hcnn_scalar_add(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint6
  * sample_poly replication ring.py:463-467, encode reduction ckks.py:284-288 */
 int hcnn_from_signed(hcnn_ctx* ctx, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np, uint32_t npolys,
                      void* stream);
+/* as hcnn_from_signed, output in Montgomery form (v R mod q): NTT-linear, so
+ * NTT(from_signed_mont(v)) == to_mont(NTT(from_signed(v))) bit for bit --
+ * the mask path's to_mont pass folded away (packing.py _mask_pt rows) */
+int hcnn_from_signed_mont(hcnn_ctx* ctx, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np,
+                          uint32_t npolys, void* stream);
 /* automorphism X -> X^g.  eval_domain=0: ring.automorphism ring.py:427-439
  * (coefficient domain, signed permutation); eval_domain=1: the equivalent
  * index permutation of the bit-reversed NTT output. */
@@ -127,6 +132,23 @@ int hcnn_hmult(hcnn_ctx* ctx, uint64_t* out_ct, const uint64_t* a_ct, const uint
 int hcnn_rotate_hoisted(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* ct, uint32_t level, uint32_t n_rot,
                         const uint64_t* galois, const uint64_t* const* keys_b, const uint64_t* const* keys_a,
                         void* ws, void* stream);
+/* ---- batched ciphertext ops ---------------------------------------------
+ * A batch is nb ciphertexts stored back to back ([nb][2][level+1][N]); every
+ * kernel of the op covers the whole batch and each key / mask load feeds
+ * several entries.  Entry-wise bit-exact with the single-ciphertext calls. */
+size_t hcnn_ks_workspace_bytes_batch(const hcnn_ctx* ctx, uint32_t level, uint32_t nb);
+int hcnn_hmult_batch(hcnn_ctx* ctx, uint64_t* out_cts, const uint64_t* a_cts, const uint64_t* b_cts, uint32_t level,
+                     uint32_t nb, const uint64_t* rlk_b, const uint64_t* rlk_a, void* ws, void* stream);
+/* outs[i]: batch buffer receiving rotation i of every entry */
+int hcnn_rotate_hoisted_batch(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* cts, uint32_t level,
+                              uint32_t nb, uint32_t n_rot, const uint64_t* galois, const uint64_t* const* keys_b,
+                              const uint64_t* const* keys_a, void* ws, void* stream);
+/* hcnn_mac_terms over batches: cts[t] and out_cts are batches, the masks are
+ * shared by every entry (bootstrapping's CtS/StC diagonals) */
+int hcnn_mac_terms_batch(hcnn_ctx* ctx, uint64_t* out_cts, const uint64_t* const* cts,
+                         const uint64_t* const* masks_mont, uint32_t n_terms, uint32_t level, uint32_t nb,
+                         int accumulate, void* stream);
+
 /* rescale ckks.py:506-528 for npolys polys at `level` -> level-1 */
 size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* ctx, uint32_t npolys);
 int hcnn_rescale(hcnn_ctx* ctx, uint64_t* out, const uint64_t* in, uint32_t level, uint32_t npolys, void* ws,
@@ -144,10 +166,12 @@ int hcnn_mac_terms(hcnn_ctx* ctx, uint64_t* out_ct, const uint64_t* const* cts, 
  * poly (a longer ciphertext is read as its level-dropped prefix).  Replaces
  * the per-coefficient mul_const / add chain of a Chebyshev evaluation
  * (no reference counterpart: the reference has no bootstrapping,
- * ckks.py:667-690 debug_refresh); any number of terms (batched by 16). */
+ * ckks.py:667-690 debug_refresh); any number of terms (batched by 16).
+ * c0_add (nullable, one per limb) is added to every even poly (the c0 of
+ * each ciphertext): a plaintext constant joins the same pass. */
 int hcnn_scalar_mac(hcnn_ctx* ctx, uint64_t* out, const uint64_t* const* srcs, const uint32_t* src_limbs,
                     const uint64_t* consts, uint32_t n_terms, uint32_t nq, uint32_t npolys, int accumulate,
-                    void* stream);
+                    const uint64_t* c0_add, void* stream);
 
 /* ---- instrumentation ------------------------------------------------------ */
 /* count of engine kernels launched since load (all contexts) */

@@ -38,6 +38,7 @@ from dataclasses import dataclass
 
 import numpy as np
 import scipy.sparse as sp
+import torch
 from numpy.polynomial import chebyshev as npcheb
 
 from . import ckks
@@ -269,9 +270,9 @@ class _Exact:
         return [k % m.q for m in self.params.mods_at(level)]
 
     def add_const(self, a: Ciphertext, c: float, inplace: bool = False) -> Ciphertext:
-        k = int(round(c * a.scale))
+        """a + c exactly at a's scale (every c0 of a batch)."""
         out = a.data if inplace else a.data.clone()
-        self.ctx.scalar_mul(out[0], self._int_consts(k, a.level), a.level + 1, out=out[0], add=True)
+        self.ctx.scalar_mac([], [], a.level, out=out, accumulate=True, c0_add=int(round(c * a.scale)))
         return Ciphertext(out, a.scale, a.n, a.params)
 
     def mul_const(self, a: Ciphertext, c: float, target_scale: float) -> Ciphertext:
@@ -294,13 +295,12 @@ class _Exact:
             raise LevelError("bootstrap evaluator ran out of levels")
         p = ckks.hmult(self.drop(a, lvl), self.drop(b, lvl), self.ks)
         two = [2] * (lvl + 1)
-        if t1 is None:
-            d = self.ctx.scalar_mac([p.data], [two], lvl)
+        if t1 is None:  # 2 T_a^2 - 1: the constant at the product's scale
+            d = self.ctx.scalar_mac([p.data], [two], lvl, c0_add=-int(round(p.scale)))
         else:
             k = int(round(p.scale / t1.scale))
             d = self.ctx.scalar_mac([p.data, t1.data], [two, [-k] * (lvl + 1)], lvl)
-        out = ckks.rescale(Ciphertext(d, p.scale, p.n, p.params), self.params)
-        return self.add_const(out, -1.0, inplace=True) if t1 is None else out
+        return ckks.rescale(Ciphertext(d, p.scale, p.n, p.params), self.params)
 
     def lincomb(self, terms: list[tuple[Ciphertext, float]], c0: float, level: int, scale: float) -> Ciphertext:
         """c0 + sum c_i t_i landing exactly on (level, scale): one scalar-MAC
@@ -309,9 +309,9 @@ class _Exact:
         q = self.params.q_mods[lvl].q
         srcs = [t.data for t, _ in terms]
         consts = [[int(round(c * scale * q / t.scale))] * (lvl + 1) for t, c in terms]
-        acc = self.ctx.scalar_mac(srcs, consts, lvl)
+        acc = self.ctx.scalar_mac(srcs, consts, lvl, c0_add=int(round(c0 * scale * q)))
         out = ckks.rescale(Ciphertext(acc, scale * q, terms[0][0].n, terms[0][0].params), self.params)
-        return self.add_const(Ciphertext(out.data, scale, out.n, out.params), c0, inplace=True)
+        return Ciphertext(out.data, scale, out.n, out.params)
 
 
 def cheb_divide(c: np.ndarray, m: int) -> tuple[np.ndarray, np.ndarray]:
@@ -440,7 +440,8 @@ class Bootstrapper:
 
     # -- keys ---------------------------------------------------------------
     def rotation_steps(self) -> set[int]:
-        return plan_rotations(self.cts_plans) | plan_rotations(self.stc_plans)
+        # + slots/2: X -> -X, unpacks two even-polynomial messages (bootstrap_pairs)
+        return plan_rotations(self.cts_plans) | plan_rotations(self.stc_plans) | {self.params.slots // 2}
 
     def keygen(self, rng: np.random.Generator, rotations=()) -> KeySet:
         steps = sorted(set(rotations) | self.rotation_steps())
@@ -528,7 +529,12 @@ class Bootstrapper:
         uc = ckks.conjugate(u, ks)
         y_lo = ev.add(u, uc)                                                   # t_lo / (q0 B)
         y_hi = ckks.mul_monomial(ev.add(u, uc, sub=True), 3 * params.n // 2)  # -i * 2i Im u
-        v_lo, v_hi = self.eval_mod(y_lo, ks), self.eval_mod(y_hi, ks)
+        # both halves (of every batch entry) through one EvalMod pass
+        both = torch.cat([y_lo.data, y_hi.data]) if u.batch is not None else torch.stack([y_lo.data, y_hi.data])
+        vb = self.eval_mod(Ciphertext(both, y_lo.scale, y_lo.n, y_lo.params), ks)
+        h = vb.data.shape[0] // 2
+        v_lo = Ciphertext(vb.data[:h] if u.batch is not None else vb.data[0], vb.scale, vb.n, vb.params)
+        v_hi = Ciphertext(vb.data[h:] if u.batch is not None else vb.data[1], vb.scale, vb.n, vb.params)
         v = ev.add(v_lo, ckks.mul_monomial(v_hi, params.n // 2))              # 2 pi (m_lo + i m_hi) / q0
         # StC computes U0 BR; slots of the message are U0 m / Delta1 = v q0 / (2 pi Delta1)
         v = self._relabel(v, v.scale * (2.0 * math.pi * delta1) / self.q0)
@@ -536,3 +542,52 @@ class Bootstrapper:
         if out.level > self.output_level:
             out = ckks.mod_drop(out, self.output_level)
         return out
+
+    def bootstrap_many(self, cts: list[Ciphertext], ks: KeySet, max_batch: int = 16,
+                       out_scale_factor: float = 1.0) -> list[Ciphertext]:
+        """Bootstrap several ciphertexts; members sharing (level, scale) run
+        as one batch (every kernel covers the batch, key and diagonal loads
+        are shared).  Entry-wise identical to ``bootstrap``."""
+        out: list[Ciphertext | None] = [None] * len(cts)
+        groups: dict = {}
+        for i, c in enumerate(cts):
+            groups.setdefault((c.level, c.scale), []).append(i)
+        for idx in groups.values():
+            for s0 in range(0, len(idx), max_batch):
+                part = idx[s0:s0 + max_batch]
+                osc = cts[part[0]].scale * out_scale_factor
+                if len(part) == 1:
+                    out[part[0]] = self.bootstrap(cts[part[0]], ks, osc)
+                    continue
+                res = ckks.unstack(self.bootstrap(ckks.stack([cts[i] for i in part]), ks, osc))
+                for i, r in zip(part, res):
+                    out[i] = r
+        return out
+
+    def bootstrap_pairs(self, pairs: list[tuple[Ciphertext, Ciphertext]], ks: KeySet) -> list[tuple[Ciphertext, Ciphertext]]:
+        """Two ciphertexts per bootstrap.  Both members must encrypt even
+        polynomials (slot vectors invariant under rotation by slots/2, see
+        packing.slot_period) at one level and scale.  m = a + X b is
+        bootstrapped once (at half the scale); then with s: X -> -X (the
+        rotation by slots/2), a = (m + s(m))/2 and b = X^-1 (m - s(m))/2 --
+        no level, one rotation for the whole batch."""
+        if not pairs:
+            return []
+        n = self.params.n
+        packed = [ckks.hadd(a, ckks.mul_monomial(b, 1)) for a, b in pairs]
+        outs = self.bootstrap_many(packed, ks, out_scale_factor=0.5)
+        res: list = [None] * len(pairs)
+        groups: dict = {}
+        for i, o in enumerate(outs):
+            groups.setdefault((o.level, o.scale), []).append(i)
+        ctx = self.params.ctx
+        for idx in groups.values():
+            o = outs[idx[0]] if len(idx) == 1 else ckks.stack([outs[i] for i in idx])
+            r = ckks.rotate(o, self.params.slots // 2, ks)
+            lvl = o.level
+            even = Ciphertext(ctx.binop("add", o.data, r.data, lvl + 1), 2.0 * o.scale, o.n, o.params)
+            odd = ckks.mul_monomial(Ciphertext(ctx.binop("sub", o.data, r.data, lvl + 1), 2.0 * o.scale, o.n, o.params),
+                                    2 * n - 1)
+            for k, a_out, b_out in zip(idx, ckks.unstack(even), ckks.unstack(odd)):
+                res[k] = (a_out, b_out)
+        return res

@@ -164,6 +164,10 @@ __global__ void __launch_bounds__(256) k_scalar_mac(int nt, u64* __restrict__ ou
       acc.x = add_mod(acc.x, shoup_mul(x.x, w, wp, q), q);
       acc.y = add_mod(acc.y, shoup_mul(x.y, w, wp, q), q);
     }
+    if (A.has_add0 && (z & 1) == 0) {
+      acc.x = add_mod(acc.x, A.add0[r], q);
+      acc.y = add_mod(acc.y, A.add0[r], q);
+    }
     O[i] = acc;
   }
 }
@@ -178,16 +182,17 @@ cudaError_t launch_scalar_mac(const ScalarMacArgs& A, int nt, u64* out, u32 nl, 
 // signed int64 coefficients (one row of N per poly) -> residues in every
 // limb (ring.py:446-468 replication, ckks.py:284-288 encode reduction)
 __global__ void k_from_signed(u64* __restrict__ out, const long long* __restrict__ in, Basis basis, u32 logN,
-                              const ModConsts* __restrict__ mc) {
+                              const ModConsts* __restrict__ mc, int mont) {
   RowCtx rc = row_ctx(basis);
   const u32 N = 1u << logN;
   const ModConsts C = mc[rc.mod];
   const long long* src = in + (size_t)rc.z * N;
   u64* O = out + (size_t)rc.row * N;
+  const u64 k = mont ? C.r2 : C.one_m;  // |v| R mod q (Montgomery form) or |v| mod q
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
     long long v = src[i];
     u64 mag = v >= 0 ? (u64)v : (u64)(-(v + 1)) + 1ull;
-    u64 red = mont_mul(mag, C.one_m, C.q, C.ninv);  // |v| mod q
+    u64 red = mont_mul(mag, k, C.q, C.ninv);
     O[i] = v >= 0 ? red : neg_mod(red, C.q);
   }
 }
@@ -298,10 +303,11 @@ template <int NS>
 __global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, int tab_per_z,
                                                const ModConsts* __restrict__ mc, const u64* __restrict__ in,
                                                size_t in_pst, u64* __restrict__ out, size_t out_pst, u32 logN,
-                                               u32 nt_override, u32 z0) {
+                                               u32 nt_override, u32 z0, u32 zdiv, size_t in_bst, size_t out_bst) {
   constexpr int NM = 1 << NS;
   extern __shared__ u64 sh[];
-  const u32 N = 1u << logN, z = blockIdx.y + z0;
+  // blockIdx.y = b * zdiv + j: poly/digit j of batch entry b
+  const u32 N = 1u << logN, b = blockIdx.y / zdiv, z = blockIdx.y % zdiv + z0;
   const FbcDev& T = tabs[tab_per_z ? z : 0];
   const u32 nt_all = nt_override ? nt_override : T.nt;
   // blockIdx.z selects a group of kFbcTG targets (more CTAs; y recomputed)
@@ -330,8 +336,8 @@ __global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, 
     ips[i] = T.inv_punc_sh[i];
   }
   __syncthreads();
-  const u64* src = in + (size_t)z * in_pst;
-  u64* dst = out + (size_t)z * out_pst;
+  const u64* src = in + (size_t)b * in_bst + (size_t)z * in_pst;
+  u64* dst = out + (size_t)b * out_bst + (size_t)z * out_pst;
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
     u64 y[NS];
     u32 mask = 0;
@@ -376,42 +382,86 @@ __global__ void k_modup(const FbcDev* __restrict__ tabs, const ModConsts* __rest
 // (key rows are Montgomery form, so the 128-bit sum REDCs straight to the
 // ordinary residue).  g != 1 applies the eval-domain Galois permutation to
 // the raised digits on the fly (hoisted rotation).
+int g_ks_batch = 1;  // measured: grid-batched entries share keys through L2; NB>1 costs occupancy
+
+template <int NB, int VEC>
 __global__ void __launch_bounds__(256) k_ks_inner(u64* __restrict__ acc, const u64* __restrict__ x_eval,
                                                   const u64* __restrict__ raised, const u64* __restrict__ key_b,
                                                   const u64* __restrict__ key_a, Basis basis, u32 alpha, u32 ndig,
-                                                  u32 logN, u64 g, const ModConsts* __restrict__ mc) {
+                                                  u32 logN, u64 g, const ModConsts* __restrict__ mc, u32 nb,
+                                                  size_t x_bst) {
+  // VEC adjacent coefficients x NB batch entries per thread (NB*VEC <= 4 keeps
+  // the 128-bit accumulators at 16 registers pairs: full occupancy)
   const u32 N = 1u << logN, r = blockIdx.y;
   const u32 n_ext = basis.nlimbs();
   const u32 mod = basis.mod_of(r);
   const u64 q = mc[mod].q, ninv = mc[mod].ninv;
   const size_t key_dst = (size_t)(basis.Lq + basis.np) * N;  // per-digit key stride
   const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;     // digit owning limb r
-  // two adjacent coefficients per thread: 16-byte key / raised / acc accesses
-  for (u32 k2 = blockIdx.x * blockDim.x + threadIdx.x; k2 < N / 2; k2 += gridDim.x * blockDim.x) {
-    const u32 k = 2 * k2;
-    u64 bh0 = 0, bl0 = 0, ah0 = 0, al0 = 0, bh1 = 0, bl1 = 0, ah1 = 0, al1 = 0;
+  const u32 b0 = blockIdx.z * NB;                             // NB batch entries share every key load
+  const u32 ne = nb - b0 < (u32)NB ? nb - b0 : (u32)NB;
+  const size_t r_bst = (size_t)ndig * n_ext * N, a_bst = 2 * (size_t)n_ext * N;
+  for (u32 kv = blockIdx.x * blockDim.x + threadIdx.x; kv < N / VEC; kv += gridDim.x * blockDim.x) {
+    const u32 k = VEC * kv;
+    u64 bh[NB][VEC], bl[NB][VEC], ah[NB][VEC], al[NB][VEC];
+#pragma unroll
+    for (int e = 0; e < NB; ++e)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) bh[e][v] = bl[e][v] = ah[e][v] = al[e][v] = 0;
 #pragma unroll 2
     for (u32 j = 0; j < ndig; ++j) {
-      const u64* src = (j == own) ? x_eval + (size_t)r * N : raised + ((size_t)j * n_ext + r) * N;
-      ulonglong2 v;
-      if (g == 1) {
-        v = *reinterpret_cast<const ulonglong2*>(src + k);
-      } else {
-        v.x = src[galois_src(k, g, logN)];
-        v.y = src[galois_src(k + 1, g, logN)];
-      }
       const size_t kofs = (size_t)j * key_dst + (size_t)mod * N + k;
-      const ulonglong2 kb = *reinterpret_cast<const ulonglong2*>(key_b + kofs);
-      const ulonglong2 ka = *reinterpret_cast<const ulonglong2*>(key_a + kofs);
-      mac128(bh0, bl0, v.x, kb.x, q);
-      mac128(bh1, bl1, v.y, kb.y, q);
-      mac128(ah0, al0, v.x, ka.x, q);
-      mac128(ah1, al1, v.y, ka.y, q);
+      u64 kb[VEC], ka[VEC];
+      if (VEC == 2) {
+        const ulonglong2 b2 = *reinterpret_cast<const ulonglong2*>(key_b + kofs);
+        const ulonglong2 a2 = *reinterpret_cast<const ulonglong2*>(key_a + kofs);
+        kb[0] = b2.x;
+        kb[VEC - 1] = b2.y;
+        ka[0] = a2.x;
+        ka[VEC - 1] = a2.y;
+      } else {
+        kb[0] = key_b[kofs];
+        ka[0] = key_a[kofs];
+      }
+#pragma unroll
+      for (int e = 0; e < NB; ++e) {
+        if ((u32)e >= ne) break;
+        const u64* src = (j == own) ? x_eval + (size_t)(b0 + e) * x_bst + (size_t)r * N
+                                    : raised + (size_t)(b0 + e) * r_bst + ((size_t)j * n_ext + r) * N;
+        u64 x[VEC];
+        if (g == 1) {
+          if (VEC == 2) {
+            const ulonglong2 x2 = *reinterpret_cast<const ulonglong2*>(src + k);
+            x[0] = x2.x;
+            x[VEC - 1] = x2.y;
+          } else {
+            x[0] = src[k];
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) x[v] = src[galois_src(k + v, g, logN)];
+        }
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          mac128(bh[e][v], bl[e][v], x[v], kb[v], q);
+          mac128(ah[e][v], al[e][v], x[v], ka[v], q);
+        }
+      }
     }
-    *reinterpret_cast<ulonglong2*>(acc + (size_t)r * N + k) =
-        make_ulonglong2(redc128(bh0, bl0, q, ninv), redc128(bh1, bl1, q, ninv));
-    *reinterpret_cast<ulonglong2*>(acc + ((size_t)n_ext + r) * N + k) =
-        make_ulonglong2(redc128(ah0, al0, q, ninv), redc128(ah1, al1, q, ninv));
+#pragma unroll
+    for (int e = 0; e < NB; ++e) {
+      if ((u32)e >= ne) break;
+      u64* A = acc + (size_t)(b0 + e) * a_bst;
+      if (VEC == 2) {
+        *reinterpret_cast<ulonglong2*>(A + (size_t)r * N + k) =
+            make_ulonglong2(redc128(bh[e][0], bl[e][0], q, ninv), redc128(bh[e][VEC - 1], bl[e][VEC - 1], q, ninv));
+        *reinterpret_cast<ulonglong2*>(A + ((size_t)n_ext + r) * N + k) =
+            make_ulonglong2(redc128(ah[e][0], al[e][0], q, ninv), redc128(ah[e][VEC - 1], al[e][VEC - 1], q, ninv));
+      } else {
+        A[(size_t)r * N + k] = redc128(bh[e][0], bl[e][0], q, ninv);
+        A[((size_t)n_ext + r) * N + k] = redc128(ah[e][0], al[e][0], q, ninv);
+      }
+    }
   }
 }
 
@@ -421,14 +471,17 @@ __global__ void __launch_bounds__(256) k_moddown_combine(u64* __restrict__ out0,
                                                          const u64* __restrict__ add0, const u64* __restrict__ add1,
                                                          u64 g_add, u32 nq, u32 n_ext, u32 logN,
                                                          const u64* __restrict__ pinv, const u64* __restrict__ pinv_sh,
-                                                         const ModConsts* __restrict__ mc) {
-  const u32 N = 1u << logN, r = blockIdx.y, z = blockIdx.z;
+                                                         const ModConsts* __restrict__ mc, size_t out_bst,
+                                                         size_t add_bst) {
+  // z = 2 b + p: poly p of batch entry b (acc [nb][2][n_ext], lift [nb][2][nq])
+  const u32 N = 1u << logN, r = blockIdx.y, z = blockIdx.z, b = z >> 1, p = z & 1;
   const u64 q = mc[r].q;
   const u64 w = pinv[r], wp = pinv_sh[r];
   const u64* A = acc + ((size_t)z * n_ext + r) * N;
   const u64* L = lift + ((size_t)z * nq + r) * N;
-  const u64* ADD = z == 0 ? add0 : add1;
-  u64* O = (z == 0 ? out0 : out1) + (size_t)r * N;
+  const u64* ADD = p == 0 ? add0 : add1;
+  if (ADD) ADD += (size_t)b * add_bst;
+  u64* O = (p == 0 ? out0 : out1) + (size_t)b * out_bst + (size_t)r * N;
   for (u32 k2 = blockIdx.x * blockDim.x + threadIdx.x; k2 < N / 2; k2 += gridDim.x * blockDim.x) {
     const u32 k = 2 * k2;
     const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(A + k);
@@ -457,25 +510,45 @@ __global__ void __launch_bounds__(256) k_moddown_combine(u64* __restrict__ out0,
 // with the reference's hadd(pmult_mont) chain since every partial result
 // is canonical).  accumulate: out += sum.
 // ---------------------------------------------------------------------------
+template <int NB>
 __global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __restrict__ out, u32 nq, u32 logN,
-                                                   int accumulate, const ModConsts* __restrict__ mc) {
-  const u32 N = 1u << logN, r = blockIdx.y, z = blockIdx.z;
+                                                   int accumulate, const ModConsts* __restrict__ mc, u32 nb) {
+  // blockIdx.z = 2 * chunk + poly; NB batch entries (ciphertexts 2*nq*N apart) share each mask load
+  const u32 N = 1u << logN, r = blockIdx.y, p = blockIdx.z & 1, b0 = (blockIdx.z >> 1) * NB;
   const u64 q = mc[r].q, ninv = mc[r].ninv;
-  const size_t off = ((size_t)z * nq + r) * N, moff = (size_t)r * N;
+  const size_t bst = 2 * (size_t)nq * N;
+  const size_t off = ((size_t)p * nq + r) * N + (size_t)b0 * bst, moff = (size_t)r * N;
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
-    u64 hi = 0, lo = 0;
-    for (int t = 0; t < nt; ++t) mac128(hi, lo, T.ct[t][off + k], T.mask[t][moff + k], q);
-    u64 v = redc128(hi, lo, q, ninv);
-    if (accumulate) v = add_mod(v, out[off + k], q);
-    out[off + k] = v;
+    u64 hi[NB], lo[NB];
+#pragma unroll
+    for (int e = 0; e < NB; ++e) hi[e] = lo[e] = 0;
+#pragma unroll 4
+    for (int t = 0; t < nt; ++t) {
+      const u64 m = T.mask[t][moff + k];
+#pragma unroll
+      for (int e = 0; e < NB; ++e)
+        if (b0 + e < nb) mac128(hi[e], lo[e], T.ct[t][off + e * bst + k], m, q);
+    }
+#pragma unroll
+    for (int e = 0; e < NB; ++e) {
+      if (b0 + e >= nb) break;
+      u64 v = redc128(hi[e], lo[e], q, ninv);
+      if (accumulate) v = add_mod(v, out[off + e * bst + k], q);
+      out[off + e * bst + k] = v;
+    }
   }
 }
 
 cudaError_t launch_mac_terms(const MacTerms& T, int nt, u64* out, u32 nq, u32 logN, int accumulate,
-                             const ModConsts* mc, cudaStream_t st) {
+                             const ModConsts* mc, cudaStream_t st, u32 nb) {
   dim3 g = row_grid(1u << logN, nq, 256);
-  g.z = 2;
-  k_mac_terms<<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc);
+  if (nb <= 1) {
+    g.z = 2;
+    k_mac_terms<1><<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc, 1);
+  } else {
+    g.z = 2 * ((nb + 3) / 4);
+    k_mac_terms<4><<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc, nb);
+  }
   return cudaGetLastError();
 }
 
@@ -541,10 +614,10 @@ cudaError_t launch_ew_unary(int op, u64* out, const u64* a, Basis basis, u32 log
 }
 
 cudaError_t launch_from_signed(u64* out, const long long* in, Basis basis, u32 logN, u32 npolys,
-                               const ModConsts* mc, cudaStream_t st) {
+                               const ModConsts* mc, int mont, cudaStream_t st) {
   u32 rows = npolys * basis.nlimbs();
   if (!rows) return cudaSuccess;
-  k_from_signed<<<row_grid(1u << logN, rows, 256), 256, 0, st>>>(out, in, basis, logN, mc);
+  k_from_signed<<<row_grid(1u << logN, rows, 256), 256, 0, st>>>(out, in, basis, logN, mc, mont);
   return cudaGetLastError();
 }
 
@@ -570,28 +643,30 @@ static size_t fbc_smem(u32 nt, int ns) {
 template <int NS>
 static cudaError_t launch_fbc_t(const FbcDev* tabs, int tab_per_z, const ModConsts* mc, const u64* in,
                                 size_t in_pst, u64* out, size_t out_pst, u32 logN, u32 nz, u32 z0, u32 nt,
-                                u32 nt_override, cudaStream_t st) {
+                                u32 nt_override, u32 nb, size_t in_bst, size_t out_bst, cudaStream_t st) {
   size_t sm = fbc_smem(nt, NS);
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_fbc_t<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
   }
-  dim3 g = row_grid((1u << logN) / 2, nz, 256);
+  dim3 g = row_grid((1u << logN) / 2, nz * nb, 256);
   g.z = (nt + kFbcTG - 1) / kFbcTG;
-  k_fbc_t<NS><<<g, 256, sm, st>>>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nt_override, z0);
+  k_fbc_t<NS><<<g, 256, sm, st>>>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nt_override, z0, nz, in_bst,
+                                  out_bst);
   return cudaGetLastError();
 }
 
 static cudaError_t dispatch_fbc_t(int ns, const FbcDev* tabs, int tab_per_z, const ModConsts* mc, const u64* in,
                                   size_t in_pst, u64* out, size_t out_pst, u32 logN, u32 nz, u32 z0, u32 nt,
-                                  u32 nt_override, cudaStream_t st) {
+                                  u32 nt_override, cudaStream_t st, u32 nb = 1, size_t in_bst = 0,
+                                  size_t out_bst = 0) {
   switch (ns) {
-    case 1: return launch_fbc_t<1>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
-    case 2: return launch_fbc_t<2>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
-    case 3: return launch_fbc_t<3>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
-    case 4: return launch_fbc_t<4>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
-    case 5: return launch_fbc_t<5>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
-    case 6: return launch_fbc_t<6>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, st);
+    case 1: return launch_fbc_t<1>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, nb, in_bst, out_bst, st);
+    case 2: return launch_fbc_t<2>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, nb, in_bst, out_bst, st);
+    case 3: return launch_fbc_t<3>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, nb, in_bst, out_bst, st);
+    case 4: return launch_fbc_t<4>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, nb, in_bst, out_bst, st);
+    case 5: return launch_fbc_t<5>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, nb, in_bst, out_bst, st);
+    case 6: return launch_fbc_t<6>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nz, z0, nt, nt_override, nb, in_bst, out_bst, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -606,12 +681,15 @@ cudaError_t launch_fbc(const FbcDev& T, const FbcDev* dT, const ModConsts* mc, c
 }
 
 cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, const ModConsts* mc, const u64* xc,
-                         u64* raised, u32 alpha, u32 n_ext, u32 logN, cudaStream_t st) {
+                         u64* raised, u32 alpha, u32 n_ext, u32 logN, cudaStream_t st, u32 nb, size_t xc_bst) {
   if (alpha > FBC_MAX_SRC) return cudaErrorInvalidValue;
   bool fast = true;
   for (u32 j = 0; j < ndig; ++j) fast = fast && htabs[j].corr && htabs[j].nored && htabs[j].ns <= 6;
+  const size_t r_bst = (size_t)ndig * n_ext * (1u << logN);
   if (!fast) {
-    k_modup<<<row_grid(1u << logN, ndig, 128), 128, 0, st>>>(tabs, mc, xc, raised, alpha, n_ext, logN);
+    for (u32 b = 0; b < nb; ++b)
+      k_modup<<<row_grid(1u << logN, ndig, 128), 128, 0, st>>>(tabs, mc, xc + b * xc_bst, raised + b * r_bst, alpha,
+                                                                n_ext, logN);
     return cudaGetLastError();
   }
   // full digits share one launch; a partial last digit gets its own
@@ -620,29 +698,44 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
   cudaError_t e = cudaSuccess;
   if (nfull)
     e = dispatch_fbc_t((int)alpha, tabs, 1, mc, xc, (size_t)alpha * (1u << logN), raised,
-                       (size_t)n_ext * (1u << logN), logN, nfull, 0, htabs[0].nt, 0, st);
+                       (size_t)n_ext * (1u << logN), logN, nfull, 0, htabs[0].nt, 0, st, nb, xc_bst, r_bst);
   if (e) return e;
   if (nfull < ndig)
     e = dispatch_fbc_t((int)htabs[ndig - 1].ns, tabs, 1, mc, xc, (size_t)alpha * (1u << logN), raised,
-                       (size_t)n_ext * (1u << logN), logN, 1, nfull, htabs[ndig - 1].nt, 0, st);
+                       (size_t)n_ext * (1u << logN), logN, 1, nfull, htabs[ndig - 1].nt, 0, st, nb, xc_bst, r_bst);
   return e;
 }
 
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
-                            cudaStream_t st) {
-  k_ks_inner<<<row_grid((1u << logN) / 2, basis.nlimbs(), 256), 256, 0, st>>>(acc, x_eval, raised, key_b, key_a,
-                                                                              basis, alpha, ndig, logN, g, mc);
+                            cudaStream_t st, u32 nb, size_t x_bst) {
+  if (nb <= 1 || g_ks_batch <= 1) {
+    dim3 grid = row_grid((1u << logN) / 2, basis.nlimbs(), 256);
+    grid.z = nb;
+    k_ks_inner<1, 2><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,
+                                           nb ? nb : 1, x_bst);
+  } else if (nb == 2 || g_ks_batch == 2) {
+    dim3 grid = row_grid(1u << logN, basis.nlimbs(), 256);
+    grid.z = (nb + 1) / 2;
+    k_ks_inner<2, 1><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nb,
+                                           x_bst);
+  } else {
+    dim3 grid = row_grid(1u << logN, basis.nlimbs(), 256);
+    grid.z = (nb + 3) / 4;
+    k_ks_inner<4, 1><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nb,
+                                           x_bst);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,
                                    const u64* add1, u64 g_add, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
-                                   const u64* pinv_sh, const ModConsts* mc, cudaStream_t st) {
+                                   const u64* pinv_sh, const ModConsts* mc, cudaStream_t st, u32 nb,
+                                   size_t out_bst, size_t add_bst) {
   dim3 g = row_grid((1u << logN) / 2, nq, 256);
-  g.z = 2;
+  g.z = 2 * nb;
   k_moddown_combine<<<g, 256, 0, st>>>(out0, out1, acc, lift, add0, add1, g_add, nq, n_ext, logN, pinv, pinv_sh,
-                                       mc);
+                                       mc, out_bst, add_bst);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,7 @@ cudaError_t launch_ew_binary(int op, u64* out, const u64* a, const u64* b, Basis
 cudaError_t launch_ew_unary(int op, u64* out, const u64* a, Basis basis, u32 logN, u32 npolys,
                             const ModConsts* mc, const u64* consts, const u64* consts_sh, cudaStream_t st);
 cudaError_t launch_from_signed(u64* out, const long long* in, Basis basis, u32 logN, u32 npolys,
-                               const ModConsts* mc, cudaStream_t st);
+                               const ModConsts* mc, int mont, cudaStream_t st);
 cudaError_t launch_automorph(int eval_domain, u64* out, const u64* in, Basis basis, u32 logN, u32 npolys, u64 g,
                              const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_tensor(u64* d0, u64* d1, u64* d2, const u64* a, const u64* b, u32 nlimbs, u32 logN,
@@ -21,14 +21,21 @@ cudaError_t launch_tensor(u64* d0, u64* d1, u64* d2, const u64* a, const u64* b,
 cudaError_t launch_fbc(const FbcDev& T, const FbcDev* dT, const ModConsts* mc, const u64* in, size_t in_pst,
                        u64* out, size_t out_pst, u32 logN, u32 npolys, u32 nt, cudaStream_t st);
 // tabs: device array of per-digit tables; htabs: host copies of the same
+// batched over nb ciphertexts: xc [nb] entries xc_bst apart, raised [nb][ndig][n_ext]
 cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, const ModConsts* mc, const u64* xc,
-                         u64* raised, u32 alpha, u32 n_ext, u32 logN, cudaStream_t st);
+                         u64* raised, u32 alpha, u32 n_ext, u32 logN, cudaStream_t st, u32 nb = 1,
+                         size_t xc_bst = 0);
+// acc [nb][2][n_ext]; x_eval entries x_bst apart; one key load feeds up to
+// g_ks_batch (1, 2 or 4) entries (hcnn_set_option "ks_batch")
+extern int g_ks_batch;
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
-                            cudaStream_t st);
+                            cudaStream_t st, u32 nb = 1, size_t x_bst = 0);
+// acc [nb][2][n_ext], lift [nb][2][nq]; outputs / addends of entry b at +b*out_bst / +b*add_bst
 cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,
                                    const u64* add1, u64 g_add, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
-                                   const u64* pinv_sh, const ModConsts* mc, cudaStream_t st);
+                                   const u64* pinv_sh, const ModConsts* mc, cudaStream_t st, u32 nb = 1,
+                                   size_t out_bst = 0, size_t add_bst = 0);
 cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 npolys, const u64* qtop_mod,
                                 const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_rescale_combine(u64* out, const u64* in, u32 l, u32 logN, u32 npolys, const u64* inv,
@@ -50,6 +57,8 @@ struct ScalarMacArgs {
   u32 src_limbs[kSMacTerms];
   u64 w[kSMacTerms][kSMacLimbs];
   u64 wp[kSMacTerms][kSMacLimbs];
+  u64 add0[kSMacLimbs];  // per-limb constant added to every c0 (even poly index); has_add0
+  int has_add0;
 };
 cudaError_t launch_scalar_mac(const ScalarMacArgs& A, int nt, u64* out, u32 nl, u32 logN, u32 npolys,
                               int accumulate, const ModConsts* mc, cudaStream_t st);
@@ -59,8 +68,9 @@ struct MacTerms {
   const u64* ct[kMacMax];
   const u64* mask[kMacMax];
 };
+// nb > 1: ct[t] / out are batches of nb ciphertexts (2*nq*N apart) sharing the masks
 cudaError_t launch_mac_terms(const MacTerms& T, int nt, u64* out, u32 nq, u32 logN, int accumulate,
-                             const ModConsts* mc, cudaStream_t st);
+                             const ModConsts* mc, cudaStream_t st, u32 nb = 1);
 cudaError_t launch_gather_limb(u64* out, const u64* in, u32 limb, u32 nlimbs, u32 logN, u32 npolys,
                                cudaStream_t st);
 

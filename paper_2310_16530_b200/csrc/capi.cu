@@ -555,12 +555,15 @@ static int scalar_op(hcnn_ctx* c, int op, uint64_t* out, const uint64_t* a, cons
 }
 
 int hcnn_scalar_mac(hcnn_ctx* c, uint64_t* out, const uint64_t* const* srcs, const uint32_t* src_limbs,
-                    const uint64_t* consts, uint32_t nterms, uint32_t nq, uint32_t npolys, int accumulate, void* s) {
+                    const uint64_t* consts, uint32_t nterms, uint32_t nq, uint32_t npolys, int accumulate,
+                    const uint64_t* c0_add, void* s) {
   int rc = check_basis(c, nq, 0);
   if (rc) return rc;
   if (nq > (u32)kSMacLimbs) return fail(HCNN_E_BASIS, "too many limbs for scalar_mac");
+  if (nterms == 0 && accumulate && !c0_add) return HCNN_OK;
   ScalarMacArgs A;  // by value: capture-safe
-  for (u32 t0 = 0; t0 < nterms || (t0 == 0 && !accumulate); t0 += kSMacTerms) {
+  u32 t0 = 0;
+  do {
     const u32 nt = nterms - t0 < (u32)kSMacTerms ? nterms - t0 : (u32)kSMacTerms;
     for (u32 t = 0; t < nt; ++t) {
       if (src_limbs[t0 + t] < nq) return fail(HCNN_E_BASIS, "scalar_mac source has fewer limbs than the output");
@@ -572,20 +575,34 @@ int hcnn_scalar_mac(hcnn_ctx* c, uint64_t* out, const uint64_t* const* srcs, con
         A.wp[t][r] = h_shoup(A.w[t][r], q);
       }
     }
-    PK("scalar_mac", 8.0 * (nt + 1 + ((accumulate || t0) ? 1 : 0)) * nq * npolys * c->n, 1, STREAM(s),
-       launch_scalar_mac(A, (int)nt, out, nq, c->logN, npolys, accumulate || t0 > 0, c->d_mc, STREAM(s)));
-    if (nterms == 0) break;
-  }
+    A.has_add0 = (c0_add && t0 == 0) ? 1 : 0;  // the constant joins the first launch only
+    if (A.has_add0)
+      for (u32 r = 0; r < nq; ++r) A.add0[r] = c0_add[r] % c->mods[r];
+    const int acc = accumulate || t0 > 0;
+    PK("scalar_mac", 8.0 * (nt + 1 + (acc ? 1 : 0)) * nq * npolys * c->n, 1, STREAM(s),
+       launch_scalar_mac(A, (int)nt, out, nq, c->logN, npolys, acc, c->d_mc, STREAM(s)));
+    t0 += nt;
+  } while (t0 < nterms);
+  return HCNN_OK;
+}
+
+static int from_signed(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np, uint32_t npolys,
+                       int mont, void* s) {
+  int rc = check_basis(c, nq, np);
+  if (rc) return rc;
+  PK("from_signed", 8.0 * (nq + np + 1) * npolys * c->n, 1, STREAM(s),
+     launch_from_signed(out, (const long long*)in, c->basis(nq, np), c->logN, npolys, c->d_mc, mont, STREAM(s)));
   return HCNN_OK;
 }
 
 int hcnn_from_signed(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np, uint32_t npolys,
                      void* s) {
-  int rc = check_basis(c, nq, np);
-  if (rc) return rc;
-  PK("from_signed", 8.0 * (nq + np + 1) * npolys * c->n, 1, STREAM(s),
-     launch_from_signed(out, (const long long*)in, c->basis(nq, np), c->logN, npolys, c->d_mc, STREAM(s)));
-  return HCNN_OK;
+  return from_signed(c, out, in, nq, np, npolys, 0, s);
+}
+
+int hcnn_from_signed_mont(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np,
+                          uint32_t npolys, void* s) {
+  return from_signed(c, out, in, nq, np, npolys, 1, s);
 }
 
 int hcnn_automorphism(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint64_t g, int eval_domain, uint32_t nq,
@@ -641,14 +658,15 @@ int hcnn_base_convert(hcnn_ctx* c, uint64_t* out, const uint64_t* in, const uint
 struct KsWs {
   u64 *xc, *raised, *acc, *lift;
 };
-static KsWs ks_layout(const hcnn_ctx* c, u32 level, void* ws) {
+// batched layout: xc [nb][nq] | raised [nb][d][n_ext] | acc [nb][2][n_ext] | lift [nb][2][nq]
+static KsWs ks_layout(const hcnn_ctx* c, u32 level, void* ws, u32 nb = 1) {
   const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
   const size_t N = c->n;
   KsWs w;
   w.xc = (u64*)ws;
-  w.raised = w.xc + nq * N;
-  w.acc = w.raised + (size_t)nd * n_ext * N;
-  w.lift = w.acc + 2 * (size_t)n_ext * N;
+  w.raised = w.xc + (size_t)nb * nq * N;
+  w.acc = w.raised + (size_t)nb * nd * n_ext * N;
+  w.lift = w.acc + (size_t)nb * 2 * n_ext * N;
   return w;
 }
 
@@ -657,50 +675,69 @@ size_t hcnn_ks_workspace_bytes(const hcnn_ctx* c, uint32_t level) {
   return ((size_t)nq + (size_t)nd * n_ext + 2 * (size_t)n_ext + 2 * (size_t)nq) * c->n * 8;
 }
 
-// ModUp: iNTT a copy of x, convert every digit to Q_l||P, NTT the new limbs
-static int ks_modup(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, cudaStream_t st) {
+size_t hcnn_ks_workspace_bytes_batch(const hcnn_ctx* c, uint32_t level, uint32_t nb) {
+  return hcnn_ks_workspace_bytes(c, level) * (nb ? nb : 1);
+}
+
+// ModUp of nb polys (entry b at x_eval + b*x_bst): iNTT a copy, convert
+// every digit to Q_l||P, NTT the new limbs -- one launch per step for the batch
+static int ks_modup(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, cudaStream_t st, u32 nb = 1,
+                    size_t x_bst = 0) {
   const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
   const size_t N = c->n;
   ModupSet* mu;
   int rc = get_modup(c, level, &mu);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(w.xc, x_eval, nq * N * 8, cudaMemcpyDeviceToDevice, st));
+  if (nb == 1 || x_bst == nq * N)
+    CK(cudaMemcpyAsync(w.xc, x_eval, (size_t)nb * nq * N * 8, cudaMemcpyDeviceToDevice, st));
+  else
+    CK(cudaMemcpy2DAsync(w.xc, nq * N * 8, x_eval, x_bst * 8, nq * N * 8, nb, cudaMemcpyDeviceToDevice, st));
   LimbMap m{};
   m.base = w.xc;
   m.poly_stride = nq * N;
   m.basis = c->basis(nq, 0);
-  PK("ntt_inv", 16.0 * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), m, nq, 1, true, st));
-  PK("modup", 8.0 * (nq + (double)nd * (n_ext - c->alpha)) * N, 1, st, launch_modup(mu->d_tabs, mu->host.data(), nd, c->d_mc, w.xc, w.raised, c->alpha, n_ext, c->logN, st));
+  PK("ntt_inv", 16.0 * nb * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), m, nq, nb, true, st));
+  PK("modup", 8.0 * nb * (nq + (double)nd * (n_ext - c->alpha)) * N, 1, st,
+     launch_modup(mu->d_tabs, mu->host.data(), nd, c->d_mc, w.xc, w.raised, c->alpha, n_ext, c->logN, st, nb,
+                  nq * N));
   LimbMap r{};
   r.base = w.raised;
   r.poly_stride = (size_t)n_ext * N;
   r.basis = c->basis(nq, c->K);
   r.skip_alpha = c->alpha;
-  PK("ntt_fwd", 16.0 * ((double)nd * n_ext - nq) * N, ntt_nk(c), st, launch_ntt(c->tables(), r, n_ext, nd, false, st));
+  r.zmod = nd;
+  PK("ntt_fwd", 16.0 * nb * ((double)nd * n_ext - nq) * N, ntt_nk(c), st,
+     launch_ntt(c->tables(), r, n_ext, nd * nb, false, st));
   return HCNN_OK;
 }
 
-// inner product with one key (optionally Galois-permuted) + ModDown + combine
+// inner product with one key (optionally Galois-permuted) + ModDown + combine,
+// for nb entries: outputs / addends of entry b at +b*out_bst / +b*add_bst
 static int ks_finish(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, u64 g, const u64* kb,
                      const u64* ka, u64* out0, u64* out1, const u64* add0, const u64* add1, u64 g_add,
-                     cudaStream_t st) {
+                     cudaStream_t st, u32 nb = 1, size_t x_bst = 0, size_t out_bst = 0, size_t add_bst = 0) {
   const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
   const size_t N = c->n;
-  PK("ks_inner", 8.0 * ((double)nd * n_ext * 3 + 2 * n_ext) * N, 1, st, launch_ks_inner(w.acc, x_eval, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, g, c->d_mc, st));
+  PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, st,
+     launch_ks_inner(w.acc, x_eval, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, g, c->d_mc, st,
+                     nb, x_bst));
   LimbMap m{};
   m.base = w.acc + nq * N;
   m.poly_stride = (size_t)n_ext * N;
   m.basis = c->basis(nq, c->K);
   m.first_limb = nq;
-  PK("ntt_inv", 16.0 * 2 * c->K * N, ntt_nk(c), st, launch_ntt(c->tables(), m, c->K, 2, true, st));
-  PK("moddown_fbc", 8.0 * 2 * (c->K + nq) * N, 1, st, launch_fbc(c->moddown.dev, c->moddown.d_dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N, c->logN, 2, nq, st));
+  PK("ntt_inv", 16.0 * 2 * nb * c->K * N, ntt_nk(c), st, launch_ntt(c->tables(), m, c->K, 2 * nb, true, st));
+  PK("moddown_fbc", 8.0 * 2 * nb * (c->K + nq) * N, 1, st,
+     launch_fbc(c->moddown.dev, c->moddown.d_dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N,
+                c->logN, 2 * nb, nq, st));
   LimbMap l{};
   l.base = w.lift;
   l.poly_stride = nq * N;
   l.basis = c->basis(nq, 0);
-  PK("ntt_fwd", 16.0 * 2 * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), l, nq, 2, false, st));
-  PK("moddown_combine", 8.0 * 2 * (3 * nq + (add0 ? nq : 0)) * N, 1, st, launch_moddown_combine(out0, out1, w.acc, w.lift, add0, add1, g_add, nq, n_ext, c->logN, c->d_pinv,
-                            c->d_pinv_sh, c->d_mc, st));
+  PK("ntt_fwd", 16.0 * 2 * nb * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), l, nq, 2 * nb, false, st));
+  PK("moddown_combine", 8.0 * 2 * nb * (3 * nq + (add0 ? nq : 0)) * N, 1, st,
+     launch_moddown_combine(out0, out1, w.acc, w.lift, add0, add1, g_add, nq, n_ext, c->logN, c->d_pinv,
+                            c->d_pinv_sh, c->d_mc, st, nb, out_bst, add_bst));
   return HCNN_OK;
 }
 
@@ -721,47 +758,75 @@ int hcnn_keyswitch(hcnn_ctx* c, uint64_t* out0, uint64_t* out1, const uint64_t* 
   return ks_finish(c, level, x_eval, w, 1, kb, ka, out0, out1, nullptr, nullptr, 1, STREAM(s));
 }
 
-int hcnn_hmult(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t level,
-               const uint64_t* kb, const uint64_t* ka, void* ws, void* s) {
+int hcnn_hmult_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t level, uint32_t nb,
+                     const uint64_t* kb, const uint64_t* ka, void* ws, void* s) {
   int rc = check_level(c, level);
   if (rc) return rc;
+  if (nb == 0) return HCNN_OK;
   const u32 nq = level + 1;
-  const size_t N = c->n;
-  KsWs w = ks_layout(c, level, ws);
-  u64* d2 = w.lift;  // parked in the ModDown scratch until the inner product
-  PK("tensor", 8.0 * 7 * nq * N, 1, STREAM(s), launch_tensor(out, out + nq * N, d2, a, b, nq, c->logN, c->d_mc, STREAM(s)));
-  rc = ks_modup(c, level, d2, w, STREAM(s));
+  const size_t N = c->n, ct = 2 * (size_t)nq * N;
+  KsWs w = ks_layout(c, level, ws, nb);
+  // d2 of entry e parked in the first half of its ModDown scratch until the inner product
+  for (u32 e = 0; e < nb; ++e)
+    PK("tensor", 8.0 * 7 * nq * N, 1, STREAM(s),
+       launch_tensor(out + e * ct, out + e * ct + nq * N, w.lift + e * ct, a + e * ct, b + e * ct, nq, c->logN,
+                     c->d_mc, STREAM(s)));
+  rc = ks_modup(c, level, w.lift, w, STREAM(s), nb, ct);
   if (rc) return rc;
-  return ks_finish(c, level, d2, w, 1, kb, ka, out, out + nq * N, out, out + nq * N, 1, STREAM(s));
+  return ks_finish(c, level, w.lift, w, 1, kb, ka, out, out + nq * N, out, out + nq * N, 1, STREAM(s), nb, ct, ct,
+                   ct);
 }
 
-int hcnn_rotate_hoisted(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* ct, uint32_t level, uint32_t n_rot,
-                        const uint64_t* galois, const uint64_t* const* kbs, const uint64_t* const* kas, void* ws,
-                        void* s) {
+int hcnn_hmult(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t level,
+               const uint64_t* kb, const uint64_t* ka, void* ws, void* s) {
+  return hcnn_hmult_batch(c, out, a, b, level, 1, kb, ka, ws, s);
+}
+
+int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* cts, uint32_t level, uint32_t nb,
+                              uint32_t n_rot, const uint64_t* galois, const uint64_t* const* kbs,
+                              const uint64_t* const* kas, void* ws, void* s) {
   int rc = check_level(c, level);
   if (rc) return rc;
+  if (nb == 0) return HCNN_OK;
   const u32 nq = level + 1;
-  const size_t N = c->n;
-  KsWs w = ks_layout(c, level, ws);
-  const u64* c1 = ct + nq * N;
-  rc = ks_modup(c, level, c1, w, STREAM(s));
+  const size_t N = c->n, ct = 2 * (size_t)nq * N;
+  for (u32 i = 0; i < n_rot; ++i)
+    if ((galois[i] % (2ull * c->n) & 1) == 0) return fail(HCNN_E_PARAMETER, "galois element must be odd");
+  KsWs w = ks_layout(c, level, ws, nb);
+  const u64* c1 = cts + nq * N;
+  rc = ks_modup(c, level, c1, w, STREAM(s), nb, ct);
   if (rc) return rc;
   for (u32 i = 0; i < n_rot; ++i) {
     u64 g = galois[i] % (2ull * c->n);
-    if ((g & 1) == 0) return fail(HCNN_E_PARAMETER, "galois element must be odd");
-    rc = ks_finish(c, level, c1, w, g, kbs[i], kas[i], outs[i], outs[i] + nq * N, ct, nullptr, g, STREAM(s));
+    rc = ks_finish(c, level, c1, w, g, kbs[i], kas[i], outs[i], outs[i] + nq * N, cts, nullptr, g, STREAM(s), nb, ct,
+                   ct, ct);
     if (rc) return rc;
   }
   return HCNN_OK;
 }
 
+int hcnn_rotate_hoisted(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* ct, uint32_t level, uint32_t n_rot,
+                        const uint64_t* galois, const uint64_t* const* kbs, const uint64_t* const* kas, void* ws,
+                        void* s) {
+  return hcnn_rotate_hoisted_batch(c, outs, ct, level, 1, n_rot, galois, kbs, kas, ws, s);
+}
+
+int hcnn_mac_terms_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const uint64_t* const* masks,
+                         uint32_t n_terms, uint32_t level, uint32_t nb, int accumulate, void* s);
+
 int hcnn_mac_terms(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const uint64_t* const* masks,
                    uint32_t n_terms, uint32_t level, int accumulate, void* s) {
+  return hcnn_mac_terms_batch(c, out, cts, masks, n_terms, level, 1, accumulate, s);
+}
+
+int hcnn_mac_terms_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const uint64_t* const* masks,
+                         uint32_t n_terms, uint32_t level, uint32_t nb, int accumulate, void* s) {
   if (!c) return fail(HCNN_E_PARAMETER, "null context");
   if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
   const u32 nq = level + 1;
+  if (nb == 0) return HCNN_OK;
   if (n_terms == 0) {
-    if (!accumulate) CK(cudaMemsetAsync(out, 0, 2ull * nq * c->n * 8, STREAM(s)));
+    if (!accumulate) CK(cudaMemsetAsync(out, 0, 2ull * nb * nq * c->n * 8, STREAM(s)));
     return HCNN_OK;
   }
   for (u32 t0 = 0; t0 < n_terms; t0 += kMacMax) {
@@ -771,8 +836,8 @@ int hcnn_mac_terms(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const
       T.ct[t] = cts[t0 + t];
       T.mask[t] = masks[t0 + t];
     }
-    PK("mac_terms", 8.0 * (3.0 * nt + 2 + (accumulate || t0 ? 2 : 0)) * nq * c->n, 1, STREAM(s),
-       launch_mac_terms(T, (int)nt, out, nq, c->logN, accumulate || t0 > 0, c->d_mc, STREAM(s)));
+    PK("mac_terms", 8.0 * ((2.0 * nb + 1) * nt + nb * (2 + (accumulate || t0 ? 2 : 0))) * nq * c->n, 1, STREAM(s),
+       launch_mac_terms(T, (int)nt, out, nq, c->logN, accumulate || t0 > 0, c->d_mc, STREAM(s), nb));
   }
   return HCNN_OK;
 }
@@ -813,6 +878,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_hints") g_ntt_tuning.hints = (int)value;
   else if (k == "ntt_occupancy") g_ntt_tuning.occupancy = (int)value;
   else if (k == "ntt_split") g_ntt_tuning.split = (int)value;
+  else if (k == "ks_batch") g_ks_batch = (int)value;
   else return fail(HCNN_E_PARAMETER, "unknown option " + k);
   return HCNN_OK;
 }

@@ -15,6 +15,7 @@ struct LimbMap {
   u32 skip_alpha;
   u32 first_limb;     // basis position of the first processed limb
   u32 r0, z0;         // sub-batch offsets (limb / poly) added to blockIdx.y / blockIdx.z
+  u32 zmod;           // skip_alpha digit = z % zmod (batched ModUp: [nb][ndig] polys); 0 = z
 };
 
 // tuning knobs (hcnn_set_option): NTT sub-batch size in limbs (0 = one

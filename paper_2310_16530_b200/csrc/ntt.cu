@@ -21,6 +21,7 @@ namespace hcnn {
 __device__ __forceinline__ bool limb_skipped(const LimbMap& m, u32 r, u32 z) {
   if (m.skip_alpha == 0) return false;
   r += m.first_limb;
+  if (m.zmod) z %= m.zmod;
   u32 lo = z * m.skip_alpha;
   u32 hi = lo + m.skip_alpha;
   if (hi > m.basis.nq) hi = m.basis.nq;

@@ -159,12 +159,13 @@ class DeviceContext:
         self._chk(fn(self.handle, _ptr(out), _ptr(a), _native.u64_array(consts), nq, np_, npolys, _stream()))
         return out
 
-    def from_signed(self, rows: torch.Tensor, nq: int, np_: int = 0) -> torch.Tensor:
-        """int64 rows [npolys, N] -> residues [npolys, nlimbs, N]."""
+    def from_signed(self, rows: torch.Tensor, nq: int, np_: int = 0, mont: bool = False) -> torch.Tensor:
+        """int64 rows [npolys, N] -> residues [npolys, nlimbs, N] (Montgomery form if mont)."""
         rows = rows.contiguous()
         npolys = rows.numel() // self.n
         out = self.empty(npolys, nq + np_, self.n)
-        self._chk(self.lib.hcnn_from_signed(self.handle, _ptr(out), _ptr(rows), nq, np_, npolys, _stream()))
+        fn = self.lib.hcnn_from_signed_mont if mont else self.lib.hcnn_from_signed
+        self._chk(fn(self.handle, _ptr(out), _ptr(rows), nq, np_, npolys, _stream()))
         return out
 
     def automorphism(self, a: torch.Tensor, g: int, nq: int, np_: int = 0, eval_domain: bool = True,
@@ -187,8 +188,8 @@ class DeviceContext:
         return out
 
     # -- ckks.py level ops ----------------------------------------------------
-    def ks_workspace(self, level: int) -> torch.Tensor:
-        nbytes = int(self.lib.hcnn_ks_workspace_bytes(self.handle, level))
+    def ks_workspace(self, level: int, nb: int = 1) -> torch.Tensor:
+        nbytes = int(self.lib.hcnn_ks_workspace_bytes_batch(self.handle, level, nb))
         return self.empty(nbytes // 8)
 
     def keyswitch(self, x_eval: torch.Tensor, level: int, key_b: torch.Tensor, key_a: torch.Tensor):
@@ -198,69 +199,92 @@ class DeviceContext:
                                           _ptr(key_b), _ptr(key_a), _ptr(ws), _stream()))
         return out
 
+    def _batch(self, ct: torch.Tensor, level: int) -> int:
+        """entries of a ciphertext ([2,l+1,N]) or batch ([nb,2,l+1,N]) tensor"""
+        if not ct.is_contiguous() or ct.shape[-3:] != (2, level + 1, self.n) or ct.dim() not in (3, 4):
+            raise BasisError(f"expected a contiguous [(nb,) 2, {level + 1}, {self.n}] ciphertext tensor")
+        return 1 if ct.dim() == 3 else int(ct.shape[0])
+
     def hmult(self, a: torch.Tensor, b: torch.Tensor, level: int, key_b: torch.Tensor,
               key_a: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """tensor + relinearise one ciphertext or a batch ([nb,2,l+1,N]; one key)."""
+        nb = self._batch(a, level)
+        if b.shape != a.shape or not b.is_contiguous():
+            raise BasisError("hmult operands differ in shape")
         if out is None:
-            out = self.empty(2, level + 1, self.n)
-        ws = self.ks_workspace(level)
-        self._chk(self.lib.hcnn_hmult(self.handle, _ptr(out), _ptr(a), _ptr(b), level, _ptr(key_b),
-                                      _ptr(key_a), _ptr(ws), _stream()))
+            out = torch.empty_like(a)
+        ws = self.ks_workspace(level, nb)
+        self._chk(self.lib.hcnn_hmult_batch(self.handle, _ptr(out), _ptr(a), _ptr(b), level, nb, _ptr(key_b),
+                                            _ptr(key_a), _ptr(ws), _stream()))
         return out
 
     def rotate_hoisted(self, ct: torch.Tensor, level: int, galois: Sequence[int],
                        keys: Sequence[tuple[torch.Tensor, torch.Tensor]]) -> list[torch.Tensor]:
+        """rotations of one ciphertext or a batch sharing one ModUp; outs[i] has ct's shape."""
+        nb = self._batch(ct, level)
         n_rot = len(galois)
-        outs = [self.empty(2, level + 1, self.n) for _ in range(n_rot)]
+        outs = [torch.empty_like(ct) for _ in range(n_rot)]
         if n_rot == 0:
             return outs
-        ws = self.ks_workspace(level)
+        ws = self.ks_workspace(level, nb)
         P = ctypes.c_void_p * n_rot
         outs_p = P(*[o.data_ptr() for o in outs])
         kb = P(*[k[0].data_ptr() for k in keys])
         ka = P(*[k[1].data_ptr() for k in keys])
-        self._chk(self.lib.hcnn_rotate_hoisted(self.handle, outs_p, _ptr(ct), level, n_rot,
-                                               _native.u64_array(galois), kb, ka, _ptr(ws), _stream()))
+        self._chk(self.lib.hcnn_rotate_hoisted_batch(self.handle, outs_p, _ptr(ct), level, nb, n_rot,
+                                                     _native.u64_array(galois), kb, ka, _ptr(ws), _stream()))
         return outs
 
     def mac_terms(self, cts: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], level: int,
                   out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
-        """out (+)= sum_t cts[t] (.) masks[t] (Montgomery masks), one fused kernel."""
+        """out (+)= sum_t cts[t] (.) masks[t] (Montgomery masks), one fused kernel.
+        cts[t] may be batches [nb,2,l+1,N] sharing the masks."""
+        nb = self._batch(cts[0], level) if cts else (1 if out is None or out.dim() == 3 else out.shape[0])
         if out is None:
-            out = self.empty(2, level + 1, self.n)
+            out = self.empty(2, level + 1, self.n) if nb == 1 and (not cts or cts[0].dim() == 3) \
+                else self.empty(nb, 2, level + 1, self.n)
         n = len(cts)
+        for c in cts:
+            if c.shape != cts[0].shape or not c.is_contiguous():
+                raise BasisError("mac_terms ciphertexts differ in shape")
         P = ctypes.c_void_p * max(n, 1)
         cp = P(*[c.data_ptr() for c in cts])
         mp = P(*[m.data_ptr() for m in masks])
-        self._chk(self.lib.hcnn_mac_terms(self.handle, _ptr(out), cp, mp, n, level, 1 if accumulate else 0,
-                                          _stream()))
+        self._chk(self.lib.hcnn_mac_terms_batch(self.handle, _ptr(out), cp, mp, n, level, nb,
+                                                1 if accumulate else 0, _stream()))
         return out
 
     def scalar_mac(self, srcs: Sequence[torch.Tensor], consts: Sequence[Sequence[int]], level: int,
-                   out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+                   out: torch.Tensor | None = None, accumulate: bool = False, c0_add: int | None = None
+                   ) -> torch.Tensor:
         """out[2, level+1, N] (+)= sum_t consts[t][r] * srcs[t] per limb r;
         srcs[t] are contiguous [2, >=level+1, N] ciphertext tensors (a longer
-        one is read as its level-dropped prefix)."""
+        one is read as its level-dropped prefix).  c0_add: integer added to
+        every c0 (even poly) -- a plaintext constant in the same pass."""
         nq = level + 1
+        lead = tuple(srcs[0].shape[:-2]) if srcs else (tuple(out.shape[:-2]) if out is not None else (2,))
         if out is None:
-            out = self.empty(2, nq, self.n)
+            out = self.empty(*lead, nq, self.n)
         n = len(srcs)
         for s in srcs:
-            if not s.is_contiguous() or s.dim() != 3 or s.shape[0] != 2 or s.shape[1] < nq:
-                raise BasisError("scalar_mac sources must be contiguous [2, >=level+1, N]")
+            if not s.is_contiguous() or tuple(s.shape[:-2]) != lead or s.shape[-2] < nq:
+                raise BasisError("scalar_mac sources must be contiguous [..., >=level+1, N] of one shape")
         flat = [int(v) % self.q_list[r] for row in consts for r, v in enumerate(row[:nq])]
         if any(len(row) < nq for row in consts) or len(consts) != n:
             raise BasisError("scalar_mac needs one constant per limb per source")
         P = ctypes.c_void_p * max(n, 1)
         L = ctypes.c_uint32 * max(n, 1)
         sp = P(*[s.data_ptr() for s in srcs])
-        sl = L(*[s.shape[1] for s in srcs])
-        self._chk(self.lib.hcnn_scalar_mac(self.handle, _ptr(out), sp, sl, _native.u64_array(flat or [0]), n, nq, 2,
-                                           1 if accumulate else 0, _stream()))
+        npolys = int(np.prod(lead))
+        sl = L(*[s.shape[-2] for s in srcs])
+        add = None if c0_add is None else _native.u64_array([int(c0_add) % self.q_list[r] for r in range(nq)])
+        self._chk(self.lib.hcnn_scalar_mac(self.handle, _ptr(out), sp, sl, _native.u64_array(flat or [0]), n, nq,
+                                           npolys, 1 if accumulate else 0, add, _stream()))
         return out
 
     def rescale(self, a: torch.Tensor, level: int) -> torch.Tensor:
         npolys = self._npolys(a, level + 1, 0, self.n)
-        out = self.empty(npolys, level, self.n)
+        out = self.empty(*a.shape[:-2], level, self.n)
         ws = self.empty(npolys * self.n)
         self._chk(self.lib.hcnn_rescale(self.handle, _ptr(out), _ptr(a), level, npolys, _ptr(ws), _stream()))
         return out

@@ -59,6 +59,38 @@ def test_bootstrap_round_trip(boot12):
     assert np.max(np.abs(got2 - vals * vals)) < 2e-3
 
 
+def test_bootstrap_many_matches_single(boot12):
+    """The batched bootstrap (one pass over all members) is entry-wise
+    bit-identical to bootstrapping each ciphertext alone."""
+    import torch
+    from paper_2310_16530_b200 import ckks
+    params, cfg, b, ks = boot12
+    rng = np.random.default_rng(3)
+    cts = [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, 1), ks, rng) for _ in range(3)]
+    many = b.bootstrap_many(cts, ks)
+    for ct, m in zip(cts, many):
+        one = b.bootstrap(ct, ks)
+        assert m.level == one.level and m.scale == one.scale
+        assert torch.equal(m.data, one.data)
+
+
+def test_bootstrap_pairs_round_trip(boot12):
+    """Two half-periodic messages (even polynomials) share one bootstrap and
+    come back separated, each within the single-bootstrap precision."""
+    from paper_2310_16530_b200 import ckks
+    params, cfg, b, ks = boot12
+    rng = np.random.default_rng(4)
+    h = params.slots // 2
+    vals = [np.tile(rng.uniform(-1, 1, h), 2) for _ in range(4)]
+    cts = [ckks.encrypt(ckks.encode(v, params, 1), ks, rng) for v in vals]
+    outs = b.bootstrap_pairs([(cts[0], cts[1]), (cts[2], cts[3])], ks)
+    got = [o for pair in outs for o in pair]
+    for v, ct, o in zip(vals, cts, got):
+        assert o.level == b.output_level and abs(o.scale - ct.scale) < 1e-9 * ct.scale
+        err = float(np.max(np.abs(ckks.decode(ckks.decrypt(o, ks), params, imag_tol=None) - v)))
+        assert err < 1e-3, err
+
+
 def test_graph_refresh_slot_bootstraps():
     """Two stacked basic blocks need a refresh between them (6 levels each):
     the executor's refresh slot bootstraps (no decryption), and the result

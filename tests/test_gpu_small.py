@@ -161,3 +161,34 @@ def test_scalar_mac_exact(small, cts):
                          accumulate=True).cpu().numpy().astype(object)
     q0 = params.q_mods[0].q
     assert np.array_equal(acc[:, 0, :], (hs[0][:, 0, :] * (consts[0][0] % q0) + hs[1][:, 0, :] * (consts[1][0] % q0)) % q0)
+
+
+def test_batched_ops_match_single(small, cts):
+    """hmult / hoisted rotations / shared-mask MAC over a batch of
+    ciphertexts equal the single-ciphertext results entry by entry."""
+    import torch
+    from paper_2310_16530_b200 import ckks
+    params, ks = small
+    _, ct1, ct2 = cts
+    rng = np.random.default_rng(11)
+    more = [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, ct1.level), ks, rng)
+            for _ in range(4)]
+    A = ckks.stack([ct1, ct2] + more[:3])           # 5 entries: exercises the 4-wide kernels' tail
+    B = ckks.stack([ct2, ct1] + more[1:])
+    hm = ckks.unstack(ckks.hmult(A, B, ks))
+    for a, b, h in zip(ckks.unstack(A), ckks.unstack(B), hm):
+        assert torch.equal(h.data, ckks.hmult(a, b, ks).data)
+    rots = ckks.rotate_many(A, [1, 2, 4], ks)
+    for k, r in zip([1, 2, 4], rots):
+        for a, got in zip(ckks.unstack(A), ckks.unstack(r)):
+            assert torch.equal(got.data, ckks.rotate(a, k, ks).data)
+    ctx = params.ctx
+    masks = [ctx.unop("to_mont", ckks.encode(rng.uniform(-1, 1, params.slots), params, ct1.level).data,
+                      ct1.level + 1) for _ in range(3)]
+    outb = ctx.mac_terms([A.data, B.data, A.data], masks, ct1.level)
+    for i, (a, b) in enumerate(zip(ckks.unstack(A), ckks.unstack(B))):
+        assert torch.equal(outb[i], ctx.mac_terms([a.data, b.data, a.data], masks, ct1.level))
+    # a ciphertext-batch rescale is the per-entry rescale
+    rs = ckks.unstack(ckks.rescale(A, params))
+    for a, r in zip(ckks.unstack(A), rs):
+        assert torch.equal(r.data, ckks.rescale(a, params).data)

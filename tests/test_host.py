@@ -207,6 +207,26 @@ def test_format_b_stagger_table():
                 assert vec[16 + ((c - 1) % 4) * 4 + y * 2 + x] == v
 
 
+@pytest.mark.parametrize("variant,m,span,shape,slots", [
+    ("B", 4, 1024, (16, 32, 32), 32768), ("A", 4, 1024, (16, 32, 32), 32768), ("B", 4, 1024, (64, 8, 8), 32768),
+    ("B", 2, 16, (4, 4, 4), 64), ("A", 4, 16, (4, 4, 4), 64), ("B", 4, 16, (4, 4, 4), 64)])
+def test_slot_period_is_a_true_period(variant, m, span, shape, slots):
+    """packing.slot_period: every packed vector (and every mask built from
+    the layout) repeats with the reported period -- the premise of pairing
+    two ciphertexts per bootstrap."""
+    from paper_2310_16530_b200 import packing
+    fmt = packing.PackingFormat(variant, m, 1, span)
+    per = packing.slot_period(fmt, packing.TensorShape(*shape), slots)
+    t = np.random.default_rng(0).standard_normal(shape)
+    lay = packing.Layout(fmt, packing.TensorShape(*shape), slots)
+    for v in packing.pack(t, fmt, slots) + [lay.channel_values(0, np.arange(shape[0]) + 1.0)]:
+        assert np.array_equal(v, np.roll(v, per))
+    if per < slots:
+        assert slots % per == 0
+    if variant == "B" and slots // (m * span) >= 2 * m:
+        assert per * 2 <= slots
+
+
 def _exhaustive_refreshes(costs, max_level, target):
     n = len(costs)
     entry0 = min(max_level, sum(costs))
