@@ -71,6 +71,7 @@ def main(images: int = 2, use_graph: int = 1):
         "ms_per_bootstrap_by_point": [round(v, 2) for v in per_refresh],
         "layer_rows": [(r["name"], r["ms"]) for r in rep.per_layer],
         "mask_cache_entries": len(cache), "device_ms_profiled_image": round(dev_ms, 1), "kernels": kern,
+        "resident_mask_gb": round(packing.resident_bytes() / 2 ** 30, 1),
         "gpu_mem_gb": round(torch.cuda.max_memory_allocated() / 2 ** 30, 1)}), flush=True)
 
 
