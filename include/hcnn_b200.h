@@ -106,6 +106,12 @@ int hcnn_from_signed(hcnn_ctx* ctx, uint64_t* out, const int64_t* in, uint32_t n
  * the mask path's to_mont pass folded away (packing.py _mask_pt rows) */
 int hcnn_from_signed_mont(hcnn_ctx* ctx, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np,
                           uint32_t npolys, void* stream);
+/* forward NTT of signed int64 coefficient rows ([npolys][N], one row shared
+ * by all nq limbs) into out [npolys][nq][N], Montgomery form if mont:
+ * == hcnn_from_signed(_mont) + hcnn_ntt_forward, fused into the first NTT
+ * pass (compact-mask materialisation, packing.py _mask_pt rows) */
+int hcnn_ntt_from_signed(hcnn_ctx* ctx, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t npolys, int mont,
+                         void* stream);
 /* automorphism X -> X^g.  eval_domain=0: ring.automorphism ring.py:427-439
  * (coefficient domain, signed permutation); eval_domain=1: the equivalent
  * index permutation of the bit-reversed NTT output. */
@@ -148,6 +154,24 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* ctx, uint64_t* const* outs, const uint64
 int hcnn_mac_terms_batch(hcnn_ctx* ctx, uint64_t* out_cts, const uint64_t* const* cts,
                          const uint64_t* const* masks_mont, uint32_t n_terms, uint32_t level, uint32_t nb,
                          int accumulate, void* stream);
+
+/* ---- extended-basis (double-hoisted) linear transforms ---------------------
+ * Bootstrapping's baby-step/giant-step products keep rotations in Q_l||P
+ * (no ModDown per rotation): out = (P sigma_g(c0) + <d, key_b>, <d, key_a>)
+ * over nq + K limbs ([nb][2][nq+K][N] per rotation), MAC'd against masks
+ * encoded over Q_l||P, and brought back with one ModDown per sum.  No
+ * reference counterpart (the reference has no bootstrapping). */
+int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* ctx, uint64_t* const* outs_ext, const uint64_t* cts, uint32_t level,
+                                  uint32_t nb, uint32_t n_rot, const uint64_t* galois,
+                                  const uint64_t* const* keys_b, const uint64_t* const* keys_a, void* ws,
+                                  void* stream);
+int hcnn_mac_terms_ext_batch(hcnn_ctx* ctx, uint64_t* out_ext, const uint64_t* const* cts_ext,
+                             const uint64_t* const* masks_mont_ext, uint32_t n_terms, uint32_t level, uint32_t nb,
+                             int accumulate, void* stream);
+/* out [nb][2][nq][N] = ModDown(in_ext [nb][2][nq+K][N]); in_ext's P limbs are
+ * clobbered; ws: hcnn_ks_workspace_bytes_batch(level, nb) */
+int hcnn_moddown_batch(hcnn_ctx* ctx, uint64_t* out, uint64_t* in_ext, uint32_t level, uint32_t nb, void* ws,
+                       void* stream);
 
 /* rescale ckks.py:506-528 for npolys polys at `level` -> level-1 */
 size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* ctx, uint32_t npolys);

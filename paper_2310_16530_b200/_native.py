@@ -54,6 +54,7 @@ SIGNATURES = {
     "hcnn_scalar_mul": (_INT, [_VP, _VP, _VP, _PU64, _U32, _U32, _U32, _VP]),
     "hcnn_scalar_add": (_INT, [_VP, _VP, _VP, _PU64, _U32, _U32, _U32, _VP]),
     "hcnn_from_signed": (_INT, [_VP, _VP, _VP, _U32, _U32, _U32, _VP]),
+    "hcnn_ntt_from_signed": (_INT, [_VP, _VP, _VP, _U32, _U32, _INT, _VP]),
     "hcnn_from_signed_mont": (_INT, [_VP, _VP, _VP, _U32, _U32, _U32, _VP]),
     "hcnn_automorphism": (_INT, [_VP, _VP, _VP, _U64, _INT, _U32, _U32, _U32, _VP]),
     "hcnn_base_convert": (_INT, [_VP, _VP, _VP, _PU32, _U32, _PU32, _U32, _U32, _VP]),
@@ -68,6 +69,11 @@ SIGNATURES = {
                                          ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP, _VP]),
     "hcnn_mac_terms_batch": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _U32, _U32, _U32, _INT,
                                     _VP]),
+    "hcnn_rotate_hoisted_ext_batch": (_INT, [_VP, ctypes.POINTER(_VP), _VP, _U32, _U32, _U32, _PU64,
+                                             ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP, _VP]),
+    "hcnn_mac_terms_ext_batch": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _U32, _U32, _U32,
+                                        _INT, _VP]),
+    "hcnn_moddown_batch": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP, _VP]),
     "hcnn_rescale_workspace_bytes": (_SZ, [_VP, _U32]),
     "hcnn_rescale": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP, _VP]),
     "hcnn_scalar_mac": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_U32), _PU64, _U32, _U32, _U32, _INT,

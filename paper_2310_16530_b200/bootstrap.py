@@ -72,6 +72,11 @@ class BootConfig:
     degree: int = 59                          # Chebyshev degree before the double angles
     message_ratio_bits: int = 12              # q0 / scaled-up Delta ~ 2^bits
     secret_weight: int = 64
+    # baby steps per BSGS level matrix (None: ~sqrt of the diagonal span).
+    # Double hoisting makes babies cheap (no ModDown each) and giants dear
+    # (a ModUp each), so more babies / fewer giants wins.
+    bsgs_baby: int | None = 16
+    double_hoist: bool = True
 
     def evalmod_depth(self) -> int:
         return max(1, math.ceil(math.log2(self.degree))) + 1 + self.double_angle
@@ -168,7 +173,7 @@ class DiagPlan:
     giants: dict[int, list[tuple[int, np.ndarray]]]  # giant amount -> [(baby amount, pre-rotated diag)]
 
 
-def diag_plan(m: sp.csr_matrix) -> DiagPlan:
+def diag_plan(m: sp.csr_matrix, n1: int | None = None) -> DiagPlan:
     n = m.shape[0]
     coo = m.tocoo()
     keep = np.abs(coo.data) > 1e-300
@@ -185,7 +190,8 @@ def diag_plan(m: sp.csr_matrix) -> DiagPlan:
     stride = int(np.gcd.reduce(nz)) if nz else 1
     ks = {off: k // stride for off, k in signed.items()}
     span = max(ks.values()) - min(ks.values()) + 1
-    n1 = 1 << max(0, math.ceil(math.log2(math.sqrt(span))))
+    if n1 is None:
+        n1 = 1 << max(0, math.ceil(math.log2(math.sqrt(span))))
     giants: dict[int, list] = {}
     babies: set[int] = set()
     for off, k in ks.items():
@@ -427,8 +433,8 @@ class Bootstrapper:
         n = params.slots
         self.q0 = params.q_mods[0].q
         self.B = cfg.k_bound + 1
-        self.cts_plans = [diag_plan(m) for m in cts_groups(n, cfg.cts_stages, 1.0)]
-        self.stc_plans = [diag_plan(m) for m in stc_groups(n, cfg.stc_stages, 1.0)]
+        self.cts_plans = [diag_plan(m, cfg.bsgs_baby) for m in cts_groups(n, cfg.cts_stages, 1.0)]
+        self.stc_plans = [diag_plan(m, cfg.bsgs_baby) for m in stc_groups(n, cfg.stc_stages, 1.0)]
         self.cheb = evalmod_coeffs(cfg)
         self.output_level = params.max_level - cfg.depth()
         if self.output_level < 0:
@@ -437,6 +443,11 @@ class Bootstrapper:
         # EvalMod works at the scale of the first EvalMod level's prime
         self.eval_scale = float(params.q_mods[params.max_level - len(cfg.cts_stages)].q)
         self._masks: dict = {}
+        self.phase_hook = None  # optional callable(phase name) between pipeline phases (profiling)
+        pprod = 1
+        for m in params.p_mods:
+            pprod *= m.q
+        self._pmod_q = [pprod % m.q for m in params.q_mods]
 
     # -- keys ---------------------------------------------------------------
     def rotation_steps(self) -> set[int]:
@@ -465,8 +476,74 @@ class Bootstrapper:
             self._masks[key] = m
         return m
 
+    def _mask_ext(self, tag, values: np.ndarray, level: int, scale: float):
+        """diagonal encoded over Q_level || P, Montgomery evaluation rows"""
+        key = ("ext", tag, level, scale)
+        m = self._masks.get(key)
+        if m is None:
+            ctx = self.params.ctx
+            coeffs = ckks.encode_coeffs(values, self.params, level, scale)
+            rows = torch.from_numpy(np.ascontiguousarray(coeffs[None, :])).to(ctx.torch_device)
+            t = ctx.from_signed(rows, level + 1, ctx.K, mont=True)[0]
+            ctx.ntt(t, level + 1, ctx.K)
+            self._masks[key] = m = t
+        return m
+
+    def _lift_ext(self, ct: Ciphertext) -> torch.Tensor:
+        """(P c0, P c1) over Q_l || P (zero P limbs): the identity baby step"""
+        ctx = self.params.ctx
+        nq = ct.level + 1
+        pmod = [self._pmod_q[i] for i in range(nq)]
+        up = ctx.scalar_mul(ct.data, pmod, nq)
+        zeros = torch.zeros(*ct.data.shape[:-2], ctx.K, ct.n, dtype=up.dtype, device=up.device)
+        return torch.cat([up, zeros], dim=-2).contiguous()
+
+    def _apply_dh(self, ct: Ciphertext, plans: list[DiagPlan], ks: KeySet, tag,
+                  final_scale: float | None = None) -> Ciphertext:
+        """Double-hoisted BSGS: baby rotations stay in Q||P (one shared ModUp,
+        no ModDown), each giant group is MAC'd in Q||P, ModDown'd once and
+        rotated without ModDown into a Q||P accumulator; one final ModDown
+        per level matrix.  Same scale schedule as _apply."""
+        ctx = self.params.ctx
+        K = ctx.K
+        nlev = len(plans)
+        ratio = 1.0 if final_scale is None else (final_scale / ct.scale) ** (1.0 / nlev)
+        for li, p in enumerate(plans):
+            lvl = ct.level
+            if lvl < 1:
+                raise LevelError("linear transform ran out of levels")
+            nq = lvl + 1
+            q = self.params.q_mods[lvl].q
+            tgt = final_scale if (li == nlev - 1 and final_scale is not None) else ct.scale * ratio
+            s_d = tgt * q / ct.scale
+            babies = [b for b in p.babies if b]
+            keys = [(ks.gks[b].rows_b, ks.gks[b].rows_a) for b in babies]
+            ext = dict(zip(babies, ctx.rotate_hoisted_ext(ct.data, lvl, [ckks.galois_element(b, ct.n) for b in babies],
+                                                          keys)))
+            if 0 in p.babies:
+                ext[0] = self._lift_ext(ct)
+            acc = None
+            for gamt, terms in sorted(p.giants.items()):
+                cts = [ext[b] for b, _ in terms]
+                masks = [self._mask_ext((tag, li, gamt, b), pre, lvl, s_d) for b, pre in terms]
+                part = ctx.mac_terms_ext(cts, masks, lvl)
+                if gamt:
+                    inner = ctx.moddown(part, lvl)
+                    part = ctx.rotate_hoisted_ext(inner, lvl, [ckks.galois_element(gamt, ct.n)],
+                                                  [(ks.gks[gamt].rows_b, ks.gks[gamt].rows_a)])[0]
+                acc = part if acc is None else ctx.binop("add", acc, part, nq, K)
+            out = ctx.moddown(acc, lvl)
+            ct = ckks.rescale(Ciphertext(out, ct.scale * s_d, ct.n, ct.params), self.params)
+        return ct
+
     def _apply(self, ct: Ciphertext, plans: list[DiagPlan], ks: KeySet, tag,
                final_scale: float | None = None) -> Ciphertext:
+        if self.cfg.double_hoist and self.params.ctx.K:
+            return self._apply_dh(ct, plans, ks, tag, final_scale)
+        return self._apply_sh(ct, plans, ks, tag, final_scale)
+
+    def _apply_sh(self, ct: Ciphertext, plans: list[DiagPlan], ks: KeySet, tag,
+                  final_scale: float | None = None) -> Ciphertext:
         """Apply the level matrices.  The scale moves geometrically from the
         input scale to final_scale (None: keep) so every level's plaintext
         scale stays close to its prime -- the precision of the product."""
@@ -525,13 +602,18 @@ class Bootstrapper:
             raise KeyError_("bootstrapping needs the conjugation key (Bootstrapper.keygen)")
         out_scale = ct.scale if out_scale is None else out_scale
         ev = _Exact(params, ks)
+        hook = self.phase_hook or (lambda name: None)
+        hook("start")
         u, delta1 = self.coeff_to_slot(ct, ks)
+        hook("coeff_to_slot")
         uc = ckks.conjugate(u, ks)
         y_lo = ev.add(u, uc)                                                   # t_lo / (q0 B)
         y_hi = ckks.mul_monomial(ev.add(u, uc, sub=True), 3 * params.n // 2)  # -i * 2i Im u
         # both halves (of every batch entry) through one EvalMod pass
         both = torch.cat([y_lo.data, y_hi.data]) if u.batch is not None else torch.stack([y_lo.data, y_hi.data])
+        hook("conjugate_split")
         vb = self.eval_mod(Ciphertext(both, y_lo.scale, y_lo.n, y_lo.params), ks)
+        hook("eval_mod")
         h = vb.data.shape[0] // 2
         v_lo = Ciphertext(vb.data[:h] if u.batch is not None else vb.data[0], vb.scale, vb.n, vb.params)
         v_hi = Ciphertext(vb.data[h:] if u.batch is not None else vb.data[1], vb.scale, vb.n, vb.params)
@@ -541,6 +623,7 @@ class Bootstrapper:
         out = self._apply(v, self.stc_plans, ks, "stc", final_scale=out_scale)
         if out.level > self.output_level:
             out = ckks.mod_drop(out, self.output_level)
+        hook("slot_to_coeff")
         return out
 
     def bootstrap_many(self, cts: list[Ciphertext], ks: KeySet, max_batch: int = 16,

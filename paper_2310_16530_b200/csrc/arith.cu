@@ -389,7 +389,8 @@ __global__ void __launch_bounds__(256) k_ks_inner(u64* __restrict__ acc, const u
                                                   const u64* __restrict__ raised, const u64* __restrict__ key_b,
                                                   const u64* __restrict__ key_a, Basis basis, u32 alpha, u32 ndig,
                                                   u32 logN, u64 g, const ModConsts* __restrict__ mc, u32 nb,
-                                                  size_t x_bst) {
+                                                  size_t x_bst, const u64* __restrict__ c0, size_t c0_bst,
+                                                  const u64* __restrict__ pR) {
   // VEC adjacent coefficients x NB batch entries per thread (NB*VEC <= 4 keeps
   // the 128-bit accumulators at 16 registers pairs: full occupancy)
   const u32 N = 1u << logN, r = blockIdx.y;
@@ -446,6 +447,16 @@ __global__ void __launch_bounds__(256) k_ks_inner(u64* __restrict__ acc, const u
           mac128(bh[e][v], bl[e][v], x[v], kb[v], q);
           mac128(ah[e][v], al[e][v], x[v], ka[v], q);
         }
+      }
+    }
+    if (c0 && r < basis.nq) {  // extended-basis output: + P * sigma_g(c0) on the Q limbs
+      const u64 w = pR[r];
+#pragma unroll
+      for (int e = 0; e < NB; ++e) {
+        if ((u32)e >= ne) break;
+        const u64* src = c0 + (size_t)(b0 + e) * c0_bst + (size_t)r * N;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) mac128(bh[e][v], bl[e][v], src[g == 1 ? k + v : galois_src(k + v, g, logN)], w, q);
       }
     }
 #pragma unroll
@@ -510,44 +521,92 @@ __global__ void __launch_bounds__(256) k_moddown_combine(u64* __restrict__ out0,
 // with the reference's hadd(pmult_mont) chain since every partial result
 // is canonical).  accumulate: out += sum.
 // ---------------------------------------------------------------------------
-template <int NB>
+template <int NB, int VEC>
 __global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __restrict__ out, u32 nq, u32 logN,
-                                                   int accumulate, const ModConsts* __restrict__ mc, u32 nb) {
-  // blockIdx.z = 2 * chunk + poly; NB batch entries (ciphertexts 2*nq*N apart) share each mask load
-  const u32 N = 1u << logN, r = blockIdx.y, p = blockIdx.z & 1, b0 = (blockIdx.z >> 1) * NB;
-  const u64 q = mc[r].q, ninv = mc[r].ninv;
-  const size_t bst = 2 * (size_t)nq * N;
-  const size_t off = ((size_t)p * nq + r) * N + (size_t)b0 * bst, moff = (size_t)r * N;
-  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
-    u64 hi[NB], lo[NB];
+                                                   int accumulate, const ModConsts* __restrict__ mc, u32 nb, u32 nl,
+                                                   u32 Lq) {
+  // one thread: VEC adjacent coefficients of both polys of NB batch entries
+  // (ciphertexts 2*nl*N apart, nl = nq or nq + K limbs for Q||P); each mask
+  // load feeds all of them
+  const u32 N = 1u << logN, r = blockIdx.y, b0 = blockIdx.z * NB;
+  const u32 ne = nb - b0 < (u32)NB ? nb - b0 : (u32)NB;
+  const u32 mod = r < nq ? r : Lq + (r - nq);
+  const u64 q = mc[mod].q, ninv = mc[mod].ninv;
+  const size_t bst = 2 * (size_t)nl * N, pst = (size_t)nl * N;
+  const size_t off = (size_t)r * N + (size_t)b0 * bst, moff = (size_t)r * N;
+  for (u32 kv = blockIdx.x * blockDim.x + threadIdx.x; kv < N / VEC; kv += gridDim.x * blockDim.x) {
+    const u32 k = kv * VEC;
+    u64 hi[NB][2][VEC], lo[NB][2][VEC];
 #pragma unroll
-    for (int e = 0; e < NB; ++e) hi[e] = lo[e] = 0;
-#pragma unroll 4
+    for (int e = 0; e < NB; ++e)
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) hi[e][p][v] = lo[e][p][v] = 0;
+#pragma unroll 2
     for (int t = 0; t < nt; ++t) {
-      const u64 m = T.mask[t][moff + k];
+      u64 m[VEC];
+      if (VEC == 2) {
+        const ulonglong2 m2 = *reinterpret_cast<const ulonglong2*>(T.mask[t] + moff + k);
+        m[0] = m2.x;
+        m[VEC - 1] = m2.y;
+      } else {
+        m[0] = T.mask[t][moff + k];
+      }
 #pragma unroll
-      for (int e = 0; e < NB; ++e)
-        if (b0 + e < nb) mac128(hi[e], lo[e], T.ct[t][off + e * bst + k], m, q);
+      for (int e = 0; e < NB; ++e) {
+        if ((u32)e >= ne) break;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const u64* src = T.ct[t] + off + e * bst + p * pst + k;
+          u64 x[VEC];
+          if (VEC == 2) {
+            const ulonglong2 x2 = *reinterpret_cast<const ulonglong2*>(src);
+            x[0] = x2.x;
+            x[VEC - 1] = x2.y;
+          } else {
+            x[0] = *src;
+          }
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) mac128(hi[e][p][v], lo[e][p][v], x[v], m[v], q);
+        }
+      }
     }
 #pragma unroll
     for (int e = 0; e < NB; ++e) {
-      if (b0 + e >= nb) break;
-      u64 v = redc128(hi[e], lo[e], q, ninv);
-      if (accumulate) v = add_mod(v, out[off + e * bst + k], q);
-      out[off + e * bst + k] = v;
+      if ((u32)e >= ne) break;
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        u64* dst = out + off + e * bst + p * pst + k;
+        u64 y[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) y[v] = redc128(hi[e][p][v], lo[e][p][v], q, ninv);
+        if (VEC == 2) {
+          if (accumulate) {
+            const ulonglong2 o = *reinterpret_cast<const ulonglong2*>(dst);
+            y[0] = add_mod(y[0], o.x, q);
+            y[VEC - 1] = add_mod(y[VEC - 1], o.y, q);
+          }
+          *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(y[0], y[VEC - 1]);
+        } else {
+          if (accumulate) y[0] = add_mod(y[0], *dst, q);
+          *dst = y[0];
+        }
+      }
     }
   }
 }
 
 cudaError_t launch_mac_terms(const MacTerms& T, int nt, u64* out, u32 nq, u32 logN, int accumulate,
-                             const ModConsts* mc, cudaStream_t st, u32 nb) {
-  dim3 g = row_grid(1u << logN, nq, 256);
+                             const ModConsts* mc, cudaStream_t st, u32 nb, u32 np, u32 Lq) {
+  const u32 nl = nq + np;
   if (nb <= 1) {
-    g.z = 2;
-    k_mac_terms<1><<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc, 1);
+    dim3 g = row_grid((1u << logN) / 2, nl, 256);
+    k_mac_terms<1, 2><<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc, 1, nl, Lq);
   } else {
-    g.z = 2 * ((nb + 3) / 4);
-    k_mac_terms<4><<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc, nb);
+    dim3 g = row_grid(1u << logN, nl, 256);
+    g.z = (nb + 3) / 4;
+    k_mac_terms<4, 1><<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc, nb, nl, Lq);
   }
   return cudaGetLastError();
 }
@@ -708,22 +767,22 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
 
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
-                            cudaStream_t st, u32 nb, size_t x_bst) {
+                            cudaStream_t st, u32 nb, size_t x_bst, const u64* c0, size_t c0_bst, const u64* pR) {
   if (nb <= 1 || g_ks_batch <= 1) {
     dim3 grid = row_grid((1u << logN) / 2, basis.nlimbs(), 256);
     grid.z = nb;
     k_ks_inner<1, 2><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,
-                                           nb ? nb : 1, x_bst);
+                                           nb ? nb : 1, x_bst, c0, c0_bst, pR);
   } else if (nb == 2 || g_ks_batch == 2) {
     dim3 grid = row_grid(1u << logN, basis.nlimbs(), 256);
     grid.z = (nb + 1) / 2;
     k_ks_inner<2, 1><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nb,
-                                           x_bst);
+                                           x_bst, c0, c0_bst, pR);
   } else {
     dim3 grid = row_grid(1u << logN, basis.nlimbs(), 256);
     grid.z = (nb + 3) / 4;
     k_ks_inner<4, 1><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nb,
-                                           x_bst);
+                                           x_bst, c0, c0_bst, pR);
   }
   return cudaGetLastError();
 }

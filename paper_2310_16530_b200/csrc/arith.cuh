@@ -28,9 +28,12 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
 // acc [nb][2][n_ext]; x_eval entries x_bst apart; one key load feeds up to
 // g_ks_batch (1, 2 or 4) entries (hcnn_set_option "ks_batch")
 extern int g_ks_batch;
+// c0 (nullable): adds P * sigma_g(c0) on the Q limbs (pR[i] = P R mod q_i) --
+// the extended-basis (ModDown-free) rotation of double hoisting
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
-                            cudaStream_t st, u32 nb = 1, size_t x_bst = 0);
+                            cudaStream_t st, u32 nb = 1, size_t x_bst = 0, const u64* c0 = nullptr,
+                            size_t c0_bst = 0, const u64* pR = nullptr);
 // acc [nb][2][n_ext], lift [nb][2][nq]; outputs / addends of entry b at +b*out_bst / +b*add_bst
 cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,
                                    const u64* add1, u64 g_add, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
@@ -69,8 +72,9 @@ struct MacTerms {
   const u64* mask[kMacMax];
 };
 // nb > 1: ct[t] / out are batches of nb ciphertexts (2*nq*N apart) sharing the masks
+// np > 0: ciphertexts / masks over Q_l||P (nq + np limbs; P moduli at Lq..)
 cudaError_t launch_mac_terms(const MacTerms& T, int nt, u64* out, u32 nq, u32 logN, int accumulate,
-                             const ModConsts* mc, cudaStream_t st, u32 nb = 1);
+                             const ModConsts* mc, cudaStream_t st, u32 nb = 1, u32 np = 0, u32 Lq = 0);
 cudaError_t launch_gather_limb(u64* out, const u64* in, u32 limb, u32 nlimbs, u32 logN, u32 npolys,
                                cudaStream_t st);
 

@@ -54,6 +54,7 @@ struct hcnn_ctx {
   std::vector<unsigned char> small;  // q < 2^47
   FbcStore moddown;                  // P -> q_0..q_{Lq-1}
   u64 *d_pinv = nullptr, *d_pinv_sh = nullptr;  // P^-1 mod q_i
+  u64* d_pR = nullptr;                            // P R mod q_i (Montgomery form of P)
   u64 *d_rinv = nullptr, *d_rinv_sh = nullptr;  // [l][i] q_l^-1 mod q_i
   u64* d_qmod = nullptr;                         // [l][i] q_l mod q_i
   std::mutex mu;
@@ -393,13 +394,16 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
     }
     int rc = build_fbc(c, src, dst, pos, &c->moddown);
     if (rc) return rc;
-    std::vector<u64> pinv(n_q), pinv_sh(n_q);
+    std::vector<u64> pinv(n_q), pinv_sh(n_q), pR(n_q);
     for (u32 i = 0; i < n_q; ++i) {
       u64 qi = c->mods[i], prod = 1;
       for (u32 k = 0; k < n_p; ++k) prod = h_mulmod(prod, c->mods[n_q + k] % qi, qi);
       pinv[i] = h_invmod(prod, qi);
       pinv_sh[i] = h_shoup(pinv[i], qi);
+      pR[i] = h_to_mont(prod, qi);
     }
+    CK(cudaMalloc(&c->d_pR, n_q * 8));
+    CK(cudaMemcpy(c->d_pR, pR.data(), n_q * 8, cudaMemcpyHostToDevice));
     CK(cudaMalloc(&c->d_pinv, n_q * 8));
     CK(cudaMalloc(&c->d_pinv_sh, n_q * 8));
     CK(cudaMemcpy(c->d_pinv, pinv.data(), n_q * 8, cudaMemcpyHostToDevice));
@@ -421,6 +425,7 @@ void hcnn_ctx_destroy(hcnn_ctx* c) {
   cudaFree(c->d_ictw);
   cudaFree(c->d_pinv);
   cudaFree(c->d_pinv_sh);
+  cudaFree(c->d_pR);
   cudaFree(c->d_rinv);
   cudaFree(c->d_rinv_sh);
   cudaFree(c->d_qmod);
@@ -595,6 +600,31 @@ static int from_signed(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t n
   return HCNN_OK;
 }
 
+static int from_signed(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np, uint32_t npolys,
+                       int mont, void* s);
+
+int hcnn_ntt_from_signed(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t npolys, int mont,
+                         void* s) {
+  int rc = check_basis(c, nq, 0);
+  if (rc) return rc;
+  LimbMap m{};
+  m.base = out;
+  m.poly_stride = (size_t)nq * c->n;
+  m.basis = c->basis(nq, 0);
+  if (c->tables().ctw) {  // fused: the column pass reduces the int64 rows on load
+    m.sin = (const long long*)in;
+    m.smont = mont;
+    PK("ntt_fwd_signed", 8.0 * (1 + 2 * (double)nq) * npolys * c->n, ntt_nk(c), STREAM(s),
+       launch_ntt(c->tables(), m, nq, npolys, false, STREAM(s)));
+    return HCNN_OK;
+  }
+  rc = from_signed(c, out, in, nq, 0, npolys, mont, s);
+  if (rc) return rc;
+  PK("ntt_fwd_signed", 16.0 * nq * npolys * c->n, ntt_nk(c), STREAM(s),
+     launch_ntt(c->tables(), m, nq, npolys, false, STREAM(s)));
+  return HCNN_OK;
+}
+
 int hcnn_from_signed(hcnn_ctx* c, uint64_t* out, const int64_t* in, uint32_t nq, uint32_t np, uint32_t npolys,
                      void* s) {
   return from_signed(c, out, in, nq, np, npolys, 0, s);
@@ -696,7 +726,7 @@ static int ks_modup(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, cu
   m.base = w.xc;
   m.poly_stride = nq * N;
   m.basis = c->basis(nq, 0);
-  PK("ntt_inv", 16.0 * nb * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), m, nq, nb, true, st));
+  PK("ntt_inv_modup", 16.0 * nb * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), m, nq, nb, true, st));
   PK("modup", 8.0 * nb * (nq + (double)nd * (n_ext - c->alpha)) * N, 1, st,
      launch_modup(mu->d_tabs, mu->host.data(), nd, c->d_mc, w.xc, w.raised, c->alpha, n_ext, c->logN, st, nb,
                   nq * N));
@@ -706,8 +736,34 @@ static int ks_modup(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, cu
   r.basis = c->basis(nq, c->K);
   r.skip_alpha = c->alpha;
   r.zmod = nd;
-  PK("ntt_fwd", 16.0 * nb * ((double)nd * n_ext - nq) * N, ntt_nk(c), st,
+  PK("ntt_fwd_modup", 16.0 * nb * ((double)nd * n_ext - nq) * N, ntt_nk(c), st,
      launch_ntt(c->tables(), r, n_ext, nd * nb, false, st));
+  return HCNN_OK;
+}
+
+// ModDown of nb extended-basis ciphertexts acc [nb][2][n_ext] (P limbs are
+// clobbered by the in-place iNTT) + combine: out = (acc_Q - lift) P^-1 (+ add)
+static int ks_moddown(hcnn_ctx* c, u32 level, u64* acc, u64* lift, u64* out0, u64* out1, const u64* add0,
+                      const u64* add1, u64 g_add, cudaStream_t st, u32 nb, size_t out_bst, size_t add_bst) {
+  const u32 nq = level + 1, n_ext = nq + c->K;
+  const size_t N = c->n;
+  LimbMap m{};
+  m.base = acc + nq * N;
+  m.poly_stride = (size_t)n_ext * N;
+  m.basis = c->basis(nq, c->K);
+  m.first_limb = nq;
+  PK("ntt_inv_moddown", 16.0 * 2 * nb * c->K * N, ntt_nk(c), st, launch_ntt(c->tables(), m, c->K, 2 * nb, true, st));
+  PK("moddown_fbc", 8.0 * 2 * nb * (c->K + nq) * N, 1, st,
+     launch_fbc(c->moddown.dev, c->moddown.d_dev, c->d_mc, acc + nq * N, (size_t)n_ext * N, lift, nq * N,
+                c->logN, 2 * nb, nq, st));
+  LimbMap l{};
+  l.base = lift;
+  l.poly_stride = nq * N;
+  l.basis = c->basis(nq, 0);
+  PK("ntt_fwd_moddown", 16.0 * 2 * nb * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), l, nq, 2 * nb, false, st));
+  PK("moddown_combine", 8.0 * 2 * nb * (3 * nq + (add0 ? nq : 0)) * N, 1, st,
+     launch_moddown_combine(out0, out1, acc, lift, add0, add1, g_add, nq, n_ext, c->logN, c->d_pinv,
+                            c->d_pinv_sh, c->d_mc, st, nb, out_bst, add_bst));
   return HCNN_OK;
 }
 
@@ -721,24 +777,7 @@ static int ks_finish(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, u
   PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, st,
      launch_ks_inner(w.acc, x_eval, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, g, c->d_mc, st,
                      nb, x_bst));
-  LimbMap m{};
-  m.base = w.acc + nq * N;
-  m.poly_stride = (size_t)n_ext * N;
-  m.basis = c->basis(nq, c->K);
-  m.first_limb = nq;
-  PK("ntt_inv", 16.0 * 2 * nb * c->K * N, ntt_nk(c), st, launch_ntt(c->tables(), m, c->K, 2 * nb, true, st));
-  PK("moddown_fbc", 8.0 * 2 * nb * (c->K + nq) * N, 1, st,
-     launch_fbc(c->moddown.dev, c->moddown.d_dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N,
-                c->logN, 2 * nb, nq, st));
-  LimbMap l{};
-  l.base = w.lift;
-  l.poly_stride = nq * N;
-  l.basis = c->basis(nq, 0);
-  PK("ntt_fwd", 16.0 * 2 * nb * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), l, nq, 2 * nb, false, st));
-  PK("moddown_combine", 8.0 * 2 * nb * (3 * nq + (add0 ? nq : 0)) * N, 1, st,
-     launch_moddown_combine(out0, out1, w.acc, w.lift, add0, add1, g_add, nq, n_ext, c->logN, c->d_pinv,
-                            c->d_pinv_sh, c->d_mc, st, nb, out_bst, add_bst));
-  return HCNN_OK;
+  return ks_moddown(c, level, w.acc, w.lift, out0, out1, add0, add1, g_add, st, nb, out_bst, add_bst);
 }
 
 static int check_level(const hcnn_ctx* c, u32 level) {
@@ -805,6 +844,39 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
   return HCNN_OK;
 }
 
+int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* cts, uint32_t level,
+                                  uint32_t nb, uint32_t n_rot, const uint64_t* galois, const uint64_t* const* kbs,
+                                  const uint64_t* const* kas, void* ws, void* s) {
+  int rc = check_level(c, level);
+  if (rc) return rc;
+  if (nb == 0) return HCNN_OK;
+  const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
+  const size_t N = c->n, ct = 2 * (size_t)nq * N;
+  for (u32 i = 0; i < n_rot; ++i)
+    if ((galois[i] % (2ull * c->n) & 1) == 0) return fail(HCNN_E_PARAMETER, "galois element must be odd");
+  KsWs w = ks_layout(c, level, ws, nb);
+  const u64* c1 = cts + nq * N;
+  rc = ks_modup(c, level, c1, w, STREAM(s), nb, ct);
+  if (rc) return rc;
+  for (u32 i = 0; i < n_rot; ++i) {
+    const u64 g = galois[i] % (2ull * c->n);
+    PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext + nb * nq) * N, 1, STREAM(s),
+       launch_ks_inner(outs[i], c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd, c->logN, g,
+                       c->d_mc, STREAM(s), nb, ct, cts, ct, c->d_pR));
+  }
+  return HCNN_OK;
+}
+
+int hcnn_moddown_batch(hcnn_ctx* c, uint64_t* out, uint64_t* in_ext, uint32_t level, uint32_t nb, void* ws, void* s) {
+  int rc = check_level(c, level);
+  if (rc) return rc;
+  if (nb == 0) return HCNN_OK;
+  const u32 nq = level + 1;
+  const size_t N = c->n, ct = 2 * (size_t)nq * N;
+  KsWs w = ks_layout(c, level, ws, nb);
+  return ks_moddown(c, level, in_ext, w.lift, out, out + nq * N, nullptr, nullptr, 1, STREAM(s), nb, ct, 0);
+}
+
 int hcnn_rotate_hoisted(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* ct, uint32_t level, uint32_t n_rot,
                         const uint64_t* galois, const uint64_t* const* kbs, const uint64_t* const* kas, void* ws,
                         void* s) {
@@ -819,14 +891,28 @@ int hcnn_mac_terms(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const
   return hcnn_mac_terms_batch(c, out, cts, masks, n_terms, level, 1, accumulate, s);
 }
 
+static int mac_terms_impl(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const uint64_t* const* masks,
+                          uint32_t n_terms, uint32_t level, uint32_t nb, uint32_t np, int accumulate, void* s);
+
 int hcnn_mac_terms_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const uint64_t* const* masks,
                          uint32_t n_terms, uint32_t level, uint32_t nb, int accumulate, void* s) {
+  return mac_terms_impl(c, out, cts, masks, n_terms, level, nb, 0, accumulate, s);
+}
+
+int hcnn_mac_terms_ext_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const uint64_t* const* masks,
+                             uint32_t n_terms, uint32_t level, uint32_t nb, int accumulate, void* s) {
+  if (c && c->K == 0) return fail(HCNN_E_KEY, "no special primes");
+  return mac_terms_impl(c, out, cts, masks, n_terms, level, nb, c ? c->K : 0, accumulate, s);
+}
+
+static int mac_terms_impl(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const uint64_t* const* masks,
+                          uint32_t n_terms, uint32_t level, uint32_t nb, uint32_t np, int accumulate, void* s) {
   if (!c) return fail(HCNN_E_PARAMETER, "null context");
   if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
   const u32 nq = level + 1;
   if (nb == 0) return HCNN_OK;
   if (n_terms == 0) {
-    if (!accumulate) CK(cudaMemsetAsync(out, 0, 2ull * nb * nq * c->n * 8, STREAM(s)));
+    if (!accumulate) CK(cudaMemsetAsync(out, 0, 2ull * nb * (nq + np) * c->n * 8, STREAM(s)));
     return HCNN_OK;
   }
   for (u32 t0 = 0; t0 < n_terms; t0 += kMacMax) {
@@ -836,8 +922,9 @@ int hcnn_mac_terms_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts,
       T.ct[t] = cts[t0 + t];
       T.mask[t] = masks[t0 + t];
     }
-    PK("mac_terms", 8.0 * ((2.0 * nb + 1) * nt + nb * (2 + (accumulate || t0 ? 2 : 0))) * nq * c->n, 1, STREAM(s),
-       launch_mac_terms(T, (int)nt, out, nq, c->logN, accumulate || t0 > 0, c->d_mc, STREAM(s), nb));
+    PK("mac_terms", 8.0 * ((2.0 * nb + 1) * nt + nb * (2 + (accumulate || t0 ? 2 : 0))) * (nq + np) * c->n, 1,
+       STREAM(s), launch_mac_terms(T, (int)nt, out, nq, c->logN, accumulate || t0 > 0, c->d_mc, STREAM(s), nb, np,
+                                   c->Lq));
   }
   return HCNN_OK;
 }
@@ -857,13 +944,13 @@ int hcnn_rescale(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint32_t level,
   m.poly_stride = c->n;
   m.basis = c->basis(l + 1, 0);
   m.first_limb = l;
-  PK("ntt_inv", 16.0 * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), m, 1, npolys, true, STREAM(s)));
+  PK("ntt_inv_rescale", 16.0 * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), m, 1, npolys, true, STREAM(s)));
   PK("rescale_lift", 8.0 * (l + 1) * npolys * c->n, 1, STREAM(s), launch_rescale_lift(out, top, l, c->logN, npolys, c->d_qmod + (size_t)l * c->Lq, c->d_mc, STREAM(s)));
   LimbMap o{};
   o.base = out;
   o.poly_stride = (size_t)l * c->n;
   o.basis = c->basis(l, 0);
-  PK("ntt_fwd", 16.0 * l * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), o, l, npolys, false, STREAM(s)));
+  PK("ntt_fwd_rescale", 16.0 * l * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), o, l, npolys, false, STREAM(s)));
   PK("rescale_combine", 24.0 * l * npolys * c->n, 1, STREAM(s), launch_rescale_combine(out, in, l, c->logN, npolys, c->d_rinv + (size_t)l * c->Lq,
                             c->d_rinv_sh + (size_t)l * c->Lq, c->d_mc, STREAM(s)));
   return HCNN_OK;

@@ -16,6 +16,11 @@ struct LimbMap {
   u32 first_limb;     // basis position of the first processed limb
   u32 r0, z0;         // sub-batch offsets (limb / poly) added to blockIdx.y / blockIdx.z
   u32 zmod;           // skip_alpha digit = z % zmod (batched ModUp: [nb][ndig] polys); 0 = z
+  // forward NTT only: read signed int64 coefficients (one row of N per poly,
+  // shared by every limb) and reduce them on load instead of reading base;
+  // smont: Montgomery form (v R mod q).  Fuses from_signed into the NTT.
+  const long long* sin;
+  int smont;
 };
 
 // tuning knobs (hcnn_set_option): NTT sub-batch size in limbs (0 = one

@@ -210,8 +210,20 @@ __global__ void __launch_bounds__(256, MINB) ntt2_fwd_cols(LimbMap map, const Mo
   const int tid = threadIdx.x, c = tid % COLS, j = tid / COLS;
   for (int i = tid; i < N1; i += 256) sw[i] = make_ulonglong2(tw[(size_t)mod * N + i], twp[(size_t)mod * N + i]);
   u64 x[16];
+  if (map.sin) {
+    const long long* s = map.sin + (size_t)z * N + blockIdx.x * COLS;
+    const u64 kr = map.smont ? mc[mod].r2 : mc[mod].one_m, ninv = mc[mod].ninv;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) x[k] = ld_last<HINT>(&a[(size_t)(j + T1 * k) * N2 + c]);
+    for (int k = 0; k < 16; ++k) {
+      const long long v = s[(size_t)(j + T1 * k) * N2 + c];
+      const u64 mag = v >= 0 ? (u64)v : (u64)(-(v + 1)) + 1ull;
+      const u64 red = mont_mul(mag, kr, q, ninv);
+      x[k] = v >= 0 ? red : neg_mod(red, q);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = ld_last<HINT>(&a[(size_t)(j + T1 * k) * N2 + c]);
+  }
   __syncthreads();
   const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
   auto twA = [&](int d, int b) { return sw[(1 << d) + b]; };

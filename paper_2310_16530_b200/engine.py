@@ -168,6 +168,15 @@ class DeviceContext:
         self._chk(fn(self.handle, _ptr(out), _ptr(rows), nq, np_, npolys, _stream()))
         return out
 
+    def ntt_from_signed(self, rows: torch.Tensor, nq: int, mont: bool = False) -> torch.Tensor:
+        """int64 rows [npolys, N] -> evaluation residues [npolys, nq, N] (Montgomery if mont), one fused pass."""
+        rows = rows.contiguous()
+        npolys = rows.numel() // self.n
+        out = self.empty(npolys, nq, self.n)
+        self._chk(self.lib.hcnn_ntt_from_signed(self.handle, _ptr(out), _ptr(rows), nq, npolys, 1 if mont else 0,
+                                                _stream()))
+        return out
+
     def automorphism(self, a: torch.Tensor, g: int, nq: int, np_: int = 0, eval_domain: bool = True,
                      out: torch.Tensor | None = None) -> torch.Tensor:
         npolys = self._npolys(a, nq, np_, self.n)
@@ -234,6 +243,49 @@ class DeviceContext:
         self._chk(self.lib.hcnn_rotate_hoisted_batch(self.handle, outs_p, _ptr(ct), level, nb, n_rot,
                                                      _native.u64_array(galois), kb, ka, _ptr(ws), _stream()))
         return outs
+
+    # -- extended basis Q_l||P (double-hoisted linear transforms) --------------
+    def rotate_hoisted_ext(self, ct: torch.Tensor, level: int, galois: Sequence[int],
+                           keys: Sequence[tuple[torch.Tensor, torch.Tensor]]) -> list[torch.Tensor]:
+        """rotations kept in Q_l||P (no ModDown): outs[i] [(nb,) 2, l+1+K, N]."""
+        nb = self._batch(ct, level)
+        shape = tuple(ct.shape[:-2]) + (level + 1 + self.K, self.n)
+        outs = [self.empty(*shape) for _ in galois]
+        if not outs:
+            return outs
+        ws = self.ks_workspace(level, nb)
+        P = ctypes.c_void_p * len(outs)
+        self._chk(self.lib.hcnn_rotate_hoisted_ext_batch(
+            self.handle, P(*[o.data_ptr() for o in outs]), _ptr(ct), level, nb, len(outs),
+            _native.u64_array(galois), P(*[k[0].data_ptr() for k in keys]), P(*[k[1].data_ptr() for k in keys]),
+            _ptr(ws), _stream()))
+        return outs
+
+    def mac_terms_ext(self, cts: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], level: int,
+                      out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+        """mac_terms over Q_l||P ciphertexts and masks (nq + K limbs)."""
+        nl = level + 1 + self.K
+        for c in cts:
+            if not c.is_contiguous() or c.shape != cts[0].shape or c.shape[-2:] != (nl, self.n):
+                raise BasisError("mac_terms_ext operands must be contiguous [(nb,) 2, l+1+K, N]")
+        nb = 1 if cts[0].dim() == 3 else int(cts[0].shape[0])
+        if out is None:
+            out = self.empty(*cts[0].shape)
+        P = ctypes.c_void_p * max(len(cts), 1)
+        self._chk(self.lib.hcnn_mac_terms_ext_batch(self.handle, _ptr(out), P(*[c.data_ptr() for c in cts]),
+                                                    P(*[m.data_ptr() for m in masks]), len(cts), level, nb,
+                                                    1 if accumulate else 0, _stream()))
+        return out
+
+    def moddown(self, ext: torch.Tensor, level: int) -> torch.Tensor:
+        """Q_l||P ciphertext(s) -> Q_l (ext's P limbs are clobbered)."""
+        if not ext.is_contiguous() or ext.shape[-2:] != (level + 1 + self.K, self.n):
+            raise BasisError("moddown expects a contiguous [(nb,) 2, l+1+K, N] tensor")
+        nb = 1 if ext.dim() == 3 else int(ext.shape[0])
+        out = self.empty(*ext.shape[:-2], level + 1, self.n)
+        ws = self.ks_workspace(level, nb)
+        self._chk(self.lib.hcnn_moddown_batch(self.handle, _ptr(out), _ptr(ext), level, nb, _ptr(ws), _stream()))
+        return out
 
     def mac_terms(self, cts: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], level: int,
                   out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:

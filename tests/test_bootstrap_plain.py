@@ -120,3 +120,15 @@ def test_cheb_divide_identity():
         tm = np.polynomial.chebyshev.chebval(y, np.eye(m + 1)[m])
         ch = np.polynomial.chebyshev.chebval
         assert np.allclose(ch(y, r) + tm * ch(y, q), ch(y, c), atol=1e-12)
+
+
+@pytest.mark.parametrize("n1", [4, 16, 32])
+def test_diag_plan_any_baby_count(n1):
+    """BSGS plans with a forced baby count apply the same matrix."""
+    n = 256
+    rng = np.random.default_rng(n1)
+    v = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    for m in bt.cts_groups(n, (4, 4), 1.0):
+        p = bt.diag_plan(m, n1)
+        assert p.n1 == n1
+        assert np.allclose(bt.apply_plain([p], v), m @ v)

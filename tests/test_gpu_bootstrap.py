@@ -59,6 +59,26 @@ def test_bootstrap_round_trip(boot12):
     assert np.max(np.abs(got2 - vals * vals)) < 2e-3
 
 
+def test_double_hoisted_matches_single_hoisted():
+    """The double-hoisted linear transforms (Q||P babies and accumulator, one
+    ModDown per giant) decrypt to the single-hoisted result."""
+    from paper_2310_16530_b200 import bootstrap as bt, ckks
+    outs = []
+    for dh in (False, True):
+        rng = np.random.default_rng(5)  # same keys, same ciphertext for both
+        cfg = bt.BootConfig(cts_stages=(4, 4, 3), stc_stages=(3, 4, 4), double_hoist=dh)
+        params = bt.boot_params("boot12", 1 << 12, 4, cfg)
+        b = bt.Bootstrapper(params, cfg)
+        ks = b.keygen(np.random.default_rng(7), rotations=[1])
+        vals = np.random.default_rng(9).uniform(-1, 1, params.slots)
+        ct = ckks.encrypt(ckks.encode(vals, params, 2), ks, rng)
+        u, _ = b.coeff_to_slot(ct, ks)
+        outs.append(ckks.decode(ckks.decrypt(u, ks), params, imag_tol=None))
+        got = ckks.decode(ckks.decrypt(b.bootstrap(ct, ks), ks), params, imag_tol=None)
+        assert np.max(np.abs(got - vals)) < 1e-3
+    assert np.max(np.abs(outs[0] - outs[1])) < 1e-6
+
+
 def test_bootstrap_many_matches_single(boot12):
     """The batched bootstrap (one pass over all members) is entry-wise
     bit-identical to bootstrapping each ciphertext alone."""

@@ -83,3 +83,28 @@ def test_gate1_schoolbook(n):
         for li, m in enumerate(mods):
             want = _schoolbook([v % m.q for v in a], [v % m.q for v in b], m.q)
             assert got[li].tolist() == want
+
+
+@pytest.mark.parametrize("logn", [8, 12, 16])
+@pytest.mark.parametrize("mont", [False, True])
+def test_ntt_from_signed_fused(logn, mont):
+    """The fused signed-load forward NTT equals from_signed (+ Montgomery
+    lift) followed by the forward NTT, bit for bit, and the oracle."""
+    import torch
+    from oracle import ckks_oracle as O
+    from paper_2310_16530_b200.engine import context_for, to_host_u64
+    n = 1 << logn
+    qs = _mods(n)
+    ctx = context_for(n, qs)
+    rng = np.random.default_rng(logn + 3)
+    rows = rng.integers(-(1 << 62), 1 << 62, size=(5, n), dtype=np.int64)
+    rows[0, :4] = [-(1 << 63), (1 << 63) - 1, 0, -1]
+    dev = torch.from_numpy(rows).cuda()
+    fused = ctx.ntt_from_signed(dev, len(qs), mont=mont)
+    ref = ctx.from_signed(dev, len(qs), mont=mont)
+    ctx.ntt(ref, len(qs))
+    assert torch.equal(fused, ref)
+    if not mont:
+        want = np.stack([O.ntt(np.stack([(rows[p].astype(object) % q).astype(np.uint64) for q in qs]), qs)
+                         for p in range(5)])
+        assert np.array_equal(to_host_u64(fused), want)
