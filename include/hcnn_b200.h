@@ -138,6 +138,16 @@ int hcnn_hmult(hcnn_ctx* ctx, uint64_t* out_ct, const uint64_t* a_ct, const uint
 int hcnn_rotate_hoisted(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* ct, uint32_t level, uint32_t n_rot,
                         const uint64_t* galois, const uint64_t* const* keys_b, const uint64_t* const* keys_a,
                         void* ws, void* stream);
+/* Several MAC outputs over one shared term list (the HyPHEN conv's planes:
+ * every output plane of a layer sums masks against the same rotated input
+ * ciphertexts).  outs[g] (+)= sum_t cts[t] (.) masks[g * n_terms + t]; a null
+ * mask means output g has no term t.  Each ciphertext is read once per 4
+ * outputs instead of once per output; results equal hcnn_mac_terms on each
+ * output's non-null terms (packing.py:600-604 / :520-525). */
+int hcnn_mac_terms_multi(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* const* cts,
+                         const uint64_t* const* masks_mont, uint32_t n_out, uint32_t n_terms, uint32_t level,
+                         int accumulate, void* stream);
+
 /* ---- batched ciphertext ops ---------------------------------------------
  * A batch is nb ciphertexts stored back to back ([nb][2][level+1][N]); every
  * kernel of the op covers the whole batch and each key / mask load feeds

@@ -382,10 +382,11 @@ __global__ void k_modup(const FbcDev* __restrict__ tabs, const ModConsts* __rest
 // (key rows are Montgomery form, so the 128-bit sum REDCs straight to the
 // ordinary residue).  g != 1 applies the eval-domain Galois permutation to
 // the raised digits on the fly (hoisted rotation).
+int g_mac_batch = 1;  // shared-mask MAC: 1 = entry-fastest CTA order, 4 = 4 entries per thread
 int g_ks_batch = 1;  // measured: grid-batched entries share keys through L2; NB>1 costs occupancy
 
 template <int NB, int VEC>
-__global__ void __launch_bounds__(256) k_ks_inner(u64* __restrict__ acc, const u64* __restrict__ x_eval,
+__global__ void __launch_bounds__(256, NB == 1 ? 4 : 1) k_ks_inner(u64* __restrict__ acc, const u64* __restrict__ x_eval,
                                                   const u64* __restrict__ raised, const u64* __restrict__ key_b,
                                                   const u64* __restrict__ key_a, Basis basis, u32 alpha, u32 ndig,
                                                   u32 logN, u64 g, const ModConsts* __restrict__ mc, u32 nb,
@@ -399,17 +400,21 @@ __global__ void __launch_bounds__(256) k_ks_inner(u64* __restrict__ acc, const u
   const u64 q = mc[mod].q, ninv = mc[mod].ninv;
   const size_t key_dst = (size_t)(basis.Lq + basis.np) * N;  // per-digit key stride
   const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;     // digit owning limb r
-  const u32 b0 = blockIdx.z * NB;                             // NB batch entries share every key load
+  // NB == 1: blockIdx.x = tile * nb + entry -- the nb CTAs reading one key
+  // tile run back to back, so the key streams from HBM once per batch (L2
+  // serves the rest).  NB > 1: NB entries per thread (blockIdx.z chunks).
+  const u32 b0 = NB == 1 ? blockIdx.x % nb : blockIdx.z * NB;
   const u32 ne = nb - b0 < (u32)NB ? nb - b0 : (u32)NB;
   const size_t r_bst = (size_t)ndig * n_ext * N, a_bst = 2 * (size_t)n_ext * N;
-  for (u32 kv = blockIdx.x * blockDim.x + threadIdx.x; kv < N / VEC; kv += gridDim.x * blockDim.x) {
+  const u32 x0 = NB == 1 ? blockIdx.x / nb : blockIdx.x, xs = NB == 1 ? gridDim.x / nb : gridDim.x;
+  for (u32 kv = x0 * blockDim.x + threadIdx.x; kv < N / VEC; kv += xs * blockDim.x) {
     const u32 k = VEC * kv;
     u64 bh[NB][VEC], bl[NB][VEC], ah[NB][VEC], al[NB][VEC];
 #pragma unroll
     for (int e = 0; e < NB; ++e)
 #pragma unroll
       for (int v = 0; v < VEC; ++v) bh[e][v] = bl[e][v] = ah[e][v] = al[e][v] = 0;
-#pragma unroll 2
+#pragma unroll(NB == 1 ? 1 : 2)
     for (u32 j = 0; j < ndig; ++j) {
       const size_t kofs = (size_t)j * key_dst + (size_t)mod * N + k;
       u64 kb[VEC], ka[VEC];
@@ -528,13 +533,16 @@ __global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __re
   // one thread: VEC adjacent coefficients of both polys of NB batch entries
   // (ciphertexts 2*nl*N apart, nl = nq or nq + K limbs for Q||P); each mask
   // load feeds all of them
-  const u32 N = 1u << logN, r = blockIdx.y, b0 = blockIdx.z * NB;
+  // NB == 1: blockIdx.x = tile * nb + entry (entries sharing a mask tile run
+  // back to back: the mask streams once per batch)
+  const u32 N = 1u << logN, r = blockIdx.y, b0 = NB == 1 ? blockIdx.x % nb : blockIdx.z * NB;
   const u32 ne = nb - b0 < (u32)NB ? nb - b0 : (u32)NB;
+  const u32 x0 = NB == 1 ? blockIdx.x / nb : blockIdx.x, xs = NB == 1 ? gridDim.x / nb : gridDim.x;
   const u32 mod = r < nq ? r : Lq + (r - nq);
   const u64 q = mc[mod].q, ninv = mc[mod].ninv;
   const size_t bst = 2 * (size_t)nl * N, pst = (size_t)nl * N;
   const size_t off = (size_t)r * N + (size_t)b0 * bst, moff = (size_t)r * N;
-  for (u32 kv = blockIdx.x * blockDim.x + threadIdx.x; kv < N / VEC; kv += gridDim.x * blockDim.x) {
+  for (u32 kv = x0 * blockDim.x + threadIdx.x; kv < N / VEC; kv += xs * blockDim.x) {
     const u32 k = kv * VEC;
     u64 hi[NB][2][VEC], lo[NB][2][VEC];
 #pragma unroll
@@ -600,9 +608,10 @@ __global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __re
 cudaError_t launch_mac_terms(const MacTerms& T, int nt, u64* out, u32 nq, u32 logN, int accumulate,
                              const ModConsts* mc, cudaStream_t st, u32 nb, u32 np, u32 Lq) {
   const u32 nl = nq + np;
-  if (nb <= 1) {
+  if (nb <= 1 || g_mac_batch <= 1) {
     dim3 g = row_grid((1u << logN) / 2, nl, 256);
-    k_mac_terms<1, 2><<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc, 1, nl, Lq);
+    g.x *= (nb ? nb : 1);
+    k_mac_terms<1, 2><<<g, 256, 0, st>>>(T, nt, out, nq, logN, accumulate, mc, nb ? nb : 1, nl, Lq);
   } else {
     dim3 g = row_grid(1u << logN, nl, 256);
     g.z = (nb + 3) / 4;
@@ -648,6 +657,86 @@ __global__ void k_gather_limb(u64* __restrict__ out, const u64* __restrict__ in,
   const u32 N = 1u << logN, z = blockIdx.y;
   const u64* I = in + ((size_t)z * nlimbs + limb) * N;
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) out[(size_t)z * N + k] = I[k];
+}
+
+template <int G, int VEC>
+__global__ void __launch_bounds__(256) k_mac_multi(MacMulti M, int nt, u32 nq, u32 logN, int accumulate,
+                                                   const ModConsts* __restrict__ mc) {
+  // VEC adjacent coefficients of both polys for G outputs per thread: each
+  // ciphertext load feeds every output that has a mask for it
+  const u32 N = 1u << logN, r = blockIdx.y;
+  const u64 q = mc[r].q, ninv = mc[r].ninv;
+  const size_t pst = (size_t)nq * N, off = (size_t)r * N;
+  for (u32 kv = blockIdx.x * blockDim.x + threadIdx.x; kv < N / VEC; kv += gridDim.x * blockDim.x) {
+    const u32 k = VEC * kv;
+    u64 hi[G][2][VEC], lo[G][2][VEC];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) hi[g][p][v] = lo[g][p][v] = 0;
+#pragma unroll 2
+    for (int t = 0; t < nt; ++t) {
+      // all loads of the term first (null masks predicated to zero) so the
+      // unrolled iterations keep several loads in flight
+      u64 x[2][VEC], m[G][VEC];
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const u64* src = M.ct[t] + p * pst + off + k;
+        if (VEC == 2) {
+          const ulonglong2 v2 = *reinterpret_cast<const ulonglong2*>(src);
+          x[p][0] = v2.x;
+          x[p][VEC - 1] = v2.y;
+        } else {
+          x[p][0] = *src;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const u64* mp = M.mask[g][t];
+        if (VEC == 2) {
+          const ulonglong2 m2 = mp ? *reinterpret_cast<const ulonglong2*>(mp + off + k) : make_ulonglong2(0, 0);
+          m[g][0] = m2.x;
+          m[g][VEC - 1] = m2.y;
+        } else {
+          m[g][0] = mp ? mp[off + k] : 0ull;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) mac128(hi[g][p][v], lo[g][p][v], x[p][v], m[g][v], q);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        u64* dst = M.out[g] + p * pst + off + k;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          u64 y = redc128(hi[g][p][v], lo[g][p][v], q, ninv);
+          if (accumulate) y = add_mod(y, dst[v], q);
+          dst[v] = y;
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN, int accumulate,
+                             const ModConsts* mc, cudaStream_t st) {
+  dim3 g2 = row_grid((1u << logN) / 2, nq, 256), g1 = row_grid(1u << logN, nq, 256);
+  switch (ng) {
+    case 1: k_mac_multi<1, 2><<<g2, 256, 0, st>>>(M, nt, nq, logN, accumulate, mc); break;
+    case 2: k_mac_multi<2, 2><<<g2, 256, 0, st>>>(M, nt, nq, logN, accumulate, mc); break;
+    case 3: k_mac_multi<3, 1><<<g1, 256, 0, st>>>(M, nt, nq, logN, accumulate, mc); break;
+    case 4: k_mac_multi<4, 1><<<g1, 256, 0, st>>>(M, nt, nq, logN, accumulate, mc); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -770,7 +859,7 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
                             cudaStream_t st, u32 nb, size_t x_bst, const u64* c0, size_t c0_bst, const u64* pR) {
   if (nb <= 1 || g_ks_batch <= 1) {
     dim3 grid = row_grid((1u << logN) / 2, basis.nlimbs(), 256);
-    grid.z = nb;
+    grid.x *= (nb ? nb : 1);
     k_ks_inner<1, 2><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,
                                            nb ? nb : 1, x_bst, c0, c0_bst, pR);
   } else if (nb == 2 || g_ks_batch == 2) {

@@ -28,6 +28,7 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
 // acc [nb][2][n_ext]; x_eval entries x_bst apart; one key load feeds up to
 // g_ks_batch (1, 2 or 4) entries (hcnn_set_option "ks_batch")
 extern int g_ks_batch;
+extern int g_mac_batch;
 // c0 (nullable): adds P * sigma_g(c0) on the Q limbs (pR[i] = P R mod q_i) --
 // the extended-basis (ModDown-free) rotation of double hoisting
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
@@ -75,6 +76,18 @@ struct MacTerms {
 // np > 0: ciphertexts / masks over Q_l||P (nq + np limbs; P moduli at Lq..)
 cudaError_t launch_mac_terms(const MacTerms& T, int nt, u64* out, u32 nq, u32 logN, int accumulate,
                              const ModConsts* mc, cudaStream_t st, u32 nb = 1, u32 np = 0, u32 Lq = 0);
+// several outputs sharing one term list (HyPHEN conv planes): each rotated
+// ciphertext is read once per launch for up to kMultiG outputs; masks may be
+// null (the output has no such term)
+constexpr int kMultiG = 4;
+constexpr int kMultiT = 48;
+struct MacMulti {
+  const u64* ct[kMultiT];
+  const u64* mask[kMultiG][kMultiT];
+  u64* out[kMultiG];
+};
+cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN, int accumulate,
+                             const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_gather_limb(u64* out, const u64* in, u32 limb, u32 nlimbs, u32 logN, u32 npolys,
                                cudaStream_t st);
 

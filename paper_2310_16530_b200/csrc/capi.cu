@@ -929,6 +929,38 @@ static int mac_terms_impl(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts
   return HCNN_OK;
 }
 
+int hcnn_mac_terms_multi(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* const* cts,
+                         const uint64_t* const* masks, uint32_t n_out, uint32_t n_terms, uint32_t level, int accumulate,
+                         void* s) {
+  if (!c) return fail(HCNN_E_PARAMETER, "null context");
+  if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
+  const u32 nq = level + 1;
+  for (u32 g0 = 0; g0 < n_out; g0 += kMultiG) {
+    const u32 ng = std::min<u32>(kMultiG, n_out - g0);
+    if (n_terms == 0) {
+      if (!accumulate)
+        for (u32 g = 0; g < ng; ++g) CK(cudaMemsetAsync(outs[g0 + g], 0, 2ull * nq * c->n * 8, STREAM(s)));
+      continue;
+    }
+    for (u32 t0 = 0; t0 < n_terms; t0 += kMultiT) {
+      const u32 nt = std::min<u32>(kMultiT, n_terms - t0);
+      MacMulti M;
+      for (u32 t = 0; t < nt; ++t) M.ct[t] = cts[t0 + t];
+      double used = 0;
+      for (u32 g = 0; g < (u32)kMultiG; ++g) {
+        M.out[g] = g < ng ? outs[g0 + g] : nullptr;
+        for (u32 t = 0; t < nt; ++t) {
+          M.mask[g][t] = g < ng ? masks[(size_t)(g0 + g) * n_terms + t0 + t] : nullptr;
+          used += M.mask[g][t] ? 1 : 0;
+        }
+      }
+      PK("mac_multi", 8.0 * (2.0 * nt + used + 2.0 * ng * (accumulate || t0 ? 2 : 1)) * nq * c->n, 1, STREAM(s),
+         launch_mac_multi(M, (int)ng, (int)nt, nq, c->logN, accumulate || t0 > 0, c->d_mc, STREAM(s)));
+    }
+  }
+  return HCNN_OK;
+}
+
 size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* c, uint32_t npolys) { return (size_t)npolys * c->n * 8; }
 
 int hcnn_rescale(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint32_t level, uint32_t npolys, void* ws,
@@ -966,6 +998,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_occupancy") g_ntt_tuning.occupancy = (int)value;
   else if (k == "ntt_split") g_ntt_tuning.split = (int)value;
   else if (k == "ks_batch") g_ks_batch = (int)value;
+  else if (k == "mac_batch") g_mac_batch = (int)value;
   else return fail(HCNN_E_PARAMETER, "unknown option " + k);
   return HCNN_OK;
 }

@@ -244,6 +244,24 @@ class DeviceContext:
                                                      _native.u64_array(galois), kb, ka, _ptr(ws), _stream()))
         return outs
 
+    def mac_terms_multi(self, cts: Sequence[torch.Tensor], masks: Sequence[Sequence[torch.Tensor | None]],
+                        level: int, outs: Sequence[torch.Tensor] | None = None,
+                        accumulate: bool = False) -> list[torch.Tensor]:
+        """outs[g] (+)= sum_t cts[t] (.) masks[g][t] (None: no term), one ciphertext read per 4 outputs."""
+        G, T = len(masks), len(cts)
+        for c in cts:
+            if not c.is_contiguous() or c.shape != (2, level + 1, self.n):
+                raise BasisError("mac_terms_multi ciphertexts must be contiguous [2, l+1, N]")
+        if outs is None:
+            outs = [self.empty(2, level + 1, self.n) for _ in range(G)]
+        P = ctypes.c_void_p
+        flat = [(m.data_ptr() if m is not None else None) for row in masks for m in row]
+        self._chk(self.lib.hcnn_mac_terms_multi(self.handle, (P * max(G, 1))(*[o.data_ptr() for o in outs]),
+                                                (P * max(T, 1))(*[c.data_ptr() for c in cts]),
+                                                (P * max(G * T, 1))(*flat), G, T, level, 1 if accumulate else 0,
+                                                _stream()))
+        return list(outs)
+
     # -- extended basis Q_l||P (double-hoisted linear transforms) --------------
     def rotate_hoisted_ext(self, ct: torch.Tensor, level: int, galois: Sequence[int],
                            keys: Sequence[tuple[torch.Tensor, torch.Tensor]]) -> list[torch.Tensor]:

@@ -192,3 +192,25 @@ def test_batched_ops_match_single(small, cts):
     rs = ckks.unstack(ckks.rescale(A, params))
     for a, r in zip(ckks.unstack(A), rs):
         assert torch.equal(r.data, ckks.rescale(a, params).data)
+
+
+def test_mac_terms_multi_matches_per_output(small, cts):
+    """Multi-output MAC over a shared term list (null = absent term) equals
+    one mac_terms per output on its present terms."""
+    import torch
+    from paper_2310_16530_b200 import ckks
+    params, ks = small
+    _, ct1, ct2 = cts
+    ctx = params.ctx
+    rng = np.random.default_rng(12)
+    lvl = ct1.level
+    srcs = [ct1.data, ct2.data] + [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl), ks,
+                                                 rng).data for _ in range(3)]
+    mk = lambda: ctx.unop("to_mont", ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl).data, lvl + 1)
+    for G in (1, 2, 3, 4, 6):
+        masks = [[mk() if (g + t) % 3 else None for t in range(len(srcs))] for g in range(G)]
+        got = ctx.mac_terms_multi(srcs, masks, lvl)
+        for g in range(G):
+            terms = [(s, m) for s, m in zip(srcs, masks[g]) if m is not None]
+            want = ctx.mac_terms([s for s, _ in terms], [m for _, m in terms], lvl)
+            assert torch.equal(got[g], want)
