@@ -3,7 +3,7 @@
 Runs only in the build container, where /root/reference exists:
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python tests/golden/make_golden.py [small|deskA|bench16|layers ...]
+        python tests/golden/make_golden.py [small|deskA|bench16|layers|host|hcnk ...]
 
 Outputs (all small enough to commit):
   golden_small.npz      full residue arrays at a 256-ring (the reference's
@@ -304,8 +304,30 @@ def gen_host():
     print("host done")
 
 
+# ---------------------------------------------------------------------------
+def gen_hcnk():
+    """HCNK containers written by the reference's io.py (io.py:54-249) for the
+    unit-small key set and ciphertexts of gen_small: the device loader must
+    read them, and the device writer must reproduce them byte for byte."""
+    from hcnn import io as hio
+    params = ckks.CkksParams.build("unit-small", 256, 50, 40, 4, 50, 2)
+    ks = ckks.keygen(params, np.random.default_rng(3), rotations=[1, 2, 4])
+    vrng = np.random.default_rng(12345)
+    v1 = vrng.uniform(-1, 1, params.slots)
+    L = params.max_level
+    ct1 = ckks.encrypt(ckks.encode(v1, params, L), ks, np.random.default_rng(77))
+    hio.save_keyset(str(HERE / "hcnk_unit_small.keyset"), ks)
+    hio.save_ciphertext(str(HERE / "hcnk_unit_small_ct1.ct"), ct1, params)
+    hio.save_ciphertext(str(HERE / "hcnk_unit_small_ct1_l2.ct"), ckks.mod_drop(ct1, 2), params)
+    from hcnn.packing import PackedTensor, PackingFormat, TensorShape
+    pt = PackedTensor(cts=[ct1, ckks.mod_drop(ct1, L)], fmt=PackingFormat("B", 4, 1, 4),
+                      shape=TensorShape(8, 2, 2))
+    hio.save_packed_tensor(str(HERE / "hcnk_unit_small.packed"), pt, params)
+    print("hcnk done")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "deskA", "bench16", "layers", "host"]
+    which = sys.argv[1:] or ["small", "deskA", "bench16", "layers", "host", "hcnk"]
     for w in which:
         {"small": gen_small, "deskA": gen_deska, "bench16": gen_bench16, "layers": gen_layers,
-         "host": gen_host}[w]()
+         "host": gen_host, "hcnk": gen_hcnk}[w]()
