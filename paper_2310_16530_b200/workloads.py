@@ -35,7 +35,8 @@ def resnet20_setup(app_levels: int = 14, seed: int = 3, key_seed: int = 20) -> R
     fx = graph.gen_fixture("resnet20", seed, params, golden_count=1)
     g = graph.build_graph("resnet20", fx, multiplex=4)
     plan = graph.plan_levels(g, boot.output_level, refresh_target=boot.output_level, count_snapshots=True)
-    ks = boot.keygen(np.random.default_rng(key_seed), rotations=sorted(graph.required_rotation_steps(g, params.slots)))
+    steps = graph.required_rotation_steps(g, params.slots) | graph.refresh_rotation_steps(g, plan, params.slots)
+    ks = boot.keygen(np.random.default_rng(key_seed), rotations=sorted(steps))
     return ResNet20Setup(params, cfg, boot, fx, g, plan, ks)
 
 

@@ -111,6 +111,33 @@ def test_bootstrap_pairs_round_trip(boot12):
         assert err < 1e-3, err
 
 
+def test_packed_refresh_of_sparse_layout(boot12):
+    """Refresh of a gap-2 FormatB tensor: 2 ciphertexts interleaved into one
+    (graph.refresh_shifts), paired, bootstrapped, moved back -- every
+    occupied slot of every replica comes back within bootstrap precision."""
+    from paper_2310_16530_b200 import bootstrap as bt, ckks, graph, packing
+    params, cfg, b, ks0 = boot12
+    fmt = packing.PackingFormat("B", 2, 2, 256)
+    shape = packing.TensorShape(8, 8, 8)
+    shifts = graph.refresh_shifts(fmt, shape, params.slots)
+    assert shifts == [0, 1, 16, 17]
+    ks = b.keygen(np.random.default_rng(7), rotations=sorted({s for s in shifts if s} | {-s % params.slots for s in shifts}))
+    rng = np.random.default_rng(8)
+    x = rng.uniform(-1, 1, (8, 8, 8))
+    pt = packing.encrypt_tensor(x, fmt, ks, rng, 2)
+    assert len(pt.cts) == 4
+    tally = packing.OpTally()
+    out = graph._refresh_tensors([pt], ks, b.output_level, tally, cache={})[0]
+    assert tally.refreshes == 4
+    lay = packing.Layout(fmt, shape, params.slots)
+    want = packing.pack(x, fmt, params.slots)
+    for j, ct in enumerate(out.cts):
+        assert ct.level == b.output_level and abs(ct.scale - pt.cts[j].scale) < 1e-9 * ct.scale
+        got = ckks.decode(ckks.decrypt(ct, ks), params, imag_tol=None)
+        occ = lay.occupancy(j) > 0
+        assert np.max(np.abs(got[occ] - want[j][occ])) < 2e-3
+
+
 def test_graph_refresh_slot_bootstraps():
     """Two stacked basic blocks need a refresh between them (6 levels each):
     the executor's refresh slot bootstraps (no decryption), and the result
