@@ -155,10 +155,13 @@ int hcnn_mac_terms_multi(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* c
 size_t hcnn_ks_workspace_bytes_batch(const hcnn_ctx* ctx, uint32_t level, uint32_t nb);
 int hcnn_hmult_batch(hcnn_ctx* ctx, uint64_t* out_cts, const uint64_t* a_cts, const uint64_t* b_cts, uint32_t level,
                      uint32_t nb, const uint64_t* rlk_b, const uint64_t* rlk_a, void* ws, void* stream);
-/* outs[i]: batch buffer receiving rotation i of every entry */
+/* outs[i]: batch buffer receiving rotation i of every entry.  key_lqs
+ * (nullable): key i is stored truncated to its first key_lqs[i] q-limbs
+ * (rows [ceil(key_lqs[i]/K)][key_lqs[i]+K][N], same residues as the full
+ * key's prefix) -- enough for every level < key_lqs[i]; 0 = full key. */
 int hcnn_rotate_hoisted_batch(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* cts, uint32_t level,
                               uint32_t nb, uint32_t n_rot, const uint64_t* galois, const uint64_t* const* keys_b,
-                              const uint64_t* const* keys_a, void* ws, void* stream);
+                              const uint64_t* const* keys_a, const uint32_t* key_lqs, void* ws, void* stream);
 /* hcnn_mac_terms over batches: cts[t] and out_cts are batches, the masks are
  * shared by every entry (bootstrapping's CtS/StC diagonals) */
 int hcnn_mac_terms_batch(hcnn_ctx* ctx, uint64_t* out_cts, const uint64_t* const* cts,
@@ -173,8 +176,8 @@ int hcnn_mac_terms_batch(hcnn_ctx* ctx, uint64_t* out_cts, const uint64_t* const
  * reference counterpart (the reference has no bootstrapping). */
 int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* ctx, uint64_t* const* outs_ext, const uint64_t* cts, uint32_t level,
                                   uint32_t nb, uint32_t n_rot, const uint64_t* galois,
-                                  const uint64_t* const* keys_b, const uint64_t* const* keys_a, void* ws,
-                                  void* stream);
+                                  const uint64_t* const* keys_b, const uint64_t* const* keys_a,
+                                  const uint32_t* key_lqs, void* ws, void* stream);
 int hcnn_mac_terms_ext_batch(hcnn_ctx* ctx, uint64_t* out_ext, const uint64_t* const* cts_ext,
                              const uint64_t* const* masks_mont_ext, uint32_t n_terms, uint32_t level, uint32_t nb,
                              int accumulate, void* stream);

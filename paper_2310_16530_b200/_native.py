@@ -66,13 +66,13 @@ SIGNATURES = {
     "hcnn_ks_workspace_bytes_batch": (_SZ, [_VP, _U32, _U32]),
     "hcnn_hmult_batch": (_INT, [_VP, _VP, _VP, _VP, _U32, _U32, _VP, _VP, _VP, _VP]),
     "hcnn_rotate_hoisted_batch": (_INT, [_VP, ctypes.POINTER(_VP), _VP, _U32, _U32, _U32, _PU64,
-                                         ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP, _VP]),
+                                         ctypes.POINTER(_VP), ctypes.POINTER(_VP), _PU32, _VP, _VP]),
     "hcnn_mac_terms_multi": (_INT, [_VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), ctypes.POINTER(_VP), _U32, _U32,
                                     _U32, _INT, _VP]),
     "hcnn_mac_terms_batch": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _U32, _U32, _U32, _INT,
                                     _VP]),
     "hcnn_rotate_hoisted_ext_batch": (_INT, [_VP, ctypes.POINTER(_VP), _VP, _U32, _U32, _U32, _PU64,
-                                             ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP, _VP]),
+                                             ctypes.POINTER(_VP), ctypes.POINTER(_VP), _PU32, _VP, _VP]),
     "hcnn_mac_terms_ext_batch": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _U32, _U32, _U32,
                                         _INT, _VP]),
     "hcnn_moddown_batch": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP, _VP]),

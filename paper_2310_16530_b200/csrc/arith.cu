@@ -391,14 +391,17 @@ __global__ void __launch_bounds__(256, NB == 1 ? 4 : 1) k_ks_inner(u64* __restri
                                                   const u64* __restrict__ key_a, Basis basis, u32 alpha, u32 ndig,
                                                   u32 logN, u64 g, const ModConsts* __restrict__ mc, u32 nb,
                                                   size_t x_bst, const u64* __restrict__ c0, size_t c0_bst,
-                                                  const u64* __restrict__ pR) {
+                                                  const u64* __restrict__ pR, u32 key_lq) {
   // VEC adjacent coefficients x NB batch entries per thread (NB*VEC <= 4 keeps
   // the 128-bit accumulators at 16 registers pairs: full occupancy)
   const u32 N = 1u << logN, r = blockIdx.y;
   const u32 n_ext = basis.nlimbs();
   const u32 mod = basis.mod_of(r);
   const u64 q = mc[mod].q, ninv = mc[mod].ninv;
-  const size_t key_dst = (size_t)(basis.Lq + basis.np) * N;  // per-digit key stride
+  // keys may be stored truncated to their first key_lq q-limbs (+ all specials)
+  const u32 klq = key_lq ? key_lq : basis.Lq;
+  const size_t key_dst = (size_t)(klq + basis.np) * N;  // per-digit key stride
+  const u32 kmod = mod < basis.Lq ? mod : klq + (mod - basis.Lq);
   const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;     // digit owning limb r
   // NB == 1: blockIdx.x = tile * nb + entry -- the nb CTAs reading one key
   // tile run back to back, so the key streams from HBM once per batch (L2
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(256, NB == 1 ? 4 : 1) k_ks_inner(u64* __restri
       for (int v = 0; v < VEC; ++v) bh[e][v] = bl[e][v] = ah[e][v] = al[e][v] = 0;
 #pragma unroll(NB == 1 ? 1 : 2)
     for (u32 j = 0; j < ndig; ++j) {
-      const size_t kofs = (size_t)j * key_dst + (size_t)mod * N + k;
+      const size_t kofs = (size_t)j * key_dst + (size_t)kmod * N + k;
       u64 kb[VEC], ka[VEC];
       if (VEC == 2) {
         const ulonglong2 b2 = *reinterpret_cast<const ulonglong2*>(key_b + kofs);
@@ -856,22 +859,23 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
 
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
-                            cudaStream_t st, u32 nb, size_t x_bst, const u64* c0, size_t c0_bst, const u64* pR) {
+                            cudaStream_t st, u32 nb, size_t x_bst, const u64* c0, size_t c0_bst, const u64* pR,
+                            u32 key_lq) {
   if (nb <= 1 || g_ks_batch <= 1) {
     dim3 grid = row_grid((1u << logN) / 2, basis.nlimbs(), 256);
     grid.x *= (nb ? nb : 1);
     k_ks_inner<1, 2><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,
-                                           nb ? nb : 1, x_bst, c0, c0_bst, pR);
+                                           nb ? nb : 1, x_bst, c0, c0_bst, pR, key_lq);
   } else if (nb == 2 || g_ks_batch == 2) {
     dim3 grid = row_grid(1u << logN, basis.nlimbs(), 256);
     grid.z = (nb + 1) / 2;
     k_ks_inner<2, 1><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nb,
-                                           x_bst, c0, c0_bst, pR);
+                                           x_bst, c0, c0_bst, pR, key_lq);
   } else {
     dim3 grid = row_grid(1u << logN, basis.nlimbs(), 256);
     grid.z = (nb + 3) / 4;
     k_ks_inner<4, 1><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nb,
-                                           x_bst, c0, c0_bst, pR);
+                                           x_bst, c0, c0_bst, pR, key_lq);
   }
   return cudaGetLastError();
 }

@@ -771,12 +771,13 @@ static int ks_moddown(hcnn_ctx* c, u32 level, u64* acc, u64* lift, u64* out0, u6
 // for nb entries: outputs / addends of entry b at +b*out_bst / +b*add_bst
 static int ks_finish(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, u64 g, const u64* kb,
                      const u64* ka, u64* out0, u64* out1, const u64* add0, const u64* add1, u64 g_add,
-                     cudaStream_t st, u32 nb = 1, size_t x_bst = 0, size_t out_bst = 0, size_t add_bst = 0) {
+                     cudaStream_t st, u32 nb = 1, size_t x_bst = 0, size_t out_bst = 0, size_t add_bst = 0,
+                     u32 key_lq = 0) {
   const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
   const size_t N = c->n;
   PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, st,
      launch_ks_inner(w.acc, x_eval, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, g, c->d_mc, st,
-                     nb, x_bst));
+                     nb, x_bst, nullptr, 0, nullptr, key_lq));
   return ks_moddown(c, level, w.acc, w.lift, out0, out1, add0, add1, g_add, st, nb, out_bst, add_bst);
 }
 
@@ -821,9 +822,16 @@ int hcnn_hmult(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b,
   return hcnn_hmult_batch(c, out, a, b, level, 1, kb, ka, ws, s);
 }
 
+static int key_lq_ok(const hcnn_ctx* c, const uint32_t* key_lqs, uint32_t n, uint32_t level) {
+  for (uint32_t i = 0; key_lqs && i < n; ++i)
+    if (key_lqs[i] && (key_lqs[i] <= level || key_lqs[i] > c->Lq))
+      return fail(HCNN_E_KEY, "rotation key truncated below the ciphertext level");
+  return HCNN_OK;
+}
+
 int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* cts, uint32_t level, uint32_t nb,
                               uint32_t n_rot, const uint64_t* galois, const uint64_t* const* kbs,
-                              const uint64_t* const* kas, void* ws, void* s) {
+                              const uint64_t* const* kas, const uint32_t* key_lqs, void* ws, void* s) {
   int rc = check_level(c, level);
   if (rc) return rc;
   if (nb == 0) return HCNN_OK;
@@ -831,6 +839,8 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
   const size_t N = c->n, ct = 2 * (size_t)nq * N;
   for (u32 i = 0; i < n_rot; ++i)
     if ((galois[i] % (2ull * c->n) & 1) == 0) return fail(HCNN_E_PARAMETER, "galois element must be odd");
+  rc = key_lq_ok(c, key_lqs, n_rot, level);
+  if (rc) return rc;
   KsWs w = ks_layout(c, level, ws, nb);
   const u64* c1 = cts + nq * N;
   rc = ks_modup(c, level, c1, w, STREAM(s), nb, ct);
@@ -838,7 +848,7 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
   for (u32 i = 0; i < n_rot; ++i) {
     u64 g = galois[i] % (2ull * c->n);
     rc = ks_finish(c, level, c1, w, g, kbs[i], kas[i], outs[i], outs[i] + nq * N, cts, nullptr, g, STREAM(s), nb, ct,
-                   ct, ct);
+                   ct, ct, key_lqs ? key_lqs[i] : 0);
     if (rc) return rc;
   }
   return HCNN_OK;
@@ -846,7 +856,7 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
 
 int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* cts, uint32_t level,
                                   uint32_t nb, uint32_t n_rot, const uint64_t* galois, const uint64_t* const* kbs,
-                                  const uint64_t* const* kas, void* ws, void* s) {
+                                  const uint64_t* const* kas, const uint32_t* key_lqs, void* ws, void* s) {
   int rc = check_level(c, level);
   if (rc) return rc;
   if (nb == 0) return HCNN_OK;
@@ -854,6 +864,8 @@ int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* c, uint64_t* const* outs, const uint
   const size_t N = c->n, ct = 2 * (size_t)nq * N;
   for (u32 i = 0; i < n_rot; ++i)
     if ((galois[i] % (2ull * c->n) & 1) == 0) return fail(HCNN_E_PARAMETER, "galois element must be odd");
+  rc = key_lq_ok(c, key_lqs, n_rot, level);
+  if (rc) return rc;
   KsWs w = ks_layout(c, level, ws, nb);
   const u64* c1 = cts + nq * N;
   rc = ks_modup(c, level, c1, w, STREAM(s), nb, ct);
@@ -862,7 +874,7 @@ int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* c, uint64_t* const* outs, const uint
     const u64 g = galois[i] % (2ull * c->n);
     PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext + nb * nq) * N, 1, STREAM(s),
        launch_ks_inner(outs[i], c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd, c->logN, g,
-                       c->d_mc, STREAM(s), nb, ct, cts, ct, c->d_pR));
+                       c->d_mc, STREAM(s), nb, ct, cts, ct, c->d_pR, key_lqs ? key_lqs[i] : 0));
   }
   return HCNN_OK;
 }
@@ -880,7 +892,7 @@ int hcnn_moddown_batch(hcnn_ctx* c, uint64_t* out, uint64_t* in_ext, uint32_t le
 int hcnn_rotate_hoisted(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* ct, uint32_t level, uint32_t n_rot,
                         const uint64_t* galois, const uint64_t* const* kbs, const uint64_t* const* kas, void* ws,
                         void* s) {
-  return hcnn_rotate_hoisted_batch(c, outs, ct, level, 1, n_rot, galois, kbs, kas, ws, s);
+  return hcnn_rotate_hoisted_batch(c, outs, ct, level, 1, n_rot, galois, kbs, kas, nullptr, ws, s);
 }
 
 int hcnn_mac_terms_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts, const uint64_t* const* masks,

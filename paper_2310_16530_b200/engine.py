@@ -241,8 +241,13 @@ class DeviceContext:
         kb = P(*[k[0].data_ptr() for k in keys])
         ka = P(*[k[1].data_ptr() for k in keys])
         self._chk(self.lib.hcnn_rotate_hoisted_batch(self.handle, outs_p, _ptr(ct), level, nb, n_rot,
-                                                     _native.u64_array(galois), kb, ka, _ptr(ws), _stream()))
+                                                     _native.u64_array(galois), kb, ka, self._key_lqs(keys),
+                                                     _ptr(ws), _stream()))
         return outs
+
+    def _key_lqs(self, keys):
+        """q-limb rows of each key (a truncated key stores a prefix; see KeySet.truncate_rotations)"""
+        return _native.u32_array([int(k[0].shape[-2]) - self.K for k in keys])
 
     def mac_terms_multi(self, cts: Sequence[torch.Tensor], masks: Sequence[Sequence[torch.Tensor | None]],
                         level: int, outs: Sequence[torch.Tensor] | None = None,
@@ -276,7 +281,7 @@ class DeviceContext:
         self._chk(self.lib.hcnn_rotate_hoisted_ext_batch(
             self.handle, P(*[o.data_ptr() for o in outs]), _ptr(ct), level, nb, len(outs),
             _native.u64_array(galois), P(*[k[0].data_ptr() for k in keys]), P(*[k[1].data_ptr() for k in keys]),
-            _ptr(ws), _stream()))
+            self._key_lqs(keys), _ptr(ws), _stream()))
         return outs
 
     def mac_terms_ext(self, cts: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], level: int,

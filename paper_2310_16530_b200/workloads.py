@@ -37,6 +37,8 @@ def resnet20_setup(app_levels: int = 14, seed: int = 3, key_seed: int = 20) -> R
     plan = graph.plan_levels(g, boot.output_level, refresh_target=boot.output_level, count_snapshots=True)
     steps = graph.required_rotation_steps(g, params.slots) | graph.refresh_rotation_steps(g, plan, params.slots)
     ks = boot.keygen(np.random.default_rng(key_seed), rotations=sorted(steps))
+    # keys used only at application levels keep their low-level rows (HBM for resident masks)
+    ks.truncate_rotations(sorted(set(steps) - boot.rotation_steps()), boot.output_level)
     return ResNet20Setup(params, cfg, boot, fx, g, plan, ks)
 
 

@@ -214,3 +214,23 @@ def test_mac_terms_multi_matches_per_output(small, cts):
             terms = [(s, m) for s, m in zip(srcs, masks[g]) if m is not None]
             want = ctx.mac_terms([s for s, _ in terms], [m for _, m in terms], lvl)
             assert torch.equal(got[g], want)
+
+
+def test_truncated_rotation_keys(small, cts):
+    """Rotation keys cut down to the rows levels <= 2 read give identical
+    rotations there and refuse higher levels (KeyError_)."""
+    import torch
+    from paper_2310_16530_b200 import ckks
+    from paper_2310_16530_b200.errors import KeyError_
+    params, ks = small
+    _, ct1, _ = cts
+    kt = ckks.keygen(params, np.random.default_rng(3), rotations=[1, 2, 4])
+    freed = kt.truncate_rotations([1, 4], 2)
+    assert freed > 0 and kt.gks[2].rows_b.shape == ks.gks[2].rows_b.shape
+    low = ckks.mod_drop(ct1, 2)
+    for k in (1, 3, 4):
+        assert torch.equal(ckks.rotate(low, k, kt).data, ckks.rotate(low, k, ks).data)
+    many = ckks.rotate_many(ckks.stack([low, low]), [1, 4], kt)
+    assert torch.equal(ckks.unstack(many[1])[1].data, ckks.rotate(low, 4, ks).data)
+    with pytest.raises(KeyError_):
+        ckks.rotate(ct1, 1, kt)
