@@ -303,17 +303,18 @@ template <int NS>
 __global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, int tab_per_z,
                                                const ModConsts* __restrict__ mc, const u64* __restrict__ in,
                                                size_t in_pst, u64* __restrict__ out, size_t out_pst, u32 logN,
-                                               u32 nt_override, u32 z0, u32 zdiv, size_t in_bst, size_t out_bst) {
+                                               u32 nt_override, u32 z0, u32 zdiv, size_t in_bst, size_t out_bst,
+                                               u32 tg) {
   constexpr int NM = 1 << NS;
   extern __shared__ u64 sh[];
   // blockIdx.y = b * zdiv + j: poly/digit j of batch entry b
   const u32 N = 1u << logN, b = blockIdx.y / zdiv, z = blockIdx.y % zdiv + z0;
   const FbcDev& T = tabs[tab_per_z ? z : 0];
   const u32 nt_all = nt_override ? nt_override : T.nt;
-  // blockIdx.z selects a group of kFbcTG targets (more CTAs; y recomputed)
-  const u32 t0 = blockIdx.z * kFbcTG;
+  // blockIdx.z selects a group of tg targets (small conversions get more CTAs)
+  const u32 t0 = blockIdx.z * tg;
   if (t0 >= nt_all) return;
-  const u32 nt = nt_all - t0 < kFbcTG ? nt_all - t0 : kFbcTG;
+  const u32 nt = nt_all - t0 < tg ? nt_all - t0 : tg;
   u64* s_q = sh;
   u64* s_ninv = s_q + nt;
   u64* s_pos = s_ninv + nt;
@@ -791,19 +792,33 @@ static size_t fbc_smem(u32 nt, int ns) {
   return (size_t)nt * (3 + ns + (1u << ns)) * 8;
 }
 
+// targets per CTA: all of them (up to kFbcTG) unless the conversion is too
+// small to fill the GPU, then split so there are >= ~8 CTAs per SM
+static u32 fbc_group(u32 nt, u32 base_ctas) {
+  u32 tg = nt < (u32)kFbcTG ? nt : (u32)kFbcTG;
+  const u32 want = 148u * 8u;
+  if (base_ctas < want && tg > 1) {
+    u32 split = (want + base_ctas - 1) / base_ctas;
+    if (split > tg) split = tg;
+    tg = (tg + split - 1) / split;
+  }
+  return tg ? tg : 1;
+}
+
 template <int NS>
 static cudaError_t launch_fbc_t(const FbcDev* tabs, int tab_per_z, const ModConsts* mc, const u64* in,
                                 size_t in_pst, u64* out, size_t out_pst, u32 logN, u32 nz, u32 z0, u32 nt,
                                 u32 nt_override, u32 nb, size_t in_bst, size_t out_bst, cudaStream_t st) {
-  size_t sm = fbc_smem(nt, NS);
+  dim3 g = row_grid(1u << logN, nz * nb, 256);
+  const u32 tg = fbc_group(nt, g.x * g.y);
+  size_t sm = fbc_smem(tg, NS);
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_fbc_t<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
   }
-  dim3 g = row_grid((1u << logN) / 2, nz * nb, 256);
-  g.z = (nt + kFbcTG - 1) / kFbcTG;
+  g.z = (nt + tg - 1) / tg;
   k_fbc_t<NS><<<g, 256, sm, st>>>(tabs, tab_per_z, mc, in, in_pst, out, out_pst, logN, nt_override, z0, nz, in_bst,
-                                  out_bst);
+                                  out_bst, tg);
   return cudaGetLastError();
 }
 
