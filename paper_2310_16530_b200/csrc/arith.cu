@@ -673,6 +673,9 @@ __global__ void __launch_bounds__(256) k_mac_multi(MacMulti M, int nt, u32 nq, u
   const size_t pst = (size_t)nq * N, off = (size_t)r * N;
   for (u32 kv = blockIdx.x * blockDim.x + threadIdx.x; kv < N / VEC; kv += gridDim.x * blockDim.x) {
     const u32 k = VEC * kv;
+    // byte offsets of this thread's coefficient in a packed mask's planes (limb r > 0)
+    const size_t lo_off = 8 * (size_t)N + 4 * ((size_t)(r - 1) * N + k);
+    const size_t hi_off = 8 * (size_t)N + 4 * (size_t)(nq - 1) * N + 2 * ((size_t)(r - 1) * N + k);
     u64 hi[G][2][VEC], lo[G][2][VEC];
 #pragma unroll
     for (int g = 0; g < G; ++g)
@@ -699,12 +702,26 @@ __global__ void __launch_bounds__(256) k_mac_multi(MacMulti M, int nt, u32 nq, u
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const u64* mp = M.mask[g][t];
+        if (mp && M.packed[g][t] && r > 0) {  // 48-bit packed limb: u32 low plane + u16 high plane
+          const char* b = reinterpret_cast<const char*>(mp);
+          if (VEC == 2) {
+            const uint2 l2 = *reinterpret_cast<const uint2*>(b + lo_off);
+            const unsigned h2 = *reinterpret_cast<const unsigned*>(b + hi_off);
+            m[g][0] = (u64)l2.x | ((u64)(h2 & 0xffffu) << 32);
+            m[g][VEC - 1] = (u64)l2.y | ((u64)(h2 >> 16) << 32);
+          } else {
+            m[g][0] = (u64)*reinterpret_cast<const unsigned*>(b + lo_off) |
+                      ((u64)*reinterpret_cast<const unsigned short*>(b + hi_off) << 32);
+          }
+          continue;
+        }
+        const u64* src = (mp && M.packed[g][t]) ? mp + k : mp + off + k;  // packed limb 0 sits first
         if (VEC == 2) {
-          const ulonglong2 m2 = mp ? *reinterpret_cast<const ulonglong2*>(mp + off + k) : make_ulonglong2(0, 0);
+          const ulonglong2 m2 = mp ? *reinterpret_cast<const ulonglong2*>(src) : make_ulonglong2(0, 0);
           m[g][0] = m2.x;
           m[g][VEC - 1] = m2.y;
         } else {
-          m[g][0] = mp ? mp[off + k] : 0ull;
+          m[g][0] = mp ? *src : 0ull;
         }
       }
 #pragma unroll
@@ -730,15 +747,122 @@ __global__ void __launch_bounds__(256) k_mac_multi(MacMulti M, int nt, u32 nq, u
   }
 }
 
+__global__ void k_pack_masks(unsigned char* __restrict__ out, const u64* __restrict__ in, u32 nq, u32 logN) {
+  const u32 N = 1u << logN, r = blockIdx.y, m = blockIdx.z;
+  const size_t mbytes = (8 + 6 * (size_t)(nq - 1)) * N;
+  unsigned char* base = out + (size_t)m * mbytes;
+  const u64* src = in + ((size_t)m * nq + r) * N;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    const u64 v = src[k];
+    if (r == 0) {
+      reinterpret_cast<u64*>(base)[k] = v;
+    } else {
+      reinterpret_cast<unsigned*>(base + 8 * (size_t)N)[(size_t)(r - 1) * N + k] = (unsigned)v;
+      reinterpret_cast<unsigned short*>(base + 8 * (size_t)N + 4 * (size_t)(nq - 1) * N)[(size_t)(r - 1) * N + k] =
+          (unsigned short)(v >> 32);
+    }
+  }
+}
+
+__global__ void k_unpack_mask(u64* __restrict__ out, const unsigned char* __restrict__ in, u32 nq, u32 logN) {
+  const u32 N = 1u << logN, r = blockIdx.y;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    u64 v;
+    if (r == 0) {
+      v = reinterpret_cast<const u64*>(in)[k];
+    } else {
+      v = (u64)reinterpret_cast<const unsigned*>(in + 8 * (size_t)N)[(size_t)(r - 1) * N + k] |
+          ((u64)reinterpret_cast<const unsigned short*>(in + 8 * (size_t)N + 4 * (size_t)(nq - 1) * N)[(size_t)(r - 1) * N + k]
+           << 32);
+    }
+    out[(size_t)r * N + k] = v;
+  }
+}
+
+cudaError_t launch_pack_masks(unsigned char* out, const u64* in, u32 nm, u32 nq, u32 logN, cudaStream_t st) {
+  if (!nm || !nq) return cudaSuccess;
+  dim3 g = row_grid(1u << logN, nq, 256);
+  g.z = nm;
+  k_pack_masks<<<g, 256, 0, st>>>(out, in, nq, logN);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_mask(u64* out, const unsigned char* in, u32 nq, u32 logN, cudaStream_t st) {
+  k_unpack_mask<<<row_grid(1u << logN, nq, 256), 256, 0, st>>>(out, in, nq, logN);
+  return cudaGetLastError();
+}
+
+// One lane per (output g, coefficient pair): the 4 lanes of a pair sit in one
+// warp, so each ciphertext load is one broadcast transaction feeding all
+// outputs, while every lane keeps only its own 8 accumulator words (high
+// occupancy, many loads in flight).
+__global__ void __launch_bounds__(256) k_mac_multi_lanes(MacMulti M, int ng, int nt, u32 nq, u32 logN,
+                                                         int accumulate, const ModConsts* __restrict__ mc) {
+  const u32 N = 1u << logN, r = blockIdx.y;
+  const u32 g = threadIdx.x & 3u;
+  const u32 kp = blockIdx.x * (blockDim.x >> 2) + (threadIdx.x >> 2);  // coefficient pair
+  if (kp >= N / 2 || (int)g >= ng) return;
+  const u32 k = 2 * kp;
+  const u64 q = mc[r].q, ninv = mc[r].ninv;
+  const size_t pst = (size_t)nq * N, off = (size_t)r * N;
+  const size_t lo_off = 8 * (size_t)N + 4 * ((size_t)(r - 1) * N + k);
+  const size_t hi_off = 8 * (size_t)N + 4 * (size_t)(nq - 1) * N + 2 * ((size_t)(r - 1) * N + k);
+  u64 h00 = 0, l00 = 0, h01 = 0, l01 = 0, h10 = 0, l10 = 0, h11 = 0, l11 = 0;
+#pragma unroll 4
+  for (int t = 0; t < nt; ++t) {
+    const u64* mp = M.mask[g][t];
+    if (!mp) continue;
+    u64 m0, m1;
+    if (M.packed[g][t] && r > 0) {
+      const char* b = reinterpret_cast<const char*>(mp);
+      const uint2 l2 = *reinterpret_cast<const uint2*>(b + lo_off);
+      const unsigned h2 = *reinterpret_cast<const unsigned*>(b + hi_off);
+      m0 = (u64)l2.x | ((u64)(h2 & 0xffffu) << 32);
+      m1 = (u64)l2.y | ((u64)(h2 >> 16) << 32);
+    } else {
+      const ulonglong2 m2 = *reinterpret_cast<const ulonglong2*>(M.packed[g][t] ? mp + k : mp + off + k);
+      m0 = m2.x;
+      m1 = m2.y;
+    }
+    const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(M.ct[t] + off + k);
+    const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(M.ct[t] + pst + off + k);
+    mac128(h00, l00, x0.x, m0, q);
+    mac128(h01, l01, x0.y, m1, q);
+    mac128(h10, l10, x1.x, m0, q);
+    mac128(h11, l11, x1.y, m1, q);
+  }
+  u64* d0 = M.out[g] + off + k;
+  u64* d1 = M.out[g] + pst + off + k;
+  u64 y00 = redc128(h00, l00, q, ninv), y01 = redc128(h01, l01, q, ninv);
+  u64 y10 = redc128(h10, l10, q, ninv), y11 = redc128(h11, l11, q, ninv);
+  if (accumulate) {
+    const ulonglong2 o0 = *reinterpret_cast<const ulonglong2*>(d0);
+    const ulonglong2 o1 = *reinterpret_cast<const ulonglong2*>(d1);
+    y00 = add_mod(y00, o0.x, q);
+    y01 = add_mod(y01, o0.y, q);
+    y10 = add_mod(y10, o1.x, q);
+    y11 = add_mod(y11, o1.y, q);
+  }
+  *reinterpret_cast<ulonglong2*>(d0) = make_ulonglong2(y00, y01);
+  *reinterpret_cast<ulonglong2*>(d1) = make_ulonglong2(y10, y11);
+}
+
+int g_mac_lanes = 1;  // 1: k_mac_multi_lanes, 0: register-blocked k_mac_multi
+
 cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN, int accumulate,
                              const ModConsts* mc, cudaStream_t st) {
+  if (ng < 1 || ng > kMultiG) return cudaErrorInvalidValue;
+  if (g_mac_lanes) {
+    dim3 g((((1u << logN) / 2) + 63) / 64, nq, 1);
+    k_mac_multi_lanes<<<g, 256, 0, st>>>(M, ng, nt, nq, logN, accumulate, mc);
+    return cudaGetLastError();
+  }
   dim3 g2 = row_grid((1u << logN) / 2, nq, 256), g1 = row_grid(1u << logN, nq, 256);
   switch (ng) {
     case 1: k_mac_multi<1, 2><<<g2, 256, 0, st>>>(M, nt, nq, logN, accumulate, mc); break;
     case 2: k_mac_multi<2, 2><<<g2, 256, 0, st>>>(M, nt, nq, logN, accumulate, mc); break;
     case 3: k_mac_multi<3, 1><<<g1, 256, 0, st>>>(M, nt, nq, logN, accumulate, mc); break;
-    case 4: k_mac_multi<4, 1><<<g1, 256, 0, st>>>(M, nt, nq, logN, accumulate, mc); break;
-    default: return cudaErrorInvalidValue;
+    default: k_mac_multi<4, 1><<<g1, 256, 0, st>>>(M, nt, nq, logN, accumulate, mc); break;
   }
   return cudaGetLastError();
 }

@@ -29,6 +29,7 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
 // g_ks_batch (1, 2 or 4) entries (hcnn_set_option "ks_batch")
 extern int g_ks_batch;
 extern int g_mac_batch;
+extern int g_mac_lanes;
 // c0 (nullable): adds P * sigma_g(c0) on the Q limbs (pR[i] = P R mod q_i) --
 // the extended-basis (ModDown-free) rotation of double hoisting
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
@@ -85,7 +86,13 @@ struct MacMulti {
   const u64* ct[kMultiT];
   const u64* mask[kMultiG][kMultiT];
   u64* out[kMultiG];
+  unsigned char packed[kMultiG][kMultiT];  // 1: mask in the 48-bit packed layout (launch_pack_masks)
 };
+// 48-bit packed masks: limb 0 as u64 [N], limbs 1..nq-1 as u32 low words
+// [nq-1][N] then u16 high words [nq-1][N] -- (8 + 6 (nq-1)) N bytes, for
+// chains whose q_1..q_{nq-1} are < 2^48 (the application primes)
+cudaError_t launch_pack_masks(unsigned char* out, const u64* in, u32 nm, u32 nq, u32 logN, cudaStream_t st);
+cudaError_t launch_unpack_mask(u64* out, const unsigned char* in, u32 nq, u32 logN, cudaStream_t st);
 cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN, int accumulate,
                              const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_gather_limb(u64* out, const u64* in, u32 limb, u32 nlimbs, u32 logN, u32 npolys,

@@ -941,9 +941,38 @@ static int mac_terms_impl(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts
   return HCNN_OK;
 }
 
+static int masks_packable(const hcnn_ctx* c, u32 nq) {
+  for (u32 r = 1; r < nq; ++r)
+    if (c->mods[r] >> 48) return 0;
+  return 1;
+}
+
+int hcnn_pack_masks(hcnn_ctx* c, void* out, const uint64_t* in, uint32_t n_masks, uint32_t level, void* s) {
+  if (!c) return fail(HCNN_E_PARAMETER, "null context");
+  if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
+  if (!masks_packable(c, level + 1)) return fail(HCNN_E_BASIS, "a modulus above 2^48: masks not packable");
+  PK("pack_masks", (8.0 + 8.0 + 6.0 * level) * n_masks * c->n, 1, STREAM(s),
+     launch_pack_masks((unsigned char*)out, in, n_masks, level + 1, c->logN, STREAM(s)));
+  return HCNN_OK;
+}
+
+int hcnn_unpack_mask(hcnn_ctx* c, uint64_t* out, const void* in, uint32_t level, void* s) {
+  if (!c) return fail(HCNN_E_PARAMETER, "null context");
+  if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
+  PK("unpack_mask", (8.0 + 8.0 + 6.0 * level) * c->n, 1, STREAM(s),
+     launch_unpack_mask(out, (const unsigned char*)in, level + 1, c->logN, STREAM(s)));
+  return HCNN_OK;
+}
+
 int hcnn_mac_terms_multi(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* const* cts,
                          const uint64_t* const* masks, uint32_t n_out, uint32_t n_terms, uint32_t level, int accumulate,
                          void* s) {
+  return hcnn_mac_terms_multi_packed(c, outs, cts, masks, nullptr, n_out, n_terms, level, accumulate, s);
+}
+
+int hcnn_mac_terms_multi_packed(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* const* cts,
+                                const uint64_t* const* masks, const unsigned char* packed, uint32_t n_out,
+                                uint32_t n_terms, uint32_t level, int accumulate, void* s) {
   if (!c) return fail(HCNN_E_PARAMETER, "null context");
   if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
   const u32 nq = level + 1;
@@ -962,8 +991,10 @@ int hcnn_mac_terms_multi(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* con
       for (u32 g = 0; g < (u32)kMultiG; ++g) {
         M.out[g] = g < ng ? outs[g0 + g] : nullptr;
         for (u32 t = 0; t < nt; ++t) {
-          M.mask[g][t] = g < ng ? masks[(size_t)(g0 + g) * n_terms + t0 + t] : nullptr;
-          used += M.mask[g][t] ? 1 : 0;
+          const size_t idx = (size_t)(g0 + g) * n_terms + t0 + t;
+          M.mask[g][t] = g < ng ? masks[idx] : nullptr;
+          M.packed[g][t] = (g < ng && packed) ? packed[idx] : 0;
+          used += M.mask[g][t] ? (M.packed[g][t] ? 0.75 : 1.0) : 0.0;
         }
       }
       PK("mac_multi", 8.0 * (2.0 * nt + used + 2.0 * ng * (accumulate || t0 ? 2 : 1)) * nq * c->n, 1, STREAM(s),
@@ -1011,6 +1042,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_split") g_ntt_tuning.split = (int)value;
   else if (k == "ks_batch") g_ks_batch = (int)value;
   else if (k == "mac_batch") g_mac_batch = (int)value;
+  else if (k == "mac_lanes") g_mac_lanes = (int)value;
   else return fail(HCNN_E_PARAMETER, "unknown option " + k);
   return HCNN_OK;
 }

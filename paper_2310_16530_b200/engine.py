@@ -252,7 +252,8 @@ class DeviceContext:
     def mac_terms_multi(self, cts: Sequence[torch.Tensor], masks: Sequence[Sequence[torch.Tensor | None]],
                         level: int, outs: Sequence[torch.Tensor] | None = None,
                         accumulate: bool = False) -> list[torch.Tensor]:
-        """outs[g] (+)= sum_t cts[t] (.) masks[g][t] (None: no term), one ciphertext read per 4 outputs."""
+        """outs[g] (+)= sum_t cts[t] (.) masks[g][t] (None: no term), one ciphertext read per 4 outputs.
+        A mask may be an int64 [l+1, N] Montgomery row tensor or a uint8 packed mask (pack_masks)."""
         G, T = len(masks), len(cts)
         for c in cts:
             if not c.is_contiguous() or c.shape != (2, level + 1, self.n):
@@ -260,12 +261,34 @@ class DeviceContext:
         if outs is None:
             outs = [self.empty(2, level + 1, self.n) for _ in range(G)]
         P = ctypes.c_void_p
-        flat = [(m.data_ptr() if m is not None else None) for row in masks for m in row]
-        self._chk(self.lib.hcnn_mac_terms_multi(self.handle, (P * max(G, 1))(*[o.data_ptr() for o in outs]),
-                                                (P * max(T, 1))(*[c.data_ptr() for c in cts]),
-                                                (P * max(G * T, 1))(*flat), G, T, level, 1 if accumulate else 0,
-                                                _stream()))
+        flat = [m for row in masks for m in row]
+        ptrs = [(m.data_ptr() if m is not None else None) for m in flat]
+        packed = [1 if (m is not None and m.dtype == torch.uint8) else 0 for m in flat]
+        pk = (ctypes.c_ubyte * max(len(packed), 1))(*packed) if any(packed) else None
+        self._chk(self.lib.hcnn_mac_terms_multi_packed(self.handle, (P * max(G, 1))(*[o.data_ptr() for o in outs]),
+                                                       (P * max(T, 1))(*[c.data_ptr() for c in cts]),
+                                                       (P * max(G * T, 1))(*ptrs), pk, G, T, level,
+                                                       1 if accumulate else 0, _stream()))
         return list(outs)
+
+    def packed_mask_bytes(self, level: int) -> int:
+        return (8 + 6 * level) * self.n
+
+    def masks_packable(self, level: int) -> bool:
+        return all(q < (1 << 48) for q in self.q_list[1:level + 1])
+
+    def pack_masks(self, rows: torch.Tensor, level: int) -> torch.Tensor:
+        """Montgomery rows [k, l+1, N] -> uint8 [k, (8 + 6 l) N] (lossless 48-bit planes)."""
+        rows = rows.contiguous()
+        k = rows.numel() // ((level + 1) * self.n)
+        out = torch.empty(k, self.packed_mask_bytes(level), dtype=torch.uint8, device=self.torch_device)
+        self._chk(self.lib.hcnn_pack_masks(self.handle, _ptr(out), _ptr(rows), k, level, _stream()))
+        return out
+
+    def unpack_mask(self, packed: torch.Tensor, level: int) -> torch.Tensor:
+        out = self.empty(level + 1, self.n)
+        self._chk(self.lib.hcnn_unpack_mask(self.handle, _ptr(out), _ptr(packed), level, _stream()))
+        return out
 
     # -- extended basis Q_l||P (double-hoisted linear transforms) --------------
     def rotate_hoisted_ext(self, ct: torch.Tensor, level: int, galois: Sequence[int],

@@ -210,10 +210,18 @@ def test_mac_terms_multi_matches_per_output(small, cts):
     for G in (1, 2, 3, 4, 6):
         masks = [[mk() if (g + t) % 3 else None for t in range(len(srcs))] for g in range(G)]
         got = ctx.mac_terms_multi(srcs, masks, lvl)
+        # the same with every other mask in the 48-bit packed resident layout
+        assert ctx.masks_packable(lvl)
+        mixed = [[(ctx.pack_masks(m, lvl)[0] if (m is not None and (g + t) % 2) else m) for t, m in enumerate(row)]
+                 for g, row in enumerate(masks)]
+        got_p = ctx.mac_terms_multi(srcs, mixed, lvl)
         for g in range(G):
             terms = [(s, m) for s, m in zip(srcs, masks[g]) if m is not None]
             want = ctx.mac_terms([s for s, _ in terms], [m for _, m in terms], lvl)
             assert torch.equal(got[g], want)
+            assert torch.equal(got_p[g], want)
+    m = mk()
+    assert torch.equal(ctx.unpack_mask(ctx.pack_masks(m, lvl)[0], lvl), m)
 
 
 def test_truncated_rotation_keys(small, cts):
