@@ -207,7 +207,7 @@ def test_mac_terms_multi_matches_per_output(small, cts):
     srcs = [ct1.data, ct2.data] + [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl), ks,
                                                  rng).data for _ in range(3)]
     mk = lambda: ctx.unop("to_mont", ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl).data, lvl + 1)
-    for G in (1, 2, 3, 4, 6):
+    for G in (1, 2, 3, 4, 6, 9):
         masks = [[mk() if (g + t) % 3 else None for t in range(len(srcs))] for g in range(G)]
         got = ctx.mac_terms_multi(srcs, masks, lvl)
         # the same with every other mask in the 48-bit packed resident layout
