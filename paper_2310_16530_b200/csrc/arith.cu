@@ -847,11 +847,128 @@ __global__ void __launch_bounds__(256) k_mac_multi_lanes(MacMulti M, int ng, int
   *reinterpret_cast<ulonglong2*>(d1) = make_ulonglong2(y10, y11);
 }
 
+
+// ---------------------------------------------------------------------------
+// Shared-term MAC with a cp.async pipeline: a CTA owns a 256-coefficient
+// tile of one limb for up to 4 outputs; per term it stages the ciphertext
+// tile (2 polys) and the outputs' mask tiles (u64, or the 48-bit packed
+// planes) into shared memory kMacStages terms ahead, so HBM latency overlaps
+// the 8 mac128 per coefficient of the current term.
+// ---------------------------------------------------------------------------
+constexpr int kMacStages = 4;
+constexpr int kMacTile = 256;
+struct MacStage {
+  u64 ct[2][kMacTile];
+  u64 mask[kMultiG][kMacTile];  // unpacked rows, or lo u32 [256] + hi u16 [256] when packed
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void mac_stage_issue(MacStage& S, const MacMulti& M, int t, int ng, u32 r, u32 nq, u32 N,
+                                                u32 k0) {
+  const u32 tid = threadIdx.x;
+  const size_t off = (size_t)r * N + k0, pst = (size_t)nq * N;
+  // ciphertext: 2 polys x 2 KB = 256 chunks of 16 B
+  {
+    const u32 p = tid >> 7, c = tid & 127u;
+    cp_async16(&S.ct[p][2 * c], M.ct[t] + p * pst + off + 2 * c);
+  }
+  for (int g = 0; g < ng; ++g) {
+    const u64* mp = M.mask[g][t];
+    if (!mp) continue;
+    if (M.packed[g][t] && r > 0) {
+      const char* b = reinterpret_cast<const char*>(mp);
+      const char* lo = b + 8 * (size_t)N + 4 * ((size_t)(r - 1) * N + k0);
+      const char* hi = b + 8 * (size_t)N + 4 * (size_t)(nq - 1) * N + 2 * ((size_t)(r - 1) * N + k0);
+      char* dst = reinterpret_cast<char*>(S.mask[g]);
+      if (tid < 64) cp_async16(dst + 16 * tid, lo + 16 * tid);                       // 1 KB low words
+      else if (tid < 96) cp_async16(dst + 1024 + 16 * (tid - 64), hi + 16 * (tid - 64));  // 512 B high
+    } else {
+      const u64* src = M.packed[g][t] ? mp + k0 : mp + off;  // packed limb 0 is a plain u64 row
+      if (tid < 128) cp_async16(&S.mask[g][2 * tid], src + 2 * tid);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_mac_multi_async(MacMulti M, int ng, int nt, u32 nq, u32 logN,
+                                                         int accumulate, const ModConsts* __restrict__ mc) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MacStage* S = reinterpret_cast<MacStage*>(smem_raw);
+  const u32 N = 1u << logN, r = blockIdx.y, k0 = blockIdx.x * kMacTile, tid = threadIdx.x;
+  const u64 q = mc[r].q, ninv = mc[r].ninv;
+  for (int s = 0; s < kMacStages - 1; ++s) {
+    if (s < nt) mac_stage_issue(S[s], M, s, ng, r, nq, N, k0);
+    cp_async_commit();
+  }
+  u64 h[kMultiG][2], l[kMultiG][2];
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g) h[g][0] = h[g][1] = l[g][0] = l[g][1] = 0;
+  for (int t = 0; t < nt; ++t) {
+    cp_async_wait<kMacStages - 2>();
+    __syncthreads();
+    {  // refill the slot consumed last iteration
+      const int tn = t + kMacStages - 1;
+      if (tn < nt) mac_stage_issue(S[tn % kMacStages], M, tn, ng, r, nq, N, k0);
+      cp_async_commit();
+    }
+    const MacStage& C = S[t % kMacStages];
+    const u64 x0 = C.ct[0][tid], x1 = C.ct[1][tid];
+#pragma unroll
+    for (int g = 0; g < kMultiG; ++g) {
+      if (g >= ng || !M.mask[g][t]) continue;
+      u64 m;
+      if (M.packed[g][t] && r > 0) {
+        const unsigned* lo = reinterpret_cast<const unsigned*>(C.mask[g]);
+        const unsigned short* hi = reinterpret_cast<const unsigned short*>(
+            reinterpret_cast<const unsigned char*>(C.mask[g]) + 1024);
+        m = (u64)lo[tid] | ((u64)hi[tid] << 32);
+      } else {
+        m = C.mask[g][tid];
+      }
+      mac128(h[g][0], l[g][0], x0, m, q);
+      mac128(h[g][1], l[g][1], x1, m, q);
+    }
+  }
+  cp_async_wait<0>();
+  const size_t pst = (size_t)nq * N, off = (size_t)r * N + k0 + tid;
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g) {
+    if (g >= ng) break;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      u64* d = M.out[g] + p * pst + off;
+      u64 y = redc128(h[g][p], l[g][p], q, ninv);
+      if (accumulate) y = add_mod(y, *d, q);
+      *d = y;
+    }
+  }
+}
+
+int g_mac_async = 1;  // 1: cp.async pipeline (k_mac_multi_async), 0: k_mac_multi_lanes
+
 int g_mac_lanes = 1;  // 1: k_mac_multi_lanes, 0: register-blocked k_mac_multi
 
 cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN, int accumulate,
                              const ModConsts* mc, cudaStream_t st) {
   if (ng < 1 || ng > kMultiG) return cudaErrorInvalidValue;
+  if (g_mac_async && (1u << logN) % kMacTile == 0) {
+    static bool attr = false;
+    const size_t sm = sizeof(MacStage) * kMacStages;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_mac_multi_async, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e) return e;
+      attr = true;
+    }
+    dim3 g((1u << logN) / kMacTile, nq, 1);
+    k_mac_multi_async<<<g, 256, sm, st>>>(M, ng, nt, nq, logN, accumulate, mc);
+    return cudaGetLastError();
+  }
   if (g_mac_lanes) {
     dim3 g((((1u << logN) / 2) + 63) / 64, nq, 1);
     k_mac_multi_lanes<<<g, 256, 0, st>>>(M, ng, nt, nq, logN, accumulate, mc);

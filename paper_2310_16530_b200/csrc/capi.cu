@@ -1043,6 +1043,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ks_batch") g_ks_batch = (int)value;
   else if (k == "mac_batch") g_mac_batch = (int)value;
   else if (k == "mac_lanes") g_mac_lanes = (int)value;
+  else if (k == "mac_async") g_mac_async = (int)value;
   else return fail(HCNN_E_PARAMETER, "unknown option " + k);
   return HCNN_OK;
 }
