@@ -165,6 +165,10 @@ int hcnn_unpack_mask(hcnn_ctx* ctx, uint64_t* out, const void* in, uint32_t leve
  * kernel of the op covers the whole batch and each key / mask load feeds
  * several entries.  Entry-wise bit-exact with the single-ciphertext calls. */
 size_t hcnn_ks_workspace_bytes_batch(const hcnn_ctx* ctx, uint32_t level, uint32_t nb);
+/* workspace for hcnn_rotate_hoisted_batch with n_rot steps (all steps share
+ * one ModDown chain: ks inner products for every step, then one iNTT / FBC /
+ * NTT / combine launch each for the whole group) */
+size_t hcnn_ks_workspace_bytes_rot(const hcnn_ctx* ctx, uint32_t level, uint32_t nb, uint32_t n_rot);
 int hcnn_hmult_batch(hcnn_ctx* ctx, uint64_t* out_cts, const uint64_t* a_cts, const uint64_t* b_cts, uint32_t level,
                      uint32_t nb, const uint64_t* rlk_b, const uint64_t* rlk_a, void* ws, void* stream);
 /* outs[i]: batch buffer receiving rotation i of every entry.  key_lqs

@@ -64,6 +64,7 @@ SIGNATURES = {
     "hcnn_rotate_hoisted": (_INT, [_VP, ctypes.POINTER(_VP), _VP, _U32, _U32, _PU64,
                                    ctypes.POINTER(_VP), ctypes.POINTER(_VP), _VP, _VP]),
     "hcnn_ks_workspace_bytes_batch": (_SZ, [_VP, _U32, _U32]),
+    "hcnn_ks_workspace_bytes_rot": (_SZ, [_VP, _U32, _U32, _U32]),
     "hcnn_hmult_batch": (_INT, [_VP, _VP, _VP, _VP, _U32, _U32, _VP, _VP, _VP, _VP]),
     "hcnn_rotate_hoisted_batch": (_INT, [_VP, ctypes.POINTER(_VP), _VP, _U32, _U32, _U32, _PU64,
                                          ctypes.POINTER(_VP), ctypes.POINTER(_VP), _PU32, _VP, _VP]),

@@ -523,6 +523,49 @@ __global__ void __launch_bounds__(256) k_moddown_combine(u64* __restrict__ out0,
   }
 }
 
+// The same for the rotations of one hoisted group done together: acc / lift
+// hold [n_rot][nb][2][..]; z = (s*nb + b)*2 + p; each step s writes its own
+// output batch and gathers c0 with its own Galois element.
+__global__ void __launch_bounds__(256) k_moddown_combine_steps(ComboSteps S, const u64* __restrict__ acc,
+                                                               const u64* __restrict__ lift,
+                                                               const u64* __restrict__ add0, u32 nb, u32 nq,
+                                                               u32 n_ext, u32 logN, const u64* __restrict__ pinv,
+                                                               const u64* __restrict__ pinv_sh,
+                                                               const ModConsts* __restrict__ mc, size_t out_bst,
+                                                               size_t add_bst) {
+  const u32 N = 1u << logN, r = blockIdx.y, z = blockIdx.z, p = z & 1, sb = z >> 1, s = sb / nb, b = sb % nb;
+  const u64 q = mc[r].q;
+  const u64 w = pinv[r], wp = pinv_sh[r];
+  const u64 g_add = S.g[s];
+  const u64* A = acc + ((size_t)z * n_ext + r) * N;
+  const u64* L = lift + ((size_t)z * nq + r) * N;
+  const u64* ADD = (p == 0 && add0) ? add0 + (size_t)b * add_bst + (size_t)r * N : nullptr;
+  u64* O = S.out[s] + (size_t)b * out_bst + (size_t)p * nq * N + (size_t)r * N;
+  for (u32 k2 = blockIdx.x * blockDim.x + threadIdx.x; k2 < N / 2; k2 += gridDim.x * blockDim.x) {
+    const u32 k = 2 * k2;
+    const ulonglong2 av = *reinterpret_cast<const ulonglong2*>(A + k);
+    const ulonglong2 lv = *reinterpret_cast<const ulonglong2*>(L + k);
+    u64 v0 = shoup_mul(sub_mod(av.x, lv.x, q), w, wp, q);
+    u64 v1 = shoup_mul(sub_mod(av.y, lv.y, q), w, wp, q);
+    if (ADD) {
+      v0 = add_mod(v0, ADD[g_add == 1 ? k : galois_src(k, g_add, logN)], q);
+      v1 = add_mod(v1, ADD[g_add == 1 ? k + 1 : galois_src(k + 1, g_add, logN)], q);
+    }
+    *reinterpret_cast<ulonglong2*>(O + k) = make_ulonglong2(v0, v1);
+  }
+}
+
+cudaError_t launch_moddown_combine_steps(const ComboSteps& S, u32 n_rot, const u64* acc, const u64* lift,
+                                         const u64* add0, u32 nb, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
+                                         const u64* pinv_sh, const ModConsts* mc, size_t out_bst, size_t add_bst,
+                                         cudaStream_t st) {
+  dim3 g = row_grid((1u << logN) / 2, nq, 256);
+  g.z = 2 * nb * n_rot;
+  k_moddown_combine_steps<<<g, 256, 0, st>>>(S, acc, lift, add0, nb, nq, n_ext, logN, pinv, pinv_sh, mc, out_bst,
+                                             add_bst);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // plane MAC of the HyPHEN conv (packing.py:600-604 / :520-525):
 // out_z = sum_t ct_t,z (.) mask_t over up to kMacMax terms, masks in

@@ -46,6 +46,15 @@ cudaError_t launch_rescale_lift(u64* out, const u64* top, u32 l, u32 logN, u32 n
                                 const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_rescale_combine(u64* out, const u64* in, u32 l, u32 logN, u32 npolys, const u64* inv,
                                    const u64* inv_sh, const ModConsts* mc, cudaStream_t st);
+constexpr int kComboMax = 32;
+struct ComboSteps {
+  u64* out[kComboMax];
+  u64 g[kComboMax];
+};
+cudaError_t launch_moddown_combine_steps(const ComboSteps& S, u32 n_rot, const u64* acc, const u64* lift,
+                                         const u64* add0, u32 nb, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
+                                         const u64* pinv_sh, const ModConsts* mc, size_t out_bst, size_t add_bst,
+                                         cudaStream_t st);
 constexpr int kScalarMax = 128;
 struct ScalarArgs {
   u64 w[kScalarMax];

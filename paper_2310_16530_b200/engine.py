@@ -235,7 +235,7 @@ class DeviceContext:
         outs = [torch.empty_like(ct) for _ in range(n_rot)]
         if n_rot == 0:
             return outs
-        ws = self.ks_workspace(level, nb)
+        ws = self.empty(int(self.lib.hcnn_ks_workspace_bytes_rot(self.handle, level, nb, n_rot)) // 8)
         P = ctypes.c_void_p * n_rot
         outs_p = P(*[o.data_ptr() for o in outs])
         kb = P(*[k[0].data_ptr() for k in keys])
