@@ -123,6 +123,11 @@ def load() -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        # tuning knobs from the environment: HCNN_OPTIONS="ntt_occupancy=1,merge_moddown=0"
+        for item in filter(None, os.environ.get("HCNN_OPTIONS", "").split(",")):
+            key, _, val = item.partition("=")
+            if lib.hcnn_set_option(key.strip().encode(), int(val or 1)) != 0:
+                raise NativeError(f"unknown HCNN_OPTIONS entry {item!r}")
         _lib = lib
         return lib
 
