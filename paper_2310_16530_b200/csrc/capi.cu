@@ -709,14 +709,26 @@ size_t hcnn_ks_workspace_bytes_batch(const hcnn_ctx* c, uint32_t level, uint32_t
   return hcnn_ks_workspace_bytes(c, level) * (nb ? nb : 1);
 }
 
-// hoisted rotation groups finish all steps together: acc / lift for n_rot steps
-size_t hcnn_ks_workspace_bytes_rot(const hcnn_ctx* c, uint32_t level, uint32_t nb, uint32_t n_rot) {
+int g_merge_moddown = 1;  // rotations of a hoisted group share one ModDown chain
+
+// steps of a hoisted group that share one ModDown chain: bounded so the
+// extra acc/lift workspace stays under 1 GiB
+static u32 merge_chunk(const hcnn_ctx* c, u32 level, u32 nb, u32 n_rot) {
+  if (!g_merge_moddown || n_rot < 2) return 1;
   const u32 nq = level + 1, n_ext = nq + c->K;
-  const size_t extra = (size_t)(n_rot > 1 ? n_rot - 1 : 0) * (nb ? nb : 1) * (2 * (size_t)n_ext + 2 * (size_t)nq);
-  return hcnn_ks_workspace_bytes_batch(c, level, nb) + extra * c->n * 8;
+  const size_t per_step = (size_t)(nb ? nb : 1) * (2 * (size_t)n_ext + 2 * (size_t)nq) * c->n * 8;
+  size_t chunk = (1ull << 30) / (per_step ? per_step : 1);
+  if (chunk > n_rot) chunk = n_rot;
+  if (chunk > (size_t)kComboMax) chunk = kComboMax;
+  return chunk < 1 ? 1 : (u32)chunk;
 }
 
-int g_merge_moddown = 1;  // rotations of a hoisted group share one ModDown chain
+// hoisted rotation groups finish chunks of steps together: acc / lift for merge_chunk steps
+size_t hcnn_ks_workspace_bytes_rot(const hcnn_ctx* c, uint32_t level, uint32_t nb, uint32_t n_rot) {
+  const u32 nq = level + 1, n_ext = nq + c->K, ch = merge_chunk(c, level, nb, n_rot);
+  const size_t extra = (size_t)(ch - 1) * (nb ? nb : 1) * (2 * (size_t)n_ext + 2 * (size_t)nq);
+  return hcnn_ks_workspace_bytes_batch(c, level, nb) + extra * c->n * 8;
+}
 
 // ModUp of nb polys (entry b at x_eval + b*x_bst): iNTT a copy, convert
 // every digit to Q_l||P, NTT the new limbs -- one launch per step for the batch
@@ -850,12 +862,12 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
     if ((galois[i] % (2ull * c->n) & 1) == 0) return fail(HCNN_E_PARAMETER, "galois element must be odd");
   rc = key_lq_ok(c, key_lqs, n_rot, level);
   if (rc) return rc;
-  const bool merged = g_merge_moddown && n_rot > 1 && n_rot <= (u32)kComboMax;
-  KsWs w = ks_layout(c, level, ws, nb, merged ? n_rot : 1);
+  const u32 chunk = merge_chunk(c, level, nb, n_rot);
+  KsWs w = ks_layout(c, level, ws, nb, chunk);
   const u64* c1 = cts + nq * N;
   rc = ks_modup(c, level, c1, w, STREAM(s), nb, ct);
   if (rc) return rc;
-  if (!merged) {
+  if (chunk < 2) {
     for (u32 i = 0; i < n_rot; ++i) {
       u64 g = galois[i] % (2ull * c->n);
       rc = ks_finish(c, level, c1, w, g, kbs[i], kas[i], outs[i], outs[i] + nq * N, cts, nullptr, g, STREAM(s), nb,
@@ -864,36 +876,42 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
     }
     return HCNN_OK;
   }
-  // inner products of every step into acc[step], then one ModDown chain for all
+  // per chunk: inner products of every step into acc[step], then one ModDown chain
   const u32 n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
   const size_t a_step = (size_t)nb * 2 * n_ext * N;
-  ComboSteps S;
-  for (u32 i = 0; i < n_rot; ++i) {
-    const u64 g = galois[i] % (2ull * c->n);
-    S.out[i] = outs[i];
-    S.g[i] = g;
-    PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
-       launch_ks_inner(w.acc + i * a_step, c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd, c->logN,
-                       g, c->d_mc, STREAM(s), nb, ct, nullptr, 0, nullptr, key_lqs ? key_lqs[i] : 0));
+  for (u32 i0 = 0; i0 < n_rot; i0 += chunk) {
+    const u32 nr = n_rot - i0 < chunk ? n_rot - i0 : chunk;
+    ComboSteps S;
+    for (u32 j = 0; j < nr; ++j) {
+      const u32 i = i0 + j;
+      const u64 g = galois[i] % (2ull * c->n);
+      S.out[j] = outs[i];
+      S.g[j] = g;
+      PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
+         launch_ks_inner(w.acc + j * a_step, c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd,
+                         c->logN, g, c->d_mc, STREAM(s), nb, ct, nullptr, 0, nullptr, key_lqs ? key_lqs[i] : 0));
+    }
+    const u32 np = 2 * nb * nr;
+    LimbMap m{};
+    m.base = w.acc + nq * N;
+    m.poly_stride = (size_t)n_ext * N;
+    m.basis = c->basis(nq, c->K);
+    m.first_limb = nq;
+    PK("ntt_inv_moddown", 16.0 * np * c->K * N, ntt_nk(c), STREAM(s),
+       launch_ntt(c->tables(), m, c->K, np, true, STREAM(s)));
+    PK("moddown_fbc", 8.0 * np * (c->K + nq) * N, 1, STREAM(s),
+       launch_fbc(c->moddown.dev, c->moddown.d_dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N,
+                  c->logN, np, nq, STREAM(s)));
+    LimbMap l{};
+    l.base = w.lift;
+    l.poly_stride = nq * N;
+    l.basis = c->basis(nq, 0);
+    PK("ntt_fwd_moddown", 16.0 * np * nq * N, ntt_nk(c), STREAM(s),
+       launch_ntt(c->tables(), l, nq, np, false, STREAM(s)));
+    PK("moddown_combine", 8.0 * np * 4 * nq * N, 1, STREAM(s),
+       launch_moddown_combine_steps(S, nr, w.acc, w.lift, cts, nb, nq, n_ext, c->logN, c->d_pinv, c->d_pinv_sh,
+                                    c->d_mc, ct, ct, STREAM(s)));
   }
-  const u32 np = 2 * nb * n_rot;
-  LimbMap m{};
-  m.base = w.acc + nq * N;
-  m.poly_stride = (size_t)n_ext * N;
-  m.basis = c->basis(nq, c->K);
-  m.first_limb = nq;
-  PK("ntt_inv_moddown", 16.0 * np * c->K * N, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), m, c->K, np, true, STREAM(s)));
-  PK("moddown_fbc", 8.0 * np * (c->K + nq) * N, 1, STREAM(s),
-     launch_fbc(c->moddown.dev, c->moddown.d_dev, c->d_mc, w.acc + nq * N, (size_t)n_ext * N, w.lift, nq * N,
-                c->logN, np, nq, STREAM(s)));
-  LimbMap l{};
-  l.base = w.lift;
-  l.poly_stride = nq * N;
-  l.basis = c->basis(nq, 0);
-  PK("ntt_fwd_moddown", 16.0 * np * nq * N, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), l, nq, np, false, STREAM(s)));
-  PK("moddown_combine", 8.0 * np * 4 * nq * N, 1, STREAM(s),
-     launch_moddown_combine_steps(S, n_rot, w.acc, w.lift, cts, nb, nq, n_ext, c->logN, c->d_pinv, c->d_pinv_sh,
-                                  c->d_mc, ct, ct, STREAM(s)));
   return HCNN_OK;
 }
 

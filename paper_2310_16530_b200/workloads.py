@@ -23,18 +23,30 @@ class ResNet20Setup:
     ks: ckks.KeySet
 
 
-def resnet20_setup(app_levels: int = 14, seed: int = 3, key_seed: int = 20) -> ResNet20Setup:
+def resnet20_boot_config(stc_stages=None) -> bt.BootConfig:
+    """Bootstrapping configuration of the ResNet20 workload (HCNN_STC env: e.g. "8,7")."""
+    import os
+    env = os.environ.get("HCNN_STC")
+    if stc_stages is None and env:
+        stc_stages = tuple(int(v) for v in env.split(","))
+    return bt.BootConfig() if stc_stages is None else bt.BootConfig(stc_stages=tuple(stc_stages))
+
+
+def resnet20_setup(app_levels: int | None = None, seed: int = 3, key_seed: int = 20) -> ResNet20Setup:
     """BASELINE config 4: AESPA-ResNet20 (CIFAR-10 shape 3x32x32), HyPHEN
     packing with multiplex 4 at N=2^16 (r >= m for FormatB, packing.py:489),
     bootstrappable chain with `app_levels` computation levels, real CKKS
     bootstrapping at the snapshot-aware planner's refresh points."""
     packing.set_mask_mode("compact")
-    cfg = bt.BootConfig()
+    cfg = resnet20_boot_config()
+    if app_levels is None:  # keep the chain length (logQP) fixed: StC levels trade for application levels
+        app_levels = 17 - len(cfg.stc_stages)
     params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg)
     boot = bt.Bootstrapper(params, cfg)
     fx = graph.gen_fixture("resnet20", seed, params, golden_count=1)
     g = graph.build_graph("resnet20", fx, multiplex=4)
-    plan = graph.plan_levels(g, boot.output_level, refresh_target=boot.output_level, count_snapshots=True)
+    plan = graph.plan_levels(g, boot.output_level, refresh_target=boot.output_level,
+                             refresh_cost=graph.refresh_bootstraps(g, params.slots))
     steps = graph.required_rotation_steps(g, params.slots) | graph.refresh_rotation_steps(g, plan, params.slots)
     ks = boot.keygen(np.random.default_rng(key_seed), rotations=sorted(steps))
     # keys used only at application levels keep their low-level rows (HBM for resident masks)
@@ -62,12 +74,55 @@ RESNET20_TALLY = {"rotations": 1964, "hmults": 172, "pmults": 44464, "hadds": 44
                   "refreshes": 32}
 
 
-def resnet20_plan_only(app_levels: int = 14, seed: int = 3):
+def resnet20_plan_only(app_levels: int | None = None, seed: int = 3):
     """Host-only part of resnet20_setup (params, graph, plan; no keys/GPU)."""
-    cfg = bt.BootConfig()
+    cfg = resnet20_boot_config()
+    if app_levels is None:
+        app_levels = 17 - len(cfg.stc_stages)
     params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg)
     fx = graph.gen_fixture("resnet20", seed, params, golden_count=1)
     g = graph.build_graph("resnet20", fx, multiplex=4)
     out_level = params.max_level - cfg.depth()
-    plan = graph.plan_levels(g, out_level, refresh_target=out_level, count_snapshots=True)
+    plan = graph.plan_levels(g, out_level, refresh_target=out_level, refresh_cost=graph.refresh_bootstraps(g, params.slots))
     return params, g, plan
+
+
+def warm_up(s: ResNet20Setup, ct: packing.PackedTensor, cache: dict) -> dict:
+    """First two eager inferences of a workload, sizing mask residency from
+    measurement instead of a guess: run 1 builds every mask (compact, none
+    resident) and measures the largest transient working set of any layer
+    W (peak minus the layer's starting footprint); run 2 keeps masks
+    resident while 1.5 W + 3 GiB stays free -- room for the CUDA-graph
+    capture (graph.CapturedInference) and the live activations."""
+    import time
+    import torch
+    packing.set_residency(False)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    marks: dict = {}
+    work = [0]
+
+    def hook(i, phase):
+        torch.cuda.synchronize()
+        if phase == "start":
+            marks["start"] = torch.cuda.memory_allocated()
+            torch.cuda.reset_peak_memory_stats()
+        else:  # transient only: compact masks created by the layer persist and are not working set
+            end = torch.cuda.memory_allocated()
+            work[0] = max(work[0], torch.cuda.max_memory_allocated() - max(marks["start"], end))
+
+    t0 = time.time()
+    graph.execute(s.graph, s.plan, ct, s.ks, "encrypted", cache=cache, layer_hook=hook)
+    torch.cuda.synchronize()
+    t_build = time.time() - t0
+    after = torch.cuda.memory_allocated()
+    reserve = int(1.5 * work[0]) + (3 << 30)
+    torch.cuda.empty_cache()
+    packing.set_residency(True, reserve)
+    t0 = time.time()
+    graph.execute(s.graph, s.plan, ct, s.ks, "encrypted", cache=cache)
+    torch.cuda.synchronize()
+    return {"first_image_s": round(t_build, 2), "residency_fill_s": round(time.time() - t0, 2),
+            "layer_working_set_gb": round(work[0] / 2 ** 30, 2),
+            "persistent_growth_gb": round((after - base) / 2 ** 30, 2),
+            "reserve_gb": round(reserve / 2 ** 30, 2), "resident_mask_gb": round(packing.resident_bytes() / 2 ** 30, 1)}
