@@ -192,6 +192,39 @@ def roofline_from_profile(prof: dict) -> tuple[dict, dict]:
     return roof, kernels
 
 
+def int_roofline(roof: dict, prof: dict, limbs: dict, n: int) -> dict:
+    """The NTT family is integer-pipe bound: its roofline is the
+    butterfly rate of the same radix-16 register network with no memory
+    traffic (hcnn_ntt_butterfly_peak, measured here on this GPU, per modulus
+    class).  ideal = sum over limbs of N/2 log2 N / peak(class); frac =
+    ideal / measured device time of the family.  The HBM view is kept under
+    "hbm"."""
+    from paper_2310_16530_b200 import _native
+    fam = roof["kernel"]
+    if fam not in ("ntt_fwd", "ntt_inv"):
+        return roof
+    d = "fwd" if fam == "ntt_fwd" else "inv"
+    fast, full = limbs[f"{d}_fast"], limbs[f"{d}_full"]
+    ms = sum(v["ms"] for k, v in prof.items() if _kernel_family(k) == fam)
+    if fast + full == 0 or ms <= 0:
+        return roof
+    pf, ps = _native.ntt_butterfly_peak(True), _native.ntt_butterfly_peak(False)
+    per_limb = n // 2 * (n.bit_length() - 1)
+    ideal_s = per_limb * (fast / pf + full / ps)
+    bfly = per_limb * (fast + full)
+    achieved = bfly / (ms / 1e3)
+    peak = bfly / ideal_s
+    hbm = {k: roof[k] for k in ("achieved", "peak", "unit", "frac", "peak_source", "algorithmic_bytes_per_launch")}
+    out = {"kernel": fam, "bound": "int", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
+           "unit": "Gbutterfly/s", "frac": round(ideal_s / (ms / 1e3), 4), "traffic": roof.get("traffic"),
+           "peak_source": (f"measured on this GPU: radix-16 register network without memory traffic "
+                           f"(hcnn_ntt_butterfly_peak) {pf/1e9:.1f} Gbfly/s for q<2^47 limbs, {ps/1e9:.1f} for "
+                           f"full-width limbs, weighted by this image's {fast} + {full} limbs"),
+           "limbs": {"fast": fast, "full": full}, "share_of_device_time": roof["share_of_device_time"],
+           "hbm": hbm}
+    return out
+
+
 def peak_kind_note(kind: str) -> str:
     return f"{kind} (MEASURED_PEAKS.json hbm_gbs)" if kind == "measured" else "fallback 6650 GB/s"
 
@@ -284,13 +317,16 @@ def run_resnet20(args, d: Dist):
     warm = workloads.warm_up(s, imgs[0], cache)
     k0 = _native.kernel_launches()
     _native.profile_read(reset=True)
+    _native.ntt_limb_counts(reset=True)
     _native.profile_enable(True)
     graph.execute(s.graph, s.plan, imgs[1], s.ks, "encrypted", cache=cache)
     torch.cuda.synchronize()
     _native.profile_enable(False)
     prof = _native.profile_read(reset=True)
+    limbs = _native.ntt_limb_counts(reset=True)
     launches = _native.kernel_launches() - k0
     roofline, kernels = roofline_from_profile(prof)
+    roofline = int_roofline(roofline, prof, limbs, s.params.n)
     runner = graph.CapturedInference(s.graph, s.plan, s.ks, imgs[0], cache, warmup=False)
     tally = runner.report.totals().as_dict()
 
@@ -348,7 +384,9 @@ def run_resnet20(args, d: Dist):
                        "input": "3x32x32 U(-1,1), encrypted", "ring_n": s.params.n, "slots": s.params.slots,
                        "multiplex": 4, "q_limbs": len(s.params.q_mods), "special_limbs": len(s.params.p_mods),
                        "app_levels": s.boot.output_level, "bootstrap_depth": s.cfg.depth(),
-                       "refresh_points": list(s.plan.refresh_points), "bootstraps_per_image": tally["refreshes"],
+                       "refresh_points": list(s.plan.refresh_points), "refreshed_ciphertexts_per_image": tally["refreshes"],
+                       "bootstraps_per_image": sum(graph.refresh_bootstraps(s.graph, s.params.slots)[i]
+                                                   for i in s.plan.refresh_points),
                        "images_per_step_per_gpu": 1, "parallelism": f"dp{d.world} (independent images per GPU)",
                        "cuda_graph": True,
                        "resident_mask_gb": round(packing.resident_bytes() / 2 ** 30, 1),
@@ -393,11 +431,14 @@ def run_cfg2(args, d: Dist):
     clocks = sampler.stop()
     value = d.world * B * args.steps / (ms / 1e3)
     _native.profile_read(reset=True)
+    _native.ntt_limb_counts(reset=True)
     _native.profile_enable(True)
     step()
     torch.cuda.synchronize()
     _native.profile_enable(False)
-    roofline, kernels = roofline_from_profile(_native.profile_read(reset=True))
+    prof = _native.profile_read(reset=True)
+    roofline, kernels = roofline_from_profile(prof)
+    roofline = int_roofline(roofline, prof, _native.ntt_limb_counts(reset=True), params.n)
     if d.rank == 0:
         print(json.dumps({
             "metric": "HMult+relin+rescale+HRot primitive sets/s at N=2^16, L=24, K=4, dnum=7 (BASELINE cfg 2)",

@@ -229,6 +229,14 @@ int hcnn_scalar_mac(hcnn_ctx* ctx, uint64_t* out, const uint64_t* const* srcs, c
 /* ---- instrumentation ------------------------------------------------------ */
 /* count of engine kernels launched since load (all contexts) */
 unsigned long long hcnn_kernel_launches(void);
+/* Integer-pipe ceiling of the NTT: butterflies/s of the radix-16 register
+ * network run on register-resident data (no memory traffic) on `device`;
+ * fast = 1 times the unreduced q < 2^47 network.  No reference counterpart
+ * (roofline denominator for bench.py). */
+int hcnn_ntt_butterfly_peak(int device, int fast, double* bfly_per_s);
+/* limbs transformed since the last reset, by class:
+ * [forward q<2^47, forward full, inverse q<2^47, inverse full] */
+void hcnn_ntt_limb_counts(unsigned long long* out4, int reset);
 /* process-wide tuning knobs: "ntt_group_limbs" (NTT pass pairs run on groups
  * of this many limbs so the inter-pass data stays in L2; 0 = whole batch),
  * "ntt_hints" (1 = evict-last twiddles / streaming data loads) */

@@ -88,6 +88,8 @@ SIGNATURES = {
     "hcnn_mac_terms": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _U32, _U32, _INT, _VP]),
     "hcnn_kernel_launches": (ctypes.c_ulonglong, []),
     "hcnn_profile_enable": (None, [_INT]),
+    "hcnn_ntt_butterfly_peak": (_INT, [_INT, _INT, ctypes.POINTER(ctypes.c_double)]),
+    "hcnn_ntt_limb_counts": (None, [ctypes.POINTER(ctypes.c_ulonglong), _INT]),
     "hcnn_set_option": (_INT, [ctypes.c_char_p, ctypes.c_longlong]),
     "hcnn_profile_read": (_INT, [ctypes.c_char_p, _SZ, _INT]),
 }
@@ -142,6 +144,20 @@ def check(rc: int) -> None:
 
 def kernel_launches() -> int:
     return int(load().hcnn_kernel_launches())
+
+
+def ntt_butterfly_peak(fast: bool, device: int = 0) -> float:
+    """Measured butterflies/s of the NTT's register network (integer-pipe ceiling)."""
+    out = ctypes.c_double(0.0)
+    check(load().hcnn_ntt_butterfly_peak(int(device), 1 if fast else 0, ctypes.byref(out)))
+    return float(out.value)
+
+
+def ntt_limb_counts(reset: bool = True) -> dict:
+    """Limbs transformed since the last reset: fwd/inv x (q < 2^47 fast path, full)."""
+    buf = (ctypes.c_ulonglong * 4)()
+    load().hcnn_ntt_limb_counts(buf, 1 if reset else 0)
+    return {"fwd_fast": buf[0], "fwd_full": buf[1], "inv_fast": buf[2], "inv_full": buf[3]}
 
 
 def set_option(name: str, value: int) -> None:

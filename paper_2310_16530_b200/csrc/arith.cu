@@ -485,6 +485,78 @@ __global__ void __launch_bounds__(256, NB == 1 ? 4 : 1) k_ks_inner(u64* __restri
   }
 }
 
+// Software-pipelined form of k_ks_inner<1,2> for the single-poly-per-thread
+// case: the key / digit loads of JB digits are issued before any of their
+// MACs (more bytes in flight per SM: the kernel is HBM-latency bound), and
+// the Galois source index is computed once per coefficient instead of once
+// per digit.  Same sums, same single REDC: bit-identical outputs.
+int g_ks_pipe = 2;  // digits per load batch (0: k_ks_inner<1,2>)
+
+template <int JB>
+__global__ void __launch_bounds__(256, JB >= 4 ? 2 : 3) k_ks_inner_p(
+    u64* __restrict__ acc, const u64* __restrict__ x_eval, const u64* __restrict__ raised,
+    const u64* __restrict__ key_b, const u64* __restrict__ key_a, Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g,
+    const ModConsts* __restrict__ mc, u32 nb, size_t x_bst, const u64* __restrict__ c0, size_t c0_bst,
+    const u64* __restrict__ pR, u32 key_lq) {
+  const u32 N = 1u << logN, r = blockIdx.y;
+  const u32 n_ext = basis.nlimbs();
+  const u32 mod = basis.mod_of(r);
+  const u64 q = mc[mod].q, ninv = mc[mod].ninv;
+  const u32 klq = key_lq ? key_lq : basis.Lq;
+  const size_t key_dst = (size_t)(klq + basis.np) * N;
+  const u32 kmod = mod < basis.Lq ? mod : klq + (mod - basis.Lq);
+  const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;
+  const u32 b = blockIdx.x % nb, x0 = blockIdx.x / nb, xs = gridDim.x / nb;
+  const u64* xsrc = x_eval + (size_t)b * x_bst + (size_t)r * N;
+  const u64* rsrc = raised + (size_t)b * ndig * n_ext * N + (size_t)r * N;
+  const u64* kb_base = key_b + (size_t)kmod * N;
+  const u64* ka_base = key_a + (size_t)kmod * N;
+  for (u32 kv = x0 * blockDim.x + threadIdx.x; kv < N / 2; kv += xs * blockDim.x) {
+    const u32 k = 2 * kv;
+    const u32 p0 = g == 1 ? k : galois_src(k, g, logN), p1 = g == 1 ? k + 1 : galois_src(k + 1, g, logN);
+    u64 bh0 = 0, bl0 = 0, bh1 = 0, bl1 = 0, ah0 = 0, al0 = 0, ah1 = 0, al1 = 0;
+    for (u32 j0 = 0; j0 < ndig; j0 += JB) {
+      ulonglong2 KB[JB], KA[JB], X[JB];
+#pragma unroll
+      for (int i = 0; i < JB; ++i) {
+        const u32 j = j0 + i;
+        if (j < ndig) {
+          const size_t kofs = (size_t)j * key_dst + k;
+          KB[i] = *reinterpret_cast<const ulonglong2*>(kb_base + kofs);
+          KA[i] = *reinterpret_cast<const ulonglong2*>(ka_base + kofs);
+          const u64* src = j == own ? xsrc : rsrc + (size_t)j * n_ext * N;
+          if (g == 1) {
+            X[i] = *reinterpret_cast<const ulonglong2*>(src + k);
+          } else {
+            X[i].x = src[p0];
+            X[i].y = src[p1];
+          }
+        } else {
+          KB[i] = KA[i] = X[i] = make_ulonglong2(0, 0);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < JB; ++i) {
+        mac128(bh0, bl0, X[i].x, KB[i].x, q);
+        mac128(ah0, al0, X[i].x, KA[i].x, q);
+        mac128(bh1, bl1, X[i].y, KB[i].y, q);
+        mac128(ah1, al1, X[i].y, KA[i].y, q);
+      }
+    }
+    if (c0 && r < basis.nq) {  // extended-basis output: + P * sigma_g(c0) on the Q limbs
+      const u64 w = pR[r];
+      const u64* src = c0 + (size_t)b * c0_bst + (size_t)r * N;
+      mac128(bh0, bl0, src[p0], w, q);
+      mac128(bh1, bl1, src[p1], w, q);
+    }
+    u64* A = acc + (size_t)b * 2 * n_ext * N;
+    *reinterpret_cast<ulonglong2*>(A + (size_t)r * N + k) =
+        make_ulonglong2(redc128(bh0, bl0, q, ninv), redc128(bh1, bl1, q, ninv));
+    *reinterpret_cast<ulonglong2*>(A + ((size_t)n_ext + r) * N + k) =
+        make_ulonglong2(redc128(ah0, al0, q, ninv), redc128(ah1, al1, q, ninv));
+  }
+}
+
 // ModDown combine (ckks.py:593-601): out_z[r] = add_z[perm(k)] + (acc_z[r] - lift_z[r]) * P^-1
 __global__ void __launch_bounds__(256) k_moddown_combine(u64* __restrict__ out0, u64* __restrict__ out1,
                                                          const u64* __restrict__ acc, const u64* __restrict__ lift,
@@ -1160,7 +1232,19 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
                             cudaStream_t st, u32 nb, size_t x_bst, const u64* c0, size_t c0_bst, const u64* pR,
                             u32 key_lq) {
-  if (nb <= 1 || g_ks_batch <= 1) {
+  if ((nb <= 1 || g_ks_batch <= 1) && g_ks_pipe > 0) {
+    dim3 grid = row_grid((1u << logN) / 2, basis.nlimbs(), 256);
+    grid.x *= (nb ? nb : 1);
+    if (g_ks_pipe >= 4)
+      k_ks_inner_p<4><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,
+                                            nb ? nb : 1, x_bst, c0, c0_bst, pR, key_lq);
+    else if (g_ks_pipe == 3)
+      k_ks_inner_p<3><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,
+                                            nb ? nb : 1, x_bst, c0, c0_bst, pR, key_lq);
+    else
+      k_ks_inner_p<2><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,
+                                            nb ? nb : 1, x_bst, c0, c0_bst, pR, key_lq);
+  } else if (nb <= 1 || g_ks_batch <= 1) {
     dim3 grid = row_grid((1u << logN) / 2, basis.nlimbs(), 256);
     grid.x *= (nb ? nb : 1);
     k_ks_inner<1, 2><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,

@@ -1102,6 +1102,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_occupancy") g_ntt_tuning.occupancy = (int)value;
   else if (k == "ntt_split") g_ntt_tuning.split = (int)value;
   else if (k == "ks_batch") g_ks_batch = (int)value;
+  else if (k == "ks_pipe") g_ks_pipe = (int)value;
   else if (k == "mac_batch") g_mac_batch = (int)value;
   else if (k == "mac_lanes") g_mac_lanes = (int)value;
   else if (k == "mac_async") g_mac_async = (int)value;
@@ -1111,6 +1112,20 @@ int hcnn_set_option(const char* name, long long value) {
 }
 
 unsigned long long hcnn_kernel_launches(void) { return g_kernels.load(); }
+
+int hcnn_ntt_butterfly_peak(int device, int fast, double* bfly_per_s) {
+  if (!bfly_per_s) return fail(HCNN_E_PARAMETER, "null output");
+  CK(cudaSetDevice(device));
+  CK((cudaError_t)ntt_butterfly_peak(fast, bfly_per_s));
+  return HCNN_OK;
+}
+
+void hcnn_ntt_limb_counts(unsigned long long* out4, int reset) {
+  for (int i = 0; i < 4; ++i) {
+    if (out4) out4[i] = g_ntt_limbs[i];
+    if (reset) g_ntt_limbs[i] = 0;
+  }
+}
 
 // Drain pending event pairs into per-name totals and render them as JSON:
 // {"name": [launches, total_ms, algorithmic_bytes, kernels], ...}

@@ -50,6 +50,8 @@ cudaError_t launch_ntt(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 n
                        cudaStream_t st);
 cudaError_t ntt_configure_smem();
 bool ntt2_supported(u32 logN);
+int ntt_butterfly_peak(int fast, double* bfly_per_s);
+extern unsigned long long g_ntt_limbs[4];
 cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 npolys, bool inverse,
                         cudaStream_t st);
 

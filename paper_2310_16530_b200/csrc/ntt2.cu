@@ -412,6 +412,89 @@ __global__ void __launch_bounds__(128, MINB) ntt2_inv_chunks(LimbMap map, const 
 }
 
 // ---------------------------------------------------------------------------
+// Integer-pipe ceiling of the NTT: the same radix-16 register network
+// (ct16, 32 butterflies per call, approximate-Shoup products) iterated on
+// register-resident data with register twiddles -- no memory traffic, no
+// shuffles.  Its butterfly rate is the roofline denominator of the NTT
+// kernels ("int" bound, bench.py), measured on the box like the HBM peak.
+// ---------------------------------------------------------------------------
+template <bool FAST>
+__global__ void __launch_bounds__(256) k_bfly_peak(u64* __restrict__ out, const ulonglong2* __restrict__ tws,
+                                                   u64 q, int iters) {
+  ulonglong2 tw[15];
+#pragma unroll
+  for (int i = 0; i < 15; ++i) tw[i] = tws[i];
+  u64 x[16];
+  const u64 t = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = (t * 16 + k) % q;
+  const u64 q2 = 4 * q;
+  auto twf = [&](int d, int b) { return tw[(1 << d) - 1 + b]; };
+  for (int it = 0; it < iters; ++it) ct16<0, FAST>(x, q, q2, twf);
+  u64 acc = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc ^= x[k];
+  out[t] = acc;
+}
+
+// butterflies per second of k_bfly_peak (fast: q < 2^47 unreduced network)
+int ntt_butterfly_peak(int fast, double* bfly_per_s) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const u64 q = fast ? 1099511922689ull : 1152921504606584833ull;  // 40-bit / 60-bit NTT primes
+  const int threads = 256, blocks = sms * 8, iters = 256;
+  ulonglong2 h[15];
+  for (int i = 0; i < 15; ++i) {
+    const u64 w = (0x9E3779B97F4A7C15ull * (i + 1)) % q;
+    h[i] = make_ulonglong2(w, (u64)((((unsigned __int128)w) << 64) / q));
+  }
+  u64* d_out = nullptr;
+  ulonglong2* d_tw = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaError_t err = cudaMalloc(&d_out, (size_t)blocks * threads * 8);
+  if (!err) err = cudaMalloc(&d_tw, sizeof(h));
+  if (!err) err = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (!err) err = cudaMemcpyAsync(d_tw, h, sizeof(h), cudaMemcpyHostToDevice, st);
+  if (!err) err = cudaEventCreate(&e0);
+  if (!err) err = cudaEventCreate(&e1);
+  float ms = 0.f;
+  if (!err) {
+    auto go = [&]() {
+      if (fast) k_bfly_peak<true><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
+      else k_bfly_peak<false><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
+    };
+    for (int w = 0; w < 3; ++w) go();  // warm-up (clocks ramp)
+    cudaEventRecord(e0, st);
+    const int reps = 10;
+    for (int r = 0; r < reps; ++r) go();
+    cudaEventRecord(e1, st);
+    err = cudaEventSynchronize(e1);
+    if (!err) err = cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+  }
+  if (!err) err = cudaGetLastError();
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  cudaFree(d_out);
+  cudaFree(d_tw);
+  if (err) return (int)err;
+  *bfly_per_s = (double)blocks * threads * iters * 32.0 / (ms * 1e-3);
+  return 0;
+}
+
+// limbs transformed per class since the last read: [fwd fast, fwd full, inv fast, inv full]
+unsigned long long g_ntt_limbs[4] = {0, 0, 0, 0};
+
+static void count_limbs(const NttTables& T, const LimbMap& m, u32 ny, u32 nz, bool inverse) {
+  for (u32 r = 0; r < ny; ++r) {
+    const bool f = T.small && T.small[m.basis.mod_of(m.r0 + r + m.first_limb)];
+    g_ntt_limbs[(inverse ? 2 : 0) + (f ? 0 : 1)] += nz;
+  }
+}
+
 bool ntt2_supported(u32 logN) { return logN >= 12 && logN <= 16; }
 
 template <int L, bool H, int OCC, int F>
@@ -480,6 +563,7 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
     return cudaSuccess;
   };
   (void)hint;
+  count_limbs(T, map, nlimbs, npolys, inverse);
   const u32 G = g_ntt_tuning.group_limbs > 0 ? (u32)g_ntt_tuning.group_limbs : 0;
   if (G == 0 || nlimbs * npolys <= G) return pair(map, nlimbs, npolys);
   cudaError_t e = cudaSuccess;
