@@ -352,13 +352,7 @@ __global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, 
       const u64 qt = s_q[t];
       u64 hi = 0, lo = 0;
 #pragma unroll
-      for (int i = 0; i < NS; ++i) {
-        const u64 b = s_tm[t * NS + i];
-        const u64 plo = y[i] * b;
-        const u64 phi = __umul64hi(y[i], b);
-        lo += plo;
-        hi += phi + (lo < plo ? 1ull : 0ull);
-      }
+      for (int i = 0; i < NS; ++i) mac128_lazy(hi, lo, y[i], s_tm[t * NS + i]);  // NS <= 6 < kLazyTerms
       u64 v = redc128(hi, lo, qt, s_ninv[t]);
       dst[s_pos[t] + k] = sub_mod(v, s_corr[t * NM + mask], qt);
     }
@@ -501,30 +495,36 @@ __global__ void __launch_bounds__(256, JB >= 4 ? 2 : 3) k_ks_inner_p(
   const u32 N = 1u << logN, r = blockIdx.y;
   const u32 n_ext = basis.nlimbs();
   const u32 mod = basis.mod_of(r);
-  const u64 q = mc[mod].q, ninv = mc[mod].ninv;
+  const u64 q = mc[mod].q, ninv = mc[mod].ninv, one_sh = mc[mod].one_sh;
   const u32 klq = key_lq ? key_lq : basis.Lq;
   const size_t key_dst = (size_t)(klq + basis.np) * N;
   const u32 kmod = mod < basis.Lq ? mod : klq + (mod - basis.Lq);
   const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;
   const u32 b = blockIdx.x % nb, x0 = blockIdx.x / nb, xs = gridDim.x / nb;
+  static_assert(kLazyTerms % JB == 0, "fold cadence");
   const u64* xsrc = x_eval + (size_t)b * x_bst + (size_t)r * N;
   const u64* rsrc = raised + (size_t)b * ndig * n_ext * N + (size_t)r * N;
   const u64* kb_base = key_b + (size_t)kmod * N;
   const u64* ka_base = key_a + (size_t)kmod * N;
+  const size_t rstep = (size_t)n_ext * N;
   for (u32 kv = x0 * blockDim.x + threadIdx.x; kv < N / 2; kv += xs * blockDim.x) {
     const u32 k = 2 * kv;
     const u32 p0 = g == 1 ? k : galois_src(k, g, logN), p1 = g == 1 ? k + 1 : galois_src(k + 1, g, logN);
     u64 bh0 = 0, bl0 = 0, bh1 = 0, bl1 = 0, ah0 = 0, al0 = 0, ah1 = 0, al1 = 0;
+    // running pointers (one 64-bit add per digit instead of re-deriving
+    // every address from the digit index)
+    const u64* kbp = kb_base + k;
+    const u64* kap = ka_base + k;
+    const u64* rp = rsrc;
     for (u32 j0 = 0; j0 < ndig; j0 += JB) {
       ulonglong2 KB[JB], KA[JB], X[JB];
 #pragma unroll
       for (int i = 0; i < JB; ++i) {
         const u32 j = j0 + i;
         if (j < ndig) {
-          const size_t kofs = (size_t)j * key_dst + k;
-          KB[i] = *reinterpret_cast<const ulonglong2*>(kb_base + kofs);
-          KA[i] = *reinterpret_cast<const ulonglong2*>(ka_base + kofs);
-          const u64* src = j == own ? xsrc : rsrc + (size_t)j * n_ext * N;
+          KB[i] = *reinterpret_cast<const ulonglong2*>(kbp);
+          KA[i] = *reinterpret_cast<const ulonglong2*>(kap);
+          const u64* src = j == own ? xsrc : rp;
           if (g == 1) {
             X[i] = *reinterpret_cast<const ulonglong2*>(src + k);
           } else {
@@ -534,21 +534,34 @@ __global__ void __launch_bounds__(256, JB >= 4 ? 2 : 3) k_ks_inner_p(
         } else {
           KB[i] = KA[i] = X[i] = make_ulonglong2(0, 0);
         }
+        kbp += key_dst;
+        kap += key_dst;
+        rp += rstep;
       }
 #pragma unroll
       for (int i = 0; i < JB; ++i) {
-        mac128(bh0, bl0, X[i].x, KB[i].x, q);
-        mac128(ah0, al0, X[i].x, KA[i].x, q);
-        mac128(bh1, bl1, X[i].y, KB[i].y, q);
-        mac128(ah1, al1, X[i].y, KA[i].y, q);
+        mac128_lazy(bh0, bl0, X[i].x, KB[i].x);
+        mac128_lazy(ah0, al0, X[i].x, KA[i].x);
+        mac128_lazy(bh1, bl1, X[i].y, KB[i].y);
+        mac128_lazy(ah1, al1, X[i].y, KA[i].y);
+      }
+      if ((j0 + JB) % kLazyTerms == 0) {  // never more than kLazyTerms unfolded products
+        bh0 = fold_hi(bh0, q, one_sh);
+        bh1 = fold_hi(bh1, q, one_sh);
+        ah0 = fold_hi(ah0, q, one_sh);
+        ah1 = fold_hi(ah1, q, one_sh);
       }
     }
     if (c0 && r < basis.nq) {  // extended-basis output: + P * sigma_g(c0) on the Q limbs
       const u64 w = pR[r];
       const u64* src = c0 + (size_t)b * c0_bst + (size_t)r * N;
-      mac128(bh0, bl0, src[p0], w, q);
-      mac128(bh1, bl1, src[p1], w, q);
+      mac128_lazy(bh0, bl0, src[p0], w);
+      mac128_lazy(bh1, bl1, src[p1], w);
     }
+    bh0 = fold_hi(bh0, q, one_sh);
+    bh1 = fold_hi(bh1, q, one_sh);
+    ah0 = fold_hi(ah0, q, one_sh);
+    ah1 = fold_hi(ah1, q, one_sh);
     u64* A = acc + (size_t)b * 2 * n_ext * N;
     *reinterpret_cast<ulonglong2*>(A + (size_t)r * N + k) =
         make_ulonglong2(redc128(bh0, bl0, q, ninv), redc128(bh1, bl1, q, ninv));
@@ -658,7 +671,7 @@ __global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __re
   const u32 ne = nb - b0 < (u32)NB ? nb - b0 : (u32)NB;
   const u32 x0 = NB == 1 ? blockIdx.x / nb : blockIdx.x, xs = NB == 1 ? gridDim.x / nb : gridDim.x;
   const u32 mod = r < nq ? r : Lq + (r - nq);
-  const u64 q = mc[mod].q, ninv = mc[mod].ninv;
+  const u64 q = mc[mod].q, ninv = mc[mod].ninv, one_sh = mc[mod].one_sh;
   const size_t bst = 2 * (size_t)nl * N, pst = (size_t)nl * N;
   const size_t off = (size_t)r * N + (size_t)b0 * bst, moff = (size_t)r * N;
   for (u32 kv = x0 * blockDim.x + threadIdx.x; kv < N / VEC; kv += xs * blockDim.x) {
@@ -695,8 +708,16 @@ __global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __re
             x[0] = *src;
           }
 #pragma unroll
-          for (int v = 0; v < VEC; ++v) mac128(hi[e][p][v], lo[e][p][v], x[v], m[v], q);
+          for (int v = 0; v < VEC; ++v) mac128_lazy(hi[e][p][v], lo[e][p][v], x[v], m[v]);
         }
+      }
+      if ((t + 1) % kLazyTerms == 0 || t + 1 == nt) {
+#pragma unroll
+        for (int e = 0; e < NB; ++e)
+#pragma unroll
+          for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) hi[e][p][v] = fold_hi(hi[e][p][v], q, one_sh);
       }
     }
 #pragma unroll
@@ -1016,7 +1037,7 @@ __global__ void __launch_bounds__(256) k_mac_multi_async(MacMulti M, int ng, int
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MacStage* S = reinterpret_cast<MacStage*>(smem_raw);
   const u32 N = 1u << logN, r = blockIdx.y, k0 = blockIdx.x * kMacTile, tid = threadIdx.x;
-  const u64 q = mc[r].q, ninv = mc[r].ninv;
+  const u64 q = mc[r].q, ninv = mc[r].ninv, one_sh = mc[r].one_sh;
   for (int s = 0; s < kMacStages - 1; ++s) {
     if (s < nt) mac_stage_issue(S[s], M, s, ng, r, nq, N, k0);
     cp_async_commit();
@@ -1046,8 +1067,15 @@ __global__ void __launch_bounds__(256) k_mac_multi_async(MacMulti M, int ng, int
       } else {
         m = C.mask[g][tid];
       }
-      mac128(h[g][0], l[g][0], x0, m, q);
-      mac128(h[g][1], l[g][1], x1, m, q);
+      mac128_lazy(h[g][0], l[g][0], x0, m);
+      mac128_lazy(h[g][1], l[g][1], x1, m);
+    }
+    if ((t + 1) % kLazyTerms == 0 || t + 1 == nt) {
+#pragma unroll
+      for (int g = 0; g < kMultiG; ++g) {
+        h[g][0] = fold_hi(h[g][0], q, one_sh);
+        h[g][1] = fold_hi(h[g][1], q, one_sh);
+      }
     }
   }
   cp_async_wait<0>();
@@ -1065,6 +1093,135 @@ __global__ void __launch_bounds__(256) k_mac_multi_async(MacMulti M, int ng, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// The same shared-term MAC with the staging done by the bulk-copy engine
+// (TMA, cp.async.bulk): per term one elected thread arms the stage's
+// mbarrier with the byte count and issues <= 10 contiguous row copies
+// (2 ciphertext polys of 2 KB, each output's mask row: 2 KB, or the 1 KB
+// low + 512 B high planes of a packed limb).  The other 255 threads spend
+// no instructions on address generation or copy issue; they wait on the
+// stage's mbarrier phase and run the 8 lazy MACs per term.  Branches on
+// mask presence / packing read one flag byte per term staged in smem.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "MBAR_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mac_stage_bulk(MacStage& S, u64* bar, const MacMulti& M, int t, u32 fl, u32 r,
+                                               u32 nq, u32 N, u32 k0) {
+  const size_t off = (size_t)r * N + k0, pst = (size_t)nq * N;
+  u32 bytes = 2 * kMacTile * 8;
+  for (int g = 0; g < kMultiG; ++g)
+    if (fl >> g & 1u) bytes += (fl >> (4 + g) & 1u) ? kMacTile * 6 : kMacTile * 8;
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(S.ct[0], M.ct[t] + off, kMacTile * 8, bar);
+  bulk_g2s(S.ct[1], M.ct[t] + pst + off, kMacTile * 8, bar);
+  for (int g = 0; g < kMultiG; ++g) {
+    if (!(fl >> g & 1u)) continue;
+    const u64* mp = M.mask[g][t];
+    if (fl >> (4 + g) & 1u) {
+      const char* b = reinterpret_cast<const char*>(mp);
+      char* dst = reinterpret_cast<char*>(S.mask[g]);
+      bulk_g2s(dst, b + 8 * (size_t)N + 4 * ((size_t)(r - 1) * N + k0), kMacTile * 4, bar);
+      bulk_g2s(dst + kMacTile * 4, b + 8 * (size_t)N + 4 * (size_t)(nq - 1) * N + 2 * ((size_t)(r - 1) * N + k0),
+               kMacTile * 2, bar);
+    } else {
+      bulk_g2s(S.mask[g], M.packed[g][t] ? mp + k0 : mp + off, kMacTile * 8, bar);  // packed limb 0: u64 row
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_mac_multi_tma(MacMulti M, int ng, int nt, u32 nq, u32 logN,
+                                                       int accumulate, const ModConsts* __restrict__ mc) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  MacStage* S = reinterpret_cast<MacStage*>(smem_raw);
+  __shared__ __align__(8) u64 full[kMacStages];
+  __shared__ unsigned char flags[kMultiT];
+  const u32 N = 1u << logN, r = blockIdx.y, k0 = blockIdx.x * kMacTile, tid = threadIdx.x;
+  const u64 q = mc[r].q, ninv = mc[r].ninv, one_sh = mc[r].one_sh;
+  if (tid < (u32)nt) {
+    u32 fl = 0;
+    for (int g = 0; g < ng; ++g)
+      if (M.mask[g][tid]) fl |= (1u << g) | ((M.packed[g][tid] && r > 0) ? (16u << g) : 0u);
+    flags[tid] = (unsigned char)fl;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kMacStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < kMacStages - 1 && s < nt; ++s) mac_stage_bulk(S[s], &full[s], M, s, flags[s], r, nq, N, k0);
+  u64 h[kMultiG][2], l[kMultiG][2];
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g) h[g][0] = h[g][1] = l[g][0] = l[g][1] = 0;
+  for (int t = 0; t < nt; ++t) {
+    if (t > 0) __syncthreads();  // every thread is done with slot (t-1) % kMacStages
+    if (tid == 0) {
+      const int tn = t + kMacStages - 1;
+      if (tn < nt) mac_stage_bulk(S[tn % kMacStages], &full[tn % kMacStages], M, tn, flags[tn], r, nq, N, k0);
+    }
+    const u32 fl = flags[t];
+    mbar_wait(&full[t % kMacStages], (u32)(t / kMacStages) & 1u);
+    const MacStage& C = S[t % kMacStages];
+    const u64 x0 = C.ct[0][tid], x1 = C.ct[1][tid];
+#pragma unroll
+    for (int g = 0; g < kMultiG; ++g) {
+      if (!(fl >> g & 1u)) continue;
+      u64 m;
+      if (fl >> (4 + g) & 1u) {
+        const unsigned* lo = reinterpret_cast<const unsigned*>(C.mask[g]);
+        const unsigned short* hi =
+            reinterpret_cast<const unsigned short*>(reinterpret_cast<const unsigned char*>(C.mask[g]) + kMacTile * 4);
+        m = (u64)lo[tid] | ((u64)hi[tid] << 32);
+      } else {
+        m = C.mask[g][tid];
+      }
+      mac128_lazy(h[g][0], l[g][0], x0, m);
+      mac128_lazy(h[g][1], l[g][1], x1, m);
+    }
+    if ((t + 1) % kLazyTerms == 0 || t + 1 == nt) {
+#pragma unroll
+      for (int g = 0; g < kMultiG; ++g) {
+        h[g][0] = fold_hi(h[g][0], q, one_sh);
+        h[g][1] = fold_hi(h[g][1], q, one_sh);
+      }
+    }
+  }
+  const size_t pst = (size_t)nq * N, off = (size_t)r * N + k0 + tid;
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g) {
+    if (g >= ng) break;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      u64* d = M.out[g] + p * pst + off;
+      u64 y = redc128(h[g][p], l[g][p], q, ninv);
+      if (accumulate) y = add_mod(y, *d, q);
+      *d = y;
+    }
+  }
+}
+
+int g_mac_tma = 1;    // 1: bulk-copy (TMA) staged k_mac_multi_tma
 int g_mac_async = 1;  // 1: cp.async pipeline (k_mac_multi_async), 0: k_mac_multi_lanes
 
 int g_mac_lanes = 1;  // 1: k_mac_multi_lanes, 0: register-blocked k_mac_multi
@@ -1072,6 +1229,18 @@ int g_mac_lanes = 1;  // 1: k_mac_multi_lanes, 0: register-blocked k_mac_multi
 cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN, int accumulate,
                              const ModConsts* mc, cudaStream_t st) {
   if (ng < 1 || ng > kMultiG) return cudaErrorInvalidValue;
+  if (g_mac_tma && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
+    static bool attr_tma = false;
+    const size_t sm = sizeof(MacStage) * kMacStages;
+    if (!attr_tma) {
+      cudaError_t e = cudaFuncSetAttribute(k_mac_multi_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e) return e;
+      attr_tma = true;
+    }
+    dim3 g((1u << logN) / kMacTile, nq, 1);
+    k_mac_multi_tma<<<g, 256, sm, st>>>(M, ng, nt, nq, logN, accumulate, mc);
+    return cudaGetLastError();
+  }
   if (g_mac_async && (1u << logN) % kMacTile == 0) {
     static bool attr = false;
     const size_t sm = sizeof(MacStage) * kMacStages;
@@ -1237,9 +1406,6 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
     grid.x *= (nb ? nb : 1);
     if (g_ks_pipe >= 4)
       k_ks_inner_p<4><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,
-                                            nb ? nb : 1, x_bst, c0, c0_bst, pR, key_lq);
-    else if (g_ks_pipe == 3)
-      k_ks_inner_p<3><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,
                                             nb ? nb : 1, x_bst, c0, c0_bst, pR, key_lq);
     else
       k_ks_inner_p<2><<<grid, 256, 0, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc,

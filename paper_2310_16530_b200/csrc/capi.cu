@@ -1106,6 +1106,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "mac_batch") g_mac_batch = (int)value;
   else if (k == "mac_lanes") g_mac_lanes = (int)value;
   else if (k == "mac_async") g_mac_async = (int)value;
+  else if (k == "mac_tma") g_mac_tma = (int)value;
   else if (k == "merge_moddown") g_merge_moddown = (int)value;
   else return fail(HCNN_E_PARAMETER, "unknown option " + k);
   return HCNN_OK;
