@@ -208,7 +208,8 @@ def int_roofline(roof: dict, prof: dict, limbs: dict, n: int) -> dict:
     ms = sum(v["ms"] for k, v in prof.items() if _kernel_family(k) == fam)
     if fast + full == 0 or ms <= 0:
         return roof
-    pf, ps = _native.ntt_butterfly_peak(True), _native.ntt_butterfly_peak(False)
+    # fast limbs (q < 2^44 here) run the FP64-quotient network: its probe is their ceiling
+    pf, ps = _native.ntt_butterfly_peak(2), _native.ntt_butterfly_peak(0)
     per_limb = n // 2 * (n.bit_length() - 1)
     ideal_s = per_limb * (fast / pf + full / ps)
     bfly = per_limb * (fast + full)
@@ -218,8 +219,8 @@ def int_roofline(roof: dict, prof: dict, limbs: dict, n: int) -> dict:
     out = {"kernel": fam, "bound": "int", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
            "unit": "Gbutterfly/s", "frac": round(ideal_s / (ms / 1e3), 4), "traffic": roof.get("traffic"),
            "peak_source": (f"measured on this GPU: radix-16 register network without memory traffic "
-                           f"(hcnn_ntt_butterfly_peak) {pf/1e9:.1f} Gbfly/s for q<2^47 limbs, {ps/1e9:.1f} for "
-                           f"full-width limbs, weighted by this image's {fast} + {full} limbs"),
+                           f"(hcnn_ntt_butterfly_peak) {pf/1e9:.1f} Gbfly/s for the FP64-quotient network of "
+                           f"q<2^44 limbs, {ps/1e9:.1f} for full-width limbs, weighted by this image's {fast} + {full} limbs"),
            "limbs": {"fast": fast, "full": full}, "share_of_device_time": roof["share_of_device_time"],
            "hbm": hbm}
     return out

@@ -149,7 +149,7 @@ def kernel_launches() -> int:
 def ntt_butterfly_peak(fast: bool, device: int = 0) -> float:
     """Measured butterflies/s of the NTT's register network (integer-pipe ceiling)."""
     out = ctypes.c_double(0.0)
-    check(load().hcnn_ntt_butterfly_peak(int(device), 1 if fast else 0, ctypes.byref(out)))
+    check(load().hcnn_ntt_butterfly_peak(int(device), int(fast), ctypes.byref(out)))
     return float(out.value)
 
 

@@ -1152,7 +1152,7 @@ __device__ __forceinline__ void mac_stage_bulk(MacStage& S, u64* bar, const MacM
 
 __global__ void __launch_bounds__(256) k_mac_multi_tma(MacMulti M, int ng, int nt, u32 nq, u32 logN,
                                                        int accumulate, const ModConsts* __restrict__ mc) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   MacStage* S = reinterpret_cast<MacStage*>(smem_raw);
   __shared__ __align__(8) u64 full[kMacStages];
   __shared__ unsigned char flags[kMultiT];
@@ -1218,6 +1218,123 @@ __global__ void __launch_bounds__(256) k_mac_multi_tma(MacMulti M, int ng, int n
       if (accumulate) y = add_mod(y, *d, q);
       *d = y;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Key-switch inner product with TMA-staged operands.  A CTA owns one
+// 256-coefficient tile of one output limb r for up to kKsEntries batch
+// entries; per digit j one elected thread bulk-copies the two key rows'
+// tiles (2 x 2 KB) and every entry's raised-digit tile (2 KB each) into a
+// ring of kMacStages stages tracked by mbarriers, so each key tile leaves
+// HBM once per kKsEntries entries and no thread spends instructions on
+// address generation.  The Galois permutation maps an aligned 256-block of
+// outputs onto one aligned 256-block of sources (the low log2(N)-8 bits of
+// the natural index fix the block), so the source tile is fetched whole and
+// permuted on the shared-memory read.  Extended-basis outputs (c0 != null)
+// take one more stage: P * sigma_g(c0) on the Q limbs.  Lazy 128-bit sums,
+// one REDC: bit-identical with k_ks_inner.
+// ---------------------------------------------------------------------------
+constexpr int kKsEntries = 4;
+struct KsStage {
+  u64 kb[kMacTile];
+  u64 ka[kMacTile];
+  u64 x[kKsEntries][kMacTile];
+};
+int g_ks_tma = 1;
+int g_ks_tma_min = 3;  // smallest batch routed to k_ks_inner_tma
+
+__global__ void __launch_bounds__(256) k_ks_inner_tma(u64* __restrict__ acc, const u64* __restrict__ x_eval,
+                                                      const u64* __restrict__ raised, const u64* __restrict__ key_b,
+                                                      const u64* __restrict__ key_a, Basis basis, u32 alpha,
+                                                      u32 ndig, u32 logN, u64 g, const ModConsts* __restrict__ mc,
+                                                      u32 nb, size_t x_bst, const u64* __restrict__ c0,
+                                                      size_t c0_bst, const u64* __restrict__ pR, u32 key_lq) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  KsStage* S = reinterpret_cast<KsStage*>(smem_raw);
+  __shared__ __align__(8) u64 full[kMacStages];
+  const u32 N = 1u << logN, r = blockIdx.y, tile = blockIdx.x, tid = threadIdx.x;
+  const u32 b0 = blockIdx.z * kKsEntries;
+  const u32 ne = nb - b0 < (u32)kKsEntries ? nb - b0 : (u32)kKsEntries;
+  const u32 n_ext = basis.nlimbs();
+  const u32 mod = basis.mod_of(r);
+  const u64 q = mc[mod].q, ninv = mc[mod].ninv, one_sh = mc[mod].one_sh;
+  const u32 klq = key_lq ? key_lq : basis.Lq;
+  const size_t key_dst = (size_t)(klq + basis.np) * N;
+  const u32 kmod = mod < basis.Lq ? mod : klq + (mod - basis.Lq);
+  const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;
+  const u32 k = tile * kMacTile + tid;
+  const u32 src = g == 1 ? k : galois_src(k, g, logN);
+  const u32 s_in = src & (kMacTile - 1);                      // position inside the source tile
+  const size_t t_src = (size_t)(src & ~(u32)(kMacTile - 1));  // same block for the whole CTA
+  const size_t r_bst = (size_t)ndig * n_ext * N;
+  const bool ext = c0 != nullptr && r < basis.nq;
+  const u32 nst = ndig + (ext ? 1u : 0u);
+  auto issue = [&](u32 j) {
+    KsStage& T = S[j % kMacStages];
+    u64* bar = &full[j % kMacStages];
+    if (j < ndig) {
+      mbar_expect_tx(bar, (2 + ne) * kMacTile * 8);
+      const size_t kofs = (size_t)j * key_dst + (size_t)kmod * N + (size_t)tile * kMacTile;
+      bulk_g2s(T.kb, key_b + kofs, kMacTile * 8, bar);
+      bulk_g2s(T.ka, key_a + kofs, kMacTile * 8, bar);
+      for (u32 e = 0; e < ne; ++e) {
+        const u64* sp = j == own ? x_eval + (size_t)(b0 + e) * x_bst + (size_t)r * N
+                                 : raised + (size_t)(b0 + e) * r_bst + ((size_t)j * n_ext + r) * N;
+        bulk_g2s(T.x[e], sp + t_src, kMacTile * 8, bar);
+      }
+    } else {  // extended-basis term: c0 tiles
+      mbar_expect_tx(bar, ne * kMacTile * 8);
+      for (u32 e = 0; e < ne; ++e)
+        bulk_g2s(T.x[e], c0 + (size_t)(b0 + e) * c0_bst + (size_t)r * N + t_src, kMacTile * 8, bar);
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kMacStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (u32 j = 0; j < (u32)kMacStages - 1 && j < nst; ++j) issue(j);
+  u64 bh[kKsEntries], bl[kKsEntries], ah[kKsEntries], al[kKsEntries];
+#pragma unroll
+  for (int e = 0; e < kKsEntries; ++e) bh[e] = bl[e] = ah[e] = al[e] = 0;
+  for (u32 j = 0; j < nst; ++j) {
+    if (j > 0) __syncthreads();  // slot (j-1) % kMacStages is free
+    if (tid == 0 && j + kMacStages - 1 < nst) issue(j + kMacStages - 1);
+    mbar_wait(&full[j % kMacStages], (j / kMacStages) & 1u);
+    const KsStage& T = S[j % kMacStages];
+    if (j < ndig) {
+      const u64 kb = T.kb[tid], ka = T.ka[tid];
+#pragma unroll
+      for (int e = 0; e < kKsEntries; ++e) {
+        if ((u32)e >= ne) break;
+        const u64 x = T.x[e][s_in];
+        mac128_lazy(bh[e], bl[e], x, kb);
+        mac128_lazy(ah[e], al[e], x, ka);
+      }
+    } else {
+      const u64 w = pR[r];
+#pragma unroll
+      for (int e = 0; e < kKsEntries; ++e) {
+        if ((u32)e >= ne) break;
+        mac128_lazy(bh[e], bl[e], T.x[e][s_in], w);
+      }
+    }
+    if ((j + 1) % kLazyTerms == 0 || j + 1 == nst) {
+#pragma unroll
+      for (int e = 0; e < kKsEntries; ++e) {
+        bh[e] = fold_hi(bh[e], q, one_sh);
+        ah[e] = fold_hi(ah[e], q, one_sh);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < kKsEntries; ++e) {
+    if ((u32)e >= ne) break;
+    u64* A = acc + (size_t)(b0 + e) * 2 * n_ext * N;
+    A[(size_t)r * N + k] = redc128(bh[e], bl[e], q, ninv);
+    A[((size_t)n_ext + r) * N + k] = redc128(ah[e], al[e], q, ninv);
   }
 }
 
@@ -1401,7 +1518,21 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
                             cudaStream_t st, u32 nb, size_t x_bst, const u64* c0, size_t c0_bst, const u64* pR,
                             u32 key_lq) {
-  if ((nb <= 1 || g_ks_batch <= 1) && g_ks_pipe > 0) {
+  // TMA staging pays once a key tile feeds >= 3 entries; small batches keep
+  // the register-pipelined kernel (measured: tools/ks_bench.py)
+  if (g_ks_tma && nb >= (u32)g_ks_tma_min && (1u << logN) % kMacTile == 0) {
+    static bool attr_ks = false;
+    const size_t sm = sizeof(KsStage) * kMacStages;
+    if (!attr_ks) {
+      cudaError_t e = cudaFuncSetAttribute(k_ks_inner_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e) return e;
+      attr_ks = true;
+    }
+    const u32 nbb = nb ? nb : 1;
+    dim3 grid((1u << logN) / kMacTile, basis.nlimbs(), (nbb + kKsEntries - 1) / kKsEntries);
+    k_ks_inner_tma<<<grid, 256, sm, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nbb,
+                                          x_bst, c0, c0_bst, pR, key_lq);
+  } else if ((nb <= 1 || g_ks_batch <= 1) && g_ks_pipe > 0) {
     dim3 grid = row_grid((1u << logN) / 2, basis.nlimbs(), 256);
     grid.x *= (nb ? nb : 1);
     if (g_ks_pipe >= 4)

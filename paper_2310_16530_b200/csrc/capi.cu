@@ -348,7 +348,17 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
     // inverse e = nb-1+i -> itw[nb*(N1+g) + i] (nb = 128>>u blocks)
     const u32 N1 = n >> 8;
     std::vector<ulonglong2> ctw((size_t)c->nmods * N), ictw((size_t)c->nmods * N);
-    for (u32 m = 0; m < c->nmods; ++m)
+    for (u32 m = 0; m < c->nmods; ++m) {
+      // FP64-quotient forward butterflies (ntt2.cu, q < 2^kFpBits): the
+      // companion is double(wp * 2^-64) ~ w/q instead of the Shoup word
+      const bool fp = kNttFp && c->mods[m] < (1ull << kFpBits);
+      auto fwd_comp = [&](u64 wp) -> u64 {
+        if (!fp) return wp;
+        const double d = (double)wp * 0x1p-64;
+        u64 bits;
+        std::memcpy(&bits, &d, 8);
+        return bits;
+      };
       for (u32 g = 0; g < N1; ++g) {
         ulonglong2* F = &ctw[((size_t)m * N1 + g) * 256];
         ulonglong2* I = &ictw[((size_t)m * N1 + g) * 256];
@@ -357,12 +367,13 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
         for (u32 s = 0; s < 8; ++s)
           for (u32 i = 0; i < (1u << s); ++i) {
             size_t src = (size_t)(N1 + g) * (1u << s) + i;
-            F[(1u << s) - 1 + i] = make_ulonglong2(tw[m * N + src], twp[m * N + src]);
+            F[(1u << s) - 1 + i] = make_ulonglong2(tw[m * N + src], fwd_comp(twp[m * N + src]));
             u32 nb = 1u << s;  // inverse stage with nb blocks
             size_t isrc = (size_t)nb * (N1 + g) + i;
             I[nb - 1 + i] = make_ulonglong2(itw[m * N + isrc], itwp[m * N + isrc]);
           }
       }
+    }
     CK(cudaMalloc(&c->d_ctw, ctw.size() * sizeof(ulonglong2)));
     CK(cudaMalloc(&c->d_ictw, ictw.size() * sizeof(ulonglong2)));
     CK(cudaMemcpy(c->d_ctw, ctw.data(), ctw.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice));
@@ -1103,6 +1114,8 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_split") g_ntt_tuning.split = (int)value;
   else if (k == "ks_batch") g_ks_batch = (int)value;
   else if (k == "ks_pipe") g_ks_pipe = (int)value;
+  else if (k == "ks_tma") g_ks_tma = (int)value;
+  else if (k == "ks_tma_min") g_ks_tma_min = (int)value;
   else if (k == "mac_batch") g_mac_batch = (int)value;
   else if (k == "mac_lanes") g_mac_lanes = (int)value;
   else if (k == "mac_async") g_mac_async = (int)value;

@@ -51,6 +51,10 @@ cudaError_t launch_ntt(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 n
 cudaError_t ntt_configure_smem();
 bool ntt2_supported(u32 logN);
 int ntt_butterfly_peak(int fast, double* bfly_per_s);
+// moduli below 2^kFpBits run the forward fast path with an FP64 quotient;
+// their forward chunk-twiddle companions are double(w/q) bit patterns
+constexpr int kFpBits = 44;
+constexpr bool kNttFp = true;
 extern unsigned long long g_ntt_limbs[4];
 cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 npolys, bool inverse,
                         cudaStream_t st);

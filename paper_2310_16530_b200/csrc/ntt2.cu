@@ -23,6 +23,7 @@ namespace hcnn {
 
 NttTuning g_ntt_tuning;
 
+
 // L2 policy: keep twiddle tables resident (evict_last), stream the data
 __device__ __forceinline__ u64 keep_policy() {
   u64 pol;
@@ -82,6 +83,40 @@ __device__ __forceinline__ void gs_bfly_fast(u64& X, u64& Y, u64 w, u64 wp, u64 
   Y = shoup_approx(x - y + c, w, wp, q);
 }
 
+// Shoup product with the quotient estimated on the FP64 pipe (q < 2^47,
+// a < 2^51): wq = fl(w / q); qhat = trunc(fl(a) * wq - 1) is Q-2..Q of the
+// true quotient Q = floor(a w / q), so a*w - qhat*q (exact, low 64 bits) lies
+// in [0, 3q).  Moves the 3 IMAD.WIDE of the high product onto the DFMA and
+// conversion units.
+__device__ __forceinline__ u64 shoup_fp(u64 a, u64 w, double wq, u64 q) {
+  const double qf = fma(__ull2double_rn(a), wq, -1.0);
+  const u64 qhat = __double2ull_rz(qf);
+  return a * w - qhat * q;
+}
+// Same with magic-number conversions (no XU ops): for 0 <= a < 2^52,
+// double(a) = bits(2^52 | a) - 2^52 (one DADD), and fma(.., 2^52) rounds the
+// quotient estimate to the nearest integer in the low mantissa bits.
+// qr = round(a wq) is Q-1..Q+1, so a*w - qr*q + q lies in [0, 3q).
+__device__ __forceinline__ u64 shoup_fp2(u64 a, u64 w, double wq, u64 q) {
+  const double two52 = 4503599627370496.0;
+  const double ad = __longlong_as_double((long long)(a | 0x4330000000000000ull)) - two52;
+  const double qf = fma(ad, wq, two52);
+  const u64 qr = (u64)__double_as_longlong(qf) & 0x000FFFFFFFFFFFFFull;
+  return a * w - qr * q + q;
+}
+__device__ __forceinline__ void ct_bfly_fp2(u64& X, u64& Y, u64 w, double wq, u64 q, u64 q4) {
+  u64 t = shoup_fp2(Y, w, wq, q);
+  u64 x = X;
+  X = x + t;
+  Y = x + q4 - t;
+}
+__device__ __forceinline__ void ct_bfly_fp(u64& X, u64& Y, u64 w, double wq, u64 q, u64 q4) {
+  u64 t = shoup_fp(Y, w, wq, q);
+  u64 x = X;
+  X = x + t;
+  Y = x + q4 - t;
+}
+
 // One CT stage d of a 16-point network held in x[0..15]: pairs k with
 // k + (8>>d) inside sub-block b = k >> (4-d).  Stages are template
 // parameters so every register index is a compile-time constant.
@@ -107,10 +142,29 @@ __device__ __forceinline__ void ct_stage_fast(u64 (&x)[16], u64 q, u64 q4, TW& t
   }
 }
 
-// CT stages d in [D0,4); FAST selects the unreduced butterflies (q < 2^47)
-template <int D0, bool FAST = false, class TW>
+template <int d, class TW>
+__device__ __forceinline__ void ct_stage_fp(u64 (&x)[16], u64 q, u64 q4, TW& tw) {
+  constexpr int h = 8 >> d;
+#pragma unroll
+  for (int b = 0; b < (1 << d); ++b) {
+    ulonglong2 W = tw(d, b);
+    const double wq = __longlong_as_double((long long)W.y);
+#pragma unroll
+    for (int r = 0; r < h; ++r) ct_bfly_fp(x[2 * h * b + r], x[2 * h * b + r + h], W.x, wq, q, q4);
+  }
+}
+
+// CT stages d in [D0,4); FAST selects the unreduced butterflies (q < 2^47),
+// FP the unreduced butterflies with the FP64 quotient (q < 2^44; twiddle
+// companions hold double(w/q) bits)
+template <int D0, bool FAST = false, class TW, bool FP = false>
 __device__ __forceinline__ void ct16(u64 (&x)[16], u64 q, u64 q2, TW tw) {
-  if constexpr (FAST) {
+  if constexpr (FP) {
+    if constexpr (D0 <= 0) ct_stage_fp<0>(x, q, q2, tw);
+    if constexpr (D0 <= 1) ct_stage_fp<1>(x, q, q2, tw);
+    if constexpr (D0 <= 2) ct_stage_fp<2>(x, q, q2, tw);
+    if constexpr (D0 <= 3) ct_stage_fp<3>(x, q, q2, tw);
+  } else if constexpr (FAST) {
     if constexpr (D0 <= 0) ct_stage_fast<0>(x, q, q2, tw);
     if constexpr (D0 <= 1) ct_stage_fast<1>(x, q, q2, tw);
     if constexpr (D0 <= 2) ct_stage_fast<2>(x, q, q2, tw);
@@ -208,7 +262,12 @@ __global__ void __launch_bounds__(256, MINB) ntt2_fwd_cols(LimbMap map, const Mo
   const u64 q = mc[mod].q, q2 = mc[mod].four_q;
   u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + blockIdx.x * COLS;
   const int tid = threadIdx.x, c = tid % COLS, j = tid / COLS;
-  for (int i = tid; i < N1; i += 256) sw[i] = make_ulonglong2(tw[(size_t)mod * N + i], twp[(size_t)mod * N + i]);
+  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
+  const bool fp = fast && kNttFp && q < (1ull << kFpBits);
+  for (int i = tid; i < N1; i += 256) {
+    const u64 wp = twp[(size_t)mod * N + i];
+    sw[i] = make_ulonglong2(tw[(size_t)mod * N + i], fp ? (u64)__double_as_longlong(__ull2double_rn(wp) * 0x1p-64) : wp);
+  }
   u64 x[16];
   if (map.sin) {
     const long long* s = map.sin + (size_t)z * N + blockIdx.x * COLS;
@@ -225,9 +284,9 @@ __global__ void __launch_bounds__(256, MINB) ntt2_fwd_cols(LimbMap map, const Mo
     for (int k = 0; k < 16; ++k) x[k] = ld_last<HINT>(&a[(size_t)(j + T1 * k) * N2 + c]);
   }
   __syncthreads();
-  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
   auto twA = [&](int d, int b) { return sw[(1 << d) + b]; };
-  if (fast) ct16<0, true>(x, q, q2, twA);
+  if (fp) ct16<0, true, decltype(twA), true>(x, q, q2, twA);
+  else if (fast) ct16<0, true>(x, q, q2, twA);
   else ct16<0, false>(x, q, q2, twA);
   if (NSB > 0) {
 #pragma unroll
@@ -236,7 +295,8 @@ __global__ void __launch_bounds__(256, MINB) ntt2_fwd_cols(LimbMap map, const Mo
 #pragma unroll
     for (int k = 0; k < 16; ++k) x[k] = tile[(16 * j + k) * COLS + c];
     auto twB = [&](int d, int b) { return sw[(1 << (d + NSB)) + (j << d) + b]; };
-    if (fast) ct16<4 - NSB, true>(x, q, q2, twB);
+    if (fp) ct16<4 - NSB, true, decltype(twB), true>(x, q, q2, twB);
+    else if (fast) ct16<4 - NSB, true>(x, q, q2, twB);
     else ct16<4 - NSB, false>(x, q, q2, twB);
 #pragma unroll
     for (int k = 0; k < 16; ++k) a[(size_t)(16 * j + k) * N2 + c] = x[k];
@@ -328,8 +388,10 @@ __global__ void __launch_bounds__(128, MINB) ntt2_fwd_chunks(LimbMap map, const 
     for (int b = 0; b < (1 << d); ++b) tb[(1 << d) - 1 + b] = ld_tw<HINT>(&T[(16 << d) - 1 + (j << d) + b], pol);
   __syncwarp();
   const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
+  const bool fp = fast && kNttFp && q < (1ull << kFpBits);  // ctw companions hold double(w/q)
   auto twA = [&](int d, int b) { return twa[cc][(1 << d) - 1 + b]; };
-  if (fast) ct16<0, true>(x, q, q2, twA);
+  if (fp) ct16<0, true, decltype(twA), true>(x, q, q2, twA);
+  else if (fast) ct16<0, true>(x, q, q2, twA);
   else ct16<0, false>(x, q, q2, twA);
 #pragma unroll
   for (int k = 0; k < 16; ++k) tl[17 * k + j] = x[k];
@@ -338,7 +400,8 @@ __global__ void __launch_bounds__(128, MINB) ntt2_fwd_chunks(LimbMap map, const 
   for (int k = 0; k < 16; ++k) x[k] = tl[17 * j + k];
   auto twB = [&](int d, int b) { return tb[(1 << d) - 1 + b]; };
   if (fast) {
-    ct16<0, true>(x, q, q2, twB);
+    if (fp) ct16<0, true, decltype(twB), true>(x, q, q2, twB);
+    else ct16<0, true>(x, q, q2, twB);
     const u64 one_sh = mc[mod].one_sh;
 #pragma unroll
     for (int k = 0; k < 16; ++k) x[k] = shoup_mul(x[k], 1, one_sh, q);  // < 65q -> [0, q)
@@ -437,12 +500,49 @@ __global__ void __launch_bounds__(256) k_bfly_peak(u64* __restrict__ out, const 
   out[t] = acc;
 }
 
+// FP64-quotient variants of the same network (probe only)
+template <bool MAGIC>
+__global__ void __launch_bounds__(256) k_bfly_peak_fp(u64* __restrict__ out, const ulonglong2* __restrict__ tws,
+                                                      u64 q, int iters) {
+  u64 tw[15];
+  double wq[15];
+#pragma unroll
+  for (int i = 0; i < 15; ++i) {
+    tw[i] = tws[i].x;
+    wq[i] = (double)tws[i].x / (double)q;
+  }
+  u64 x[16];
+  const u64 t = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = (t * 16 + k) % q;
+  const u64 q4 = 4 * q;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const int h = 8 >> d;
+#pragma unroll
+      for (int b = 0; b < (1 << d); ++b)
+#pragma unroll
+        for (int r = 0; r < h; ++r)
+          if (MAGIC) ct_bfly_fp2(x[2 * h * b + r], x[2 * h * b + r + h], tw[(1 << d) - 1 + b], wq[(1 << d) - 1 + b], q, q4);
+          else ct_bfly_fp(x[2 * h * b + r], x[2 * h * b + r + h], tw[(1 << d) - 1 + b], wq[(1 << d) - 1 + b], q, q4);
+    }
+    // keep values bounded as in the real network (final reduction of each pass)
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = x[k] >= q4 ? x[k] - q4 : x[k];
+  }
+  u64 acc = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc ^= x[k];
+  out[t] = acc;
+}
+
 // butterflies per second of k_bfly_peak (fast: q < 2^47 unreduced network)
 int ntt_butterfly_peak(int fast, double* bfly_per_s) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const u64 q = fast ? 1099511922689ull : 1152921504606584833ull;  // 40-bit / 60-bit NTT primes
+  const u64 q = fast >= 1 ? 1099511922689ull : 1152921504606584833ull;  // 40-bit / 60-bit NTT primes
   const int threads = 256, blocks = sms * 8, iters = 256;
   ulonglong2 h[15];
   for (int i = 0; i < 15; ++i) {
@@ -462,7 +562,9 @@ int ntt_butterfly_peak(int fast, double* bfly_per_s) {
   float ms = 0.f;
   if (!err) {
     auto go = [&]() {
-      if (fast) k_bfly_peak<true><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
+      if (fast == 3) k_bfly_peak_fp<true><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
+      else if (fast == 2) k_bfly_peak_fp<false><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
+      else if (fast) k_bfly_peak<true><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
       else k_bfly_peak<false><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
     };
     for (int w = 0; w < 3; ++w) go();  // warm-up (clocks ramp)

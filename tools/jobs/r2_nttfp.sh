@@ -1,0 +1,7 @@
+# GPU job: FP64-quotient forward NTT -- parity, NTT microbench, bench
+set -x
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 600 python tools/ntt_bench.py 0,1,0 2>&1 | tail -2
+python bench.py --steps 3 --no-cpu-baseline > gpurun_out/bench_nttfp.log 2>&1; python -c "
+import json;d=json.loads(open('gpurun_out/bench_nttfp.log').read().strip().splitlines()[-1])
+print(d['ms_per_step'], d['roofline']['frac'], d['roofline']['achieved'], {k:(v['share'],v['ms_per_launch'],v['GBps']) for k,v in list(d['kernels'].items())[:10]})"

@@ -31,7 +31,8 @@ def profile(fn, reps=3):
 
 
 def main():
-    settings = [int(v) for v in sys.argv[1:]] or [0, 2, 3, 4]
+    # each argument: comma-separated engine options, e.g. "ks_tma=0,ks_pipe=0"
+    settings = sys.argv[1:] or ["ks_tma=0,ks_pipe=0", "ks_tma=0,ks_pipe=2", "ks_tma=1"]
     cfg = bt.BootConfig()
     params = bt.boot_params("resnet20-16", 1 << 16, 14, cfg)
     steps = [1, 2, 3, 4, 5, 6, 7, 8]
@@ -48,7 +49,9 @@ def main():
         cases[f"hmult_l{level}_nb{nb}"] = (lambda B=B: [ckks.hmult(B, B, ks).data])
     ref = {}
     for pipe in settings:
-        _native.set_option("ks_pipe", pipe)
+        for item in pipe.split(","):
+            key, _, val = item.partition("=")
+            _native.set_option(key, int(val))
         for name, fn in cases.items():
             outs = fn()
             torch.cuda.synchronize()
@@ -57,10 +60,10 @@ def main():
             same = all(torch.equal(a, b) for a, b in zip(ref[name], outs))
             p = profile(fn)
             ki = p.get("ks_inner", {"ms": 0, "GBps": 0})
-            print(json.dumps({"ks_pipe": pipe, "case": name, "bit_identical": same,
+            print(json.dumps({"options": pipe, "case": name, "bit_identical": same,
                               "total_ms": round(sum(v["ms"] for v in p.values()), 3),
                               "ks_inner_ms": round(ki["ms"], 3), "ks_inner_GBps": round(ki["GBps"], 1)}), flush=True)
-            assert same, f"ks_pipe={pipe} changed {name}"
+            assert same, f"{pipe} changed {name}"
 
 
 if __name__ == "__main__":
