@@ -1150,11 +1150,12 @@ __device__ __forceinline__ void mac_stage_bulk(MacStage& S, u64* bar, const MacM
   }
 }
 
+template <int ST>
 __global__ void __launch_bounds__(256) k_mac_multi_tma(MacMulti M, int ng, int nt, u32 nq, u32 logN,
                                                        int accumulate, const ModConsts* __restrict__ mc) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MacStage* S = reinterpret_cast<MacStage*>(smem_raw);
-  __shared__ __align__(8) u64 full[kMacStages];
+  __shared__ __align__(8) u64 full[ST];
   __shared__ unsigned char flags[kMultiT];
   const u32 N = 1u << logN, r = blockIdx.y, k0 = blockIdx.x * kMacTile, tid = threadIdx.x;
   const u64 q = mc[r].q, ninv = mc[r].ninv, one_sh = mc[r].one_sh;
@@ -1165,24 +1166,24 @@ __global__ void __launch_bounds__(256) k_mac_multi_tma(MacMulti M, int ng, int n
     flags[tid] = (unsigned char)fl;
   }
   if (tid == 0) {
-    for (int s = 0; s < kMacStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < kMacStages - 1 && s < nt; ++s) mac_stage_bulk(S[s], &full[s], M, s, flags[s], r, nq, N, k0);
+    for (int s = 0; s < ST - 1 && s < nt; ++s) mac_stage_bulk(S[s], &full[s], M, s, flags[s], r, nq, N, k0);
   u64 h[kMultiG][2], l[kMultiG][2];
 #pragma unroll
   for (int g = 0; g < kMultiG; ++g) h[g][0] = h[g][1] = l[g][0] = l[g][1] = 0;
   for (int t = 0; t < nt; ++t) {
-    if (t > 0) __syncthreads();  // every thread is done with slot (t-1) % kMacStages
+    if (t > 0) __syncthreads();  // every thread is done with slot (t-1) % ST
     if (tid == 0) {
-      const int tn = t + kMacStages - 1;
-      if (tn < nt) mac_stage_bulk(S[tn % kMacStages], &full[tn % kMacStages], M, tn, flags[tn], r, nq, N, k0);
+      const int tn = t + ST - 1;
+      if (tn < nt) mac_stage_bulk(S[tn % ST], &full[tn % ST], M, tn, flags[tn], r, nq, N, k0);
     }
     const u32 fl = flags[t];
-    mbar_wait(&full[t % kMacStages], (u32)(t / kMacStages) & 1u);
-    const MacStage& C = S[t % kMacStages];
+    mbar_wait(&full[t % ST], (u32)(t / ST) & 1u);
+    const MacStage& C = S[t % ST];
     const u64 x0 = C.ct[0][tid], x1 = C.ct[1][tid];
 #pragma unroll
     for (int g = 0; g < kMultiG; ++g) {
@@ -1226,7 +1227,7 @@ __global__ void __launch_bounds__(256) k_mac_multi_tma(MacMulti M, int ng, int n
 // 256-coefficient tile of one output limb r for up to kKsEntries batch
 // entries; per digit j one elected thread bulk-copies the two key rows'
 // tiles (2 x 2 KB) and every entry's raised-digit tile (2 KB each) into a
-// ring of kMacStages stages tracked by mbarriers, so each key tile leaves
+// ring of ST stages tracked by mbarriers, so each key tile leaves
 // HBM once per kKsEntries entries and no thread spends instructions on
 // address generation.  The Galois permutation maps an aligned 256-block of
 // outputs onto one aligned 256-block of sources (the low log2(N)-8 bits of
@@ -1244,6 +1245,7 @@ struct KsStage {
 int g_ks_tma = 1;
 int g_ks_tma_min = 3;  // smallest batch routed to k_ks_inner_tma
 
+template <int ST>
 __global__ void __launch_bounds__(256) k_ks_inner_tma(u64* __restrict__ acc, const u64* __restrict__ x_eval,
                                                       const u64* __restrict__ raised, const u64* __restrict__ key_b,
                                                       const u64* __restrict__ key_a, Basis basis, u32 alpha,
@@ -1252,7 +1254,7 @@ __global__ void __launch_bounds__(256) k_ks_inner_tma(u64* __restrict__ acc, con
                                                       size_t c0_bst, const u64* __restrict__ pR, u32 key_lq) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KsStage* S = reinterpret_cast<KsStage*>(smem_raw);
-  __shared__ __align__(8) u64 full[kMacStages];
+  __shared__ __align__(8) u64 full[ST];
   const u32 N = 1u << logN, r = blockIdx.y, tile = blockIdx.x, tid = threadIdx.x;
   const u32 b0 = blockIdx.z * kKsEntries;
   const u32 ne = nb - b0 < (u32)kKsEntries ? nb - b0 : (u32)kKsEntries;
@@ -1271,8 +1273,8 @@ __global__ void __launch_bounds__(256) k_ks_inner_tma(u64* __restrict__ acc, con
   const bool ext = c0 != nullptr && r < basis.nq;
   const u32 nst = ndig + (ext ? 1u : 0u);
   auto issue = [&](u32 j) {
-    KsStage& T = S[j % kMacStages];
-    u64* bar = &full[j % kMacStages];
+    KsStage& T = S[j % ST];
+    u64* bar = &full[j % ST];
     if (j < ndig) {
       mbar_expect_tx(bar, (2 + ne) * kMacTile * 8);
       const size_t kofs = (size_t)j * key_dst + (size_t)kmod * N + (size_t)tile * kMacTile;
@@ -1290,20 +1292,20 @@ __global__ void __launch_bounds__(256) k_ks_inner_tma(u64* __restrict__ acc, con
     }
   };
   if (tid == 0) {
-    for (int s = 0; s < kMacStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (tid == 0)
-    for (u32 j = 0; j < (u32)kMacStages - 1 && j < nst; ++j) issue(j);
+    for (u32 j = 0; j < (u32)ST - 1 && j < nst; ++j) issue(j);
   u64 bh[kKsEntries], bl[kKsEntries], ah[kKsEntries], al[kKsEntries];
 #pragma unroll
   for (int e = 0; e < kKsEntries; ++e) bh[e] = bl[e] = ah[e] = al[e] = 0;
   for (u32 j = 0; j < nst; ++j) {
-    if (j > 0) __syncthreads();  // slot (j-1) % kMacStages is free
-    if (tid == 0 && j + kMacStages - 1 < nst) issue(j + kMacStages - 1);
-    mbar_wait(&full[j % kMacStages], (j / kMacStages) & 1u);
-    const KsStage& T = S[j % kMacStages];
+    if (j > 0) __syncthreads();  // slot (j-1) % ST is free
+    if (tid == 0 && j + ST - 1 < nst) issue(j + ST - 1);
+    mbar_wait(&full[j % ST], (j / ST) & 1u);
+    const KsStage& T = S[j % ST];
     if (j < ndig) {
       const u64 kb = T.kb[tid], ka = T.ka[tid];
 #pragma unroll
@@ -1339,6 +1341,7 @@ __global__ void __launch_bounds__(256) k_ks_inner_tma(u64* __restrict__ acc, con
 }
 
 int g_mac_tma = 1;    // 1: bulk-copy (TMA) staged k_mac_multi_tma
+int g_tma_stages = 4;  // ring depth of the TMA-staged MAC / key-switch kernels (4, 6, 8)
 int g_mac_async = 1;  // 1: cp.async pipeline (k_mac_multi_async), 0: k_mac_multi_lanes
 
 int g_mac_lanes = 1;  // 1: k_mac_multi_lanes, 0: register-blocked k_mac_multi
@@ -1347,16 +1350,21 @@ cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN
                              const ModConsts* mc, cudaStream_t st) {
   if (ng < 1 || ng > kMultiG) return cudaErrorInvalidValue;
   if (g_mac_tma && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
-    static bool attr_tma = false;
-    const size_t sm = sizeof(MacStage) * kMacStages;
-    if (!attr_tma) {
-      cudaError_t e = cudaFuncSetAttribute(k_mac_multi_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e) return e;
-      attr_tma = true;
-    }
     dim3 g((1u << logN) / kMacTile, nq, 1);
-    k_mac_multi_tma<<<g, 256, sm, st>>>(M, ng, nt, nq, logN, accumulate, mc);
-    return cudaGetLastError();
+    static bool attr_done[9] = {};
+    auto go = [&](auto kern, int stages) -> cudaError_t {
+      const size_t sm = sizeof(MacStage) * stages;
+      if (!attr_done[stages]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e) return e;
+        attr_done[stages] = true;
+      }
+      kern<<<g, 256, sm, st>>>(M, ng, nt, nq, logN, accumulate, mc);
+      return cudaGetLastError();
+    };
+    if (g_tma_stages >= 8) return go(k_mac_multi_tma<8>, 8);
+    if (g_tma_stages >= 6) return go(k_mac_multi_tma<6>, 6);
+    return go(k_mac_multi_tma<4>, 4);
   }
   if (g_mac_async && (1u << logN) % kMacTile == 0) {
     static bool attr = false;
@@ -1521,17 +1529,23 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
   // TMA staging pays once a key tile feeds >= 3 entries; small batches keep
   // the register-pipelined kernel (measured: tools/ks_bench.py)
   if (g_ks_tma && nb >= (u32)g_ks_tma_min && (1u << logN) % kMacTile == 0) {
-    static bool attr_ks = false;
-    const size_t sm = sizeof(KsStage) * kMacStages;
-    if (!attr_ks) {
-      cudaError_t e = cudaFuncSetAttribute(k_ks_inner_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e) return e;
-      attr_ks = true;
-    }
     const u32 nbb = nb ? nb : 1;
     dim3 grid((1u << logN) / kMacTile, basis.nlimbs(), (nbb + kKsEntries - 1) / kKsEntries);
-    k_ks_inner_tma<<<grid, 256, sm, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nbb,
-                                          x_bst, c0, c0_bst, pR, key_lq);
+    static bool attr_done[9] = {};
+    auto go = [&](auto kern, int stages) -> cudaError_t {
+      const size_t sm = sizeof(KsStage) * stages;
+      if (!attr_done[stages]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e) return e;
+        attr_done[stages] = true;
+      }
+      kern<<<grid, 256, sm, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nbb, x_bst, c0,
+                                  c0_bst, pR, key_lq);
+      return cudaGetLastError();
+    };
+    cudaError_t e = g_tma_stages >= 8 ? go(k_ks_inner_tma<8>, 8)
+                    : g_tma_stages >= 6 ? go(k_ks_inner_tma<6>, 6) : go(k_ks_inner_tma<4>, 4);
+    if (e) return e;
   } else if ((nb <= 1 || g_ks_batch <= 1) && g_ks_pipe > 0) {
     dim3 grid = row_grid((1u << logN) / 2, basis.nlimbs(), 256);
     grid.x *= (nb ? nb : 1);

@@ -35,6 +35,7 @@ extern int g_mac_batch;
 extern int g_mac_lanes;
 extern int g_mac_async;
 extern int g_mac_tma;
+extern int g_tma_stages;
 // c0 (nullable): adds P * sigma_g(c0) on the Q limbs (pR[i] = P R mod q_i) --
 // the extended-basis (ModDown-free) rotation of double hoisting
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,

@@ -339,7 +339,8 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
   u64 qmax = 0;
   for (u64 q : c->mods) {
     qmax = q > qmax ? q : qmax;
-    c->small.push_back(q < (1ull << 47) ? 1 : 0);
+    // NTT modulus class: 2 = FP64-quotient forward path, 1 = q < 2^47 fast path, 0 = full width
+    c->small.push_back(q < (1ull << kFpBits) ? 2 : q < (1ull << 47) ? 1 : 0);
   }
   c->ntt2_ok = ntt2_supported(c->logN) && qmax < (1ull << 61);  // 8q < 2^64 (approximate-quotient NTT)
   if (c->ntt2_ok) {
@@ -1120,12 +1121,13 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "mac_lanes") g_mac_lanes = (int)value;
   else if (k == "mac_async") g_mac_async = (int)value;
   else if (k == "mac_tma") g_mac_tma = (int)value;
+  else if (k == "tma_stages") g_tma_stages = (int)value;
   else if (k == "merge_moddown") g_merge_moddown = (int)value;
   else return fail(HCNN_E_PARAMETER, "unknown option " + k);
   return HCNN_OK;
 }
 
-unsigned long long hcnn_kernel_launches(void) { return g_kernels.load(); }
+unsigned long long hcnn_kernel_launches(void) { return g_kernels.load() + g_ntt_extra_launches.load(); }
 
 int hcnn_ntt_butterfly_peak(int device, int fast, double* bfly_per_s) {
   if (!bfly_per_s) return fail(HCNN_E_PARAMETER, "null output");

@@ -1,5 +1,7 @@
 // Kernel-level interfaces shared between the .cu translation units.
 #pragma once
+#include <atomic>
+
 #include "common.cuh"
 
 namespace hcnn {
@@ -29,7 +31,7 @@ struct NttTuning {
   int group_limbs = 0;
   int hints = 1;
   int occupancy = 0;  // 1: register-capped kernels (more resident warps)
-  int split = 0;      // 1: separate launches per modulus class
+  int split = 2;      // 1: separate launches per modulus class, 2: forward transforms only
 };
 extern NttTuning g_ntt_tuning;
 
@@ -42,7 +44,7 @@ struct NttTables {
   const u64* itwp;
   const ulonglong2* ctw;   // [mod][N/256][256] per-chunk forward twiddles (ntt2.cu)
   const ulonglong2* ictw;  // [mod][N/256][256] per-chunk inverse twiddles
-  const unsigned char* small;  // host: per modulus index, q < 2^47 (unreduced fast path)
+  const unsigned char* small;  // host: per modulus index, 2: q < 2^kFpBits, 1: q < 2^47, 0: full width
 };
 
 void ntt_split(u32 logN, u32* logN1);
@@ -56,6 +58,7 @@ int ntt_butterfly_peak(int fast, double* bfly_per_s);
 constexpr int kFpBits = 44;
 constexpr bool kNttFp = true;
 extern unsigned long long g_ntt_limbs[4];
+extern std::atomic<unsigned long long> g_ntt_extra_launches;  // split NTT launches beyond one pair per call
 cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 npolys, bool inverse,
                         cudaStream_t st);
 

@@ -16,6 +16,8 @@
 // Forward keeps Harvey-lazy values in [0,4q) between passes and fully
 // reduces at the end; inverse keeps [0,2q) and folds N^-1 into the last
 // Gentleman-Sande stage.
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -262,8 +264,10 @@ __global__ void __launch_bounds__(256, MINB) ntt2_fwd_cols(LimbMap map, const Mo
   const u64 q = mc[mod].q, q2 = mc[mod].four_q;
   u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + blockIdx.x * COLS;
   const int tid = threadIdx.x, c = tid % COLS, j = tid / COLS;
-  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
-  const bool fp = fast && kNttFp && q < (1ull << kFpBits);
+  // MODE 0: full-width, 1: q < 2^47 integer fast path, 3: FP64-quotient
+  // path (q < 2^kFpBits), 2: chosen per limb at run time
+  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1 || MODE == 3);
+  const bool fp = MODE == 3 || (MODE == 2 && kNttFp && q < (1ull << kFpBits));
   for (int i = tid; i < N1; i += 256) {
     const u64 wp = twp[(size_t)mod * N + i];
     sw[i] = make_ulonglong2(tw[(size_t)mod * N + i], fp ? (u64)__double_as_longlong(__ull2double_rn(wp) * 0x1p-64) : wp);
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(256, MINB) ntt2_inv_cols(LimbMap map, const Mo
   __syncthreads();
   // stages t = 1..8 rows: contiguous groups of 16 rows; twiddle itw[H + i],
   // H = N1 >> (d+1) blocks, i = j*(8>>d) + b
-  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
+  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1 || MODE == 3);
   auto twB = [&](int d, int b) { return sw[(N1 >> (d + 1)) + j * (8 >> d) + b]; };
   auto twA = [&](int d, int b) { return sw[(8 >> d) + b]; };
   if (NSA == 0) {
@@ -387,8 +391,8 @@ __global__ void __launch_bounds__(128, MINB) ntt2_fwd_chunks(LimbMap map, const 
 #pragma unroll
     for (int b = 0; b < (1 << d); ++b) tb[(1 << d) - 1 + b] = ld_tw<HINT>(&T[(16 << d) - 1 + (j << d) + b], pol);
   __syncwarp();
-  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
-  const bool fp = fast && kNttFp && q < (1ull << kFpBits);  // ctw companions hold double(w/q)
+  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1 || MODE == 3);
+  const bool fp = MODE == 3 || (MODE == 2 && kNttFp && q < (1ull << kFpBits));  // ctw companions hold double(w/q)
   auto twA = [&](int d, int b) { return twa[cc][(1 << d) - 1 + b]; };
   if (fp) ct16<0, true, decltype(twA), true>(x, q, q2, twA);
   else if (fast) ct16<0, true>(x, q, q2, twA);
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(128, MINB) ntt2_inv_chunks(LimbMap map, const 
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 16; ++k) x[k] = tl[17 * j + k];
-  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1);
+  const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1 || MODE == 3);
   auto twB = [&](int d, int b) { return tb[16 - (16 >> d) + b]; };
   if (fast) gs16<0, false, true>(x, q, q2, twB, C, 0);
   else gs16<0, false, false>(x, q, q2, twB, C);
@@ -589,10 +593,11 @@ int ntt_butterfly_peak(int fast, double* bfly_per_s) {
 
 // limbs transformed per class since the last read: [fwd fast, fwd full, inv fast, inv full]
 unsigned long long g_ntt_limbs[4] = {0, 0, 0, 0};
+std::atomic<unsigned long long> g_ntt_extra_launches{0};
 
 static void count_limbs(const NttTables& T, const LimbMap& m, u32 ny, u32 nz, bool inverse) {
   for (u32 r = 0; r < ny; ++r) {
-    const bool f = T.small && T.small[m.basis.mod_of(m.r0 + r + m.first_limb)];
+    const bool f = T.small && T.small[m.basis.mod_of(m.r0 + r + m.first_limb)] != 0;
     g_ntt_limbs[(inverse ? 2 : 0) + (f ? 0 : 1)] += nz;
   }
 }
@@ -641,24 +646,30 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
   const bool occ = g_ntt_tuning.occupancy != 0;
   // split: one launch pair per run of limbs of one modulus class (uniform
   // kernels); otherwise one launch pair dispatching per limb at run time
-  const bool split = g_ntt_tuning.split != 0;
+  // split 1: per-class launches both directions, 2: forward only (the
+  // forward variants differ -- FP64 vs integer quotient -- so per-class
+  // kernels are smaller; the inverse keeps one run-time-dispatch launch)
+  const bool split = g_ntt_tuning.split == 1 || (g_ntt_tuning.split == 2 && !inverse);
   auto one = [&](const LimbMap& m, u32 ny, u32 nz, int mode) -> cudaError_t {
     if (mode == 0) return occ ? launch_pair<true, 1, 0>(T, m, ny, nz, inverse, st)
                               : launch_pair<true, 0, 0>(T, m, ny, nz, inverse, st);
     if (mode == 1) return occ ? launch_pair<true, 1, 1>(T, m, ny, nz, inverse, st)
                               : launch_pair<true, 0, 1>(T, m, ny, nz, inverse, st);
+    if (mode == 3) return launch_pair<true, 0, 3>(T, m, ny, nz, inverse, st);
     return occ ? launch_pair<true, 1, 2>(T, m, ny, nz, inverse, st) : launch_pair<true, 0, 2>(T, m, ny, nz, inverse, st);
   };
   auto pair = [&](const LimbMap& m, u32 ny, u32 nz) -> cudaError_t {
     if (!split || !T.small) return one(m, ny, nz, 2);
     u32 r = 0;
     while (r < ny) {
-      const bool f = T.small[m.basis.mod_of(m.r0 + r + m.first_limb)];
+      const unsigned char f = T.small[m.basis.mod_of(m.r0 + r + m.first_limb)];
       u32 e = r + 1;
-      while (e < ny && (bool)T.small[m.basis.mod_of(m.r0 + e + m.first_limb)] == f) ++e;
+      while (e < ny && T.small[m.basis.mod_of(m.r0 + e + m.first_limb)] == f) ++e;
       LimbMap mm = m;
       mm.r0 = m.r0 + r;
-      cudaError_t err = one(mm, e - r, nz, f ? 1 : 0);
+      // class 2 (FP64-quotient moduli): MODE 3 forward, integer fast inverse
+      cudaError_t err = one(mm, e - r, nz, f == 2 ? (kNttFp ? 3 : 1) : f);
+      if (r > 0) g_ntt_extra_launches += 2;  // launch accounting counts one pair per call
       if (err) return err;
       r = e;
     }
