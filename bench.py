@@ -216,8 +216,17 @@ def int_roofline(roof: dict, prof: dict, limbs: dict, n: int) -> dict:
     achieved = bfly / (ms / 1e3)
     peak = bfly / ideal_s
     hbm = {k: roof[k] for k in ("achieved", "peak", "unit", "frac", "peak_source", "algorithmic_bytes_per_launch")}
+    # DRAM traffic per launch from the committed ncu --set full capture, scaled per limb
+    traffic = roof.get("traffic")
+    tf = ROOT / "profiles" / "r01_ncu_ntt_traffic.json"
+    if traffic is None and fam == "ntt_fwd" and tf.exists():
+        per_limb = json.loads(tf.read_text())["dram_bytes_per_limb"]
+        launches = sum(v["launches"] for k, v in prof.items() if _kernel_family(k) == fam)
+        traffic = round(per_limb * (fast + full) / max(launches, 1))
+        hbm["traffic_source"] = ("profiles/r01_ncu_ntt_traffic.json (ncu, cold L2) x mean limbs per launch "
+                                 "(one launch = the cols + chunks pass pair)")
     out = {"kernel": fam, "bound": "int", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
-           "unit": "Gbutterfly/s", "frac": round(ideal_s / (ms / 1e3), 4), "traffic": roof.get("traffic"),
+           "unit": "Gbutterfly/s", "frac": round(ideal_s / (ms / 1e3), 4), "traffic": traffic,
            "peak_source": (f"measured on this GPU: radix-16 register network without memory traffic "
                            f"(hcnn_ntt_butterfly_peak) {pf/1e9:.1f} Gbfly/s for the FP64-quotient network of "
                            f"q<2^44 limbs, {ps/1e9:.1f} for full-width limbs, weighted by this image's {fast} + {full} limbs"),
