@@ -1093,12 +1093,22 @@ int hcnn_rescale(hcnn_ctx* c, uint64_t* out, const uint64_t* in, uint32_t level,
   m.basis = c->basis(l + 1, 0);
   m.first_limb = l;
   PK("ntt_inv_rescale", 16.0 * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), m, 1, npolys, true, STREAM(s)));
-  PK("rescale_lift", 8.0 * (l + 1) * npolys * c->n, 1, STREAM(s), launch_rescale_lift(out, top, l, c->logN, npolys, c->d_qmod + (size_t)l * c->Lq, c->d_mc, STREAM(s)));
   LimbMap o{};
   o.base = out;
   o.poly_stride = (size_t)l * c->n;
   o.basis = c->basis(l, 0);
-  PK("ntt_fwd_rescale", 16.0 * l * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), o, l, npolys, false, STREAM(s)));
+  if (c->tables().ctw) {
+    // the column pass lifts the (centred) top limb into every q_i on load:
+    // no lift kernel, one shared row per poly instead of l lifted rows
+    o.sin = (const long long*)top;
+    o.smont = 0;
+    o.sin_center = c->hmc[l].q;
+    PK("ntt_fwd_rescale", 8.0 * (1 + 2.0 * l) * npolys * c->n, ntt_nk(c), STREAM(s),
+       launch_ntt(c->tables(), o, l, npolys, false, STREAM(s)));
+  } else {
+    PK("rescale_lift", 8.0 * (l + 1) * npolys * c->n, 1, STREAM(s), launch_rescale_lift(out, top, l, c->logN, npolys, c->d_qmod + (size_t)l * c->Lq, c->d_mc, STREAM(s)));
+    PK("ntt_fwd_rescale", 16.0 * l * npolys * c->n, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), o, l, npolys, false, STREAM(s)));
+  }
   PK("rescale_combine", 24.0 * l * npolys * c->n, 1, STREAM(s), launch_rescale_combine(out, in, l, c->logN, npolys, c->d_rinv + (size_t)l * c->Lq,
                             c->d_rinv_sh + (size_t)l * c->Lq, c->d_mc, STREAM(s)));
   return HCNN_OK;

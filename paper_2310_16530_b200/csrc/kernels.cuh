@@ -23,6 +23,9 @@ struct LimbMap {
   // smont: Montgomery form (v R mod q).  Fuses from_signed into the NTT.
   const long long* sin;
   int smont;
+  // sin_center != 0: the row holds residues mod sin_center (a rescale's top
+  // limb after its iNTT), read as the centred lift t > q/2 ? t - q : t
+  u64 sin_center;
 };
 
 // tuning knobs (hcnn_set_option): NTT sub-batch size in limbs (0 = one

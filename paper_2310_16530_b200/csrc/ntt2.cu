@@ -278,7 +278,11 @@ __global__ void __launch_bounds__(256, MINB) ntt2_fwd_cols(LimbMap map, const Mo
     const u64 kr = map.smont ? mc[mod].r2 : mc[mod].one_m, ninv = mc[mod].ninv;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      const long long v = s[(size_t)(j + T1 * k) * N2 + c];
+      long long v = s[(size_t)(j + T1 * k) * N2 + c];
+      if (map.sin_center) {  // centred lift of a residue mod sin_center (fused rescale, ckks.py:506-528)
+        const u64 t = (u64)v;
+        v = t > (map.sin_center >> 1) ? (long long)(t - map.sin_center) : (long long)t;
+      }
       const u64 mag = v >= 0 ? (u64)v : (u64)(-(v + 1)) + 1ull;
       const u64 red = mont_mul(mag, kr, q, ninv);
       x[k] = v >= 0 ? red : neg_mod(red, q);
@@ -606,8 +610,8 @@ bool ntt2_supported(u32 logN) { return logN >= 12 && logN <= 16; }
 
 template <int L, bool H, int OCC, int F>
 static void launch_cols_t(bool inv, dim3 g, const LimbMap& map, const NttTables& T, cudaStream_t st) {
-  if (inv) ntt2_inv_cols<L, H, OCC ? 3 : 1, F><<<g, 256, 0, st>>>(map, T.mc, T.itw, T.itwp, T.logN);
-  else ntt2_fwd_cols<L, H, OCC ? 3 : 1, F><<<g, 256, 0, st>>>(map, T.mc, T.tw, T.twp, T.logN);
+  if (inv) ntt2_inv_cols<L, H, OCC == 1 ? 3 : 1, F><<<g, 256, 0, st>>>(map, T.mc, T.itw, T.itwp, T.logN);
+  else ntt2_fwd_cols<L, H, OCC == 1 ? 3 : 1, F><<<g, 256, 0, st>>>(map, T.mc, T.tw, T.twp, T.logN);
 }
 
 template <bool H, int OCC, int F>
@@ -629,9 +633,9 @@ static cudaError_t launch_pair(const NttTables& T, const LimbMap& map, u32 ny, u
   };
   if (!inverse) {
     if (!cols_launch(false)) return cudaErrorInvalidValue;
-    ntt2_fwd_chunks<H, OCC ? 5 : 1, F><<<gk, 128, 0, st>>>(map, T.mc, T.ctw, logN);
+    ntt2_fwd_chunks<H, OCC == 1 ? 5 : OCC == 2 ? 4 : 1, F><<<gk, 128, 0, st>>>(map, T.mc, T.ctw, logN);
   } else {
-    ntt2_inv_chunks<H, OCC ? 5 : 1, F><<<gk, 128, 0, st>>>(map, T.mc, T.ictw, logN);
+    ntt2_inv_chunks<H, OCC == 1 ? 5 : OCC == 2 ? 4 : 1, F><<<gk, 128, 0, st>>>(map, T.mc, T.ictw, logN);
     if (!cols_launch(true)) return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -643,7 +647,7 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
                         cudaStream_t st) {
   if (nlimbs == 0 || npolys == 0) return cudaSuccess;
   const bool hint = g_ntt_tuning.hints != 0;
-  const bool occ = g_ntt_tuning.occupancy != 0;
+  const bool occ = g_ntt_tuning.occupancy == 1;
   // split: one launch pair per run of limbs of one modulus class (uniform
   // kernels); otherwise one launch pair dispatching per limb at run time
   // split 1: per-class launches both directions, 2: forward only (the
@@ -651,11 +655,14 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
   // kernels are smaller; the inverse keeps one run-time-dispatch launch)
   const bool split = g_ntt_tuning.split == 1 || (g_ntt_tuning.split == 2 && !inverse);
   auto one = [&](const LimbMap& m, u32 ny, u32 nz, int mode) -> cudaError_t {
-    if (mode == 0) return occ ? launch_pair<true, 1, 0>(T, m, ny, nz, inverse, st)
-                              : launch_pair<true, 0, 0>(T, m, ny, nz, inverse, st);
+    if (mode == 0) return g_ntt_tuning.occupancy == 2 ? launch_pair<true, 2, 0>(T, m, ny, nz, inverse, st)
+                          : occ ? launch_pair<true, 1, 0>(T, m, ny, nz, inverse, st)
+                                : launch_pair<true, 0, 0>(T, m, ny, nz, inverse, st);
     if (mode == 1) return occ ? launch_pair<true, 1, 1>(T, m, ny, nz, inverse, st)
                               : launch_pair<true, 0, 1>(T, m, ny, nz, inverse, st);
-    if (mode == 3) return launch_pair<true, 0, 3>(T, m, ny, nz, inverse, st);
+    // occupancy 2: chunk pass capped at 128 registers (4 CTAs of 128 threads per SM), cols unchanged
+    if (mode == 3) return g_ntt_tuning.occupancy == 2 ? launch_pair<true, 2, 3>(T, m, ny, nz, inverse, st)
+                                                      : launch_pair<true, 0, 3>(T, m, ny, nz, inverse, st);
     return occ ? launch_pair<true, 1, 2>(T, m, ny, nz, inverse, st) : launch_pair<true, 0, 2>(T, m, ny, nz, inverse, st);
   };
   auto pair = [&](const LimbMap& m, u32 ny, u32 nz) -> cudaError_t {

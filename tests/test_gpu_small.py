@@ -242,3 +242,30 @@ def test_truncated_rotation_keys(small, cts):
     assert torch.equal(ckks.unstack(many[1])[1].data, ckks.rotate(low, 4, ks).data)
     with pytest.raises(KeyError_):
         ckks.rotate(ct1, 1, kt)
+
+
+def test_lazy_mac_worst_case_residues(small):
+    """Lazy 128-bit MACs fold the high word every 8 products and the plane MAC
+    chunks its term list by 48: with every residue at q-1 (the largest
+    products) and 53 terms (folds at 8, 16, ..., a 48 + 5 chunk split, mixed
+    packed / unpacked masks) the outputs still equal sum (q-1)^2 R^-1 mod q."""
+    import torch
+    params, ks = small
+    ctx = params.ctx
+    lvl = params.max_level
+    qs = [m.q for m in params.q_mods[: lvl + 1]]
+    n = params.n
+    full = torch.tensor([[q - 1] * n for q in qs], dtype=torch.int64, device=ctx.torch_device)
+    ct = torch.stack([full, full]).contiguous()
+    T = 53
+    cts = [ct] * T
+    masks = [[full.clone() for _ in range(T)], [full.clone() for _ in range(T)]]
+    masks[1] = [ctx.pack_masks(m, lvl)[0] if t % 2 else m for t, m in enumerate(masks[1])]
+    got = ctx.mac_terms_multi(cts, masks, lvl)
+    got_terms = ctx.mac_terms(cts, masks[0], lvl)
+    for i, q in enumerate(qs):
+        r_inv = pow(1 << 64, -1, q)
+        want = T * (q - 1) * (q - 1) * r_inv % q
+        for out in (got[0], got[1], got_terms):
+            row = out[:, i].cpu().numpy().view(np.uint64)
+            assert (row == np.uint64(want)).all(), (i, q)
