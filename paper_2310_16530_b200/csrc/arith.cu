@@ -339,22 +339,33 @@ __global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, 
   __syncthreads();
   const u64* src = in + (size_t)b * in_bst + (size_t)z * in_pst;
   u64* dst = out + (size_t)b * out_bst + (size_t)z * out_pst;
-  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
-    u64 y[NS];
-    u32 mask = 0;
+  // two adjacent coefficients per thread: every per-target constant read from
+  // shared memory serves both, and loads / stores are 16 bytes
+  for (u32 kv = blockIdx.x * blockDim.x + threadIdx.x; kv < N / 2; kv += gridDim.x * blockDim.x) {
+    const u32 k = 2 * kv;
+    u64 y0[NS], y1[NS];
+    u32 m0 = 0, m1 = 0;
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
-      y[i] = shoup_mul(src[(size_t)i * N + k], ip[i], ips[i], qi[i]);
-      mask |= (y[i] > hq[i] ? 1u : 0u) << i;
+      const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src + (size_t)i * N + k);
+      y0[i] = shoup_mul(x.x, ip[i], ips[i], qi[i]);
+      y1[i] = shoup_mul(x.y, ip[i], ips[i], qi[i]);
+      m0 |= (y0[i] > hq[i] ? 1u : 0u) << i;
+      m1 |= (y1[i] > hq[i] ? 1u : 0u) << i;
     }
-#pragma unroll 4
+#pragma unroll 2
     for (u32 t = 0; t < nt; ++t) {
-      const u64 qt = s_q[t];
-      u64 hi = 0, lo = 0;
+      const u64 qt = s_q[t], ni = s_ninv[t];
+      u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
 #pragma unroll
-      for (int i = 0; i < NS; ++i) mac128_lazy(hi, lo, y[i], s_tm[t * NS + i]);  // NS <= 6 < kLazyTerms
-      u64 v = redc128(hi, lo, qt, s_ninv[t]);
-      dst[s_pos[t] + k] = sub_mod(v, s_corr[t * NM + mask], qt);
+      for (int i = 0; i < NS; ++i) {  // NS <= 6 < kLazyTerms
+        const u64 b = s_tm[t * NS + i];
+        mac128_lazy(h0, l0, y0[i], b);
+        mac128_lazy(h1, l1, y1[i], b);
+      }
+      const u64 v0 = sub_mod(redc128(h0, l0, qt, ni), s_corr[t * NM + m0], qt);
+      const u64 v1 = sub_mod(redc128(h1, l1, qt, ni), s_corr[t * NM + m1], qt);
+      *reinterpret_cast<ulonglong2*>(dst + s_pos[t] + k) = make_ulonglong2(v0, v1);
     }
   }
 }
@@ -1459,7 +1470,7 @@ template <int NS>
 static cudaError_t launch_fbc_t(const FbcDev* tabs, int tab_per_z, const ModConsts* mc, const u64* in,
                                 size_t in_pst, u64* out, size_t out_pst, u32 logN, u32 nz, u32 z0, u32 nt,
                                 u32 nt_override, u32 nb, size_t in_bst, size_t out_bst, cudaStream_t st) {
-  dim3 g = row_grid(1u << logN, nz * nb, 256);
+  dim3 g = row_grid((1u << logN) / 2, nz * nb, 256);  // two coefficients per thread
   const u32 tg = fbc_group(nt, g.x * g.y);
   size_t sm = fbc_smem(tg, NS);
   if (sm > 48 * 1024) {
