@@ -1,0 +1,6 @@
+# GPU job: zero-copy stacking of unstacked batches, batched residual adds -- parity + bench
+set -x
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+python bench.py --steps 3 --no-cpu-baseline > gpurun_out/bench_zc.log 2>&1; python -c "
+import json;d=json.loads(open('gpurun_out/bench_zc.log').read().strip().splitlines()[-1])
+print(d['ms_per_step'], d['gpu_launches'], d['logits_check'], {k:(v['share'],v['ms_per_launch'],v['launches']) for k,v in list(d['kernels'].items())[:14]})"
