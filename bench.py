@@ -79,6 +79,13 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout: float = 5.0) -> None:
+        """block until nvidia-smi has produced a sample (its start-up takes
+        longer than a short timed region)"""
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -348,6 +355,7 @@ def run_resnet20(args, d: Dist):
         step()
     sampler = ClockSampler(d.local)
     sampler.start()
+    sampler.wait_first()
     ms = timed_steps(d, step, args.steps, nvtx="timed")
     clocks = sampler.stop()
     ms_img = ms / args.steps
@@ -435,6 +443,7 @@ def run_cfg2(args, d: Dist):
         step()
     sampler = ClockSampler(d.local)
     sampler.start()
+    sampler.wait_first()
     k0 = _native.kernel_launches()
     ms = timed_steps(d, step, args.steps)
     launches = _native.kernel_launches() - k0
