@@ -108,3 +108,23 @@ def test_ntt_from_signed_fused(logn, mont):
         want = np.stack([O.ntt(np.stack([(rows[p].astype(object) % q).astype(np.uint64) for q in qs]), qs)
                          for p in range(5)])
         assert np.array_equal(to_host_u64(fused), want)
+
+
+def test_roofline_instrumentation():
+    """bench.py's integer roofline: the butterfly-rate probes run and order
+    as measured (FP64 quotient > integer fast > full width), and the limb
+    counters classify one forward + one inverse transform by modulus width."""
+    from paper_2310_16530_b200 import _native
+    from paper_2310_16530_b200.engine import context_for, to_device_u64
+    fp, fast, full = (_native.ntt_butterfly_peak(k) for k in (2, 1, 0))
+    assert fp > 0 and fast > 0 and full > 0
+    assert fast > full  # the unreduced network issues fewer instructions
+    n = 1 << 16
+    qs = _mods(n)  # 59-bit (full), 40-bit (FP64 class), 45-bit (integer fast class)
+    ctx = context_for(n, qs)
+    d = to_device_u64(np.zeros((2, len(qs), n), dtype=np.uint64))
+    _native.ntt_limb_counts(reset=True)
+    ctx.ntt(d, len(qs))
+    ctx.ntt(d, len(qs), inverse=True)
+    c = _native.ntt_limb_counts(reset=True)
+    assert c == {"fwd_fast": 4, "fwd_full": 2, "inv_fast": 4, "inv_full": 2}
