@@ -149,14 +149,15 @@ int hcnn_mac_terms_multi(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* c
                          int accumulate, void* stream);
 
 /* as hcnn_mac_terms_multi; packed[g*n_terms+t] = 1 marks a mask stored in
- * the 48-bit packed layout of hcnn_pack_masks (nullable: none packed) */
+ * the packed layout of hcnn_pack_masks (nullable: none packed) */
 int hcnn_mac_terms_multi_packed(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* const* cts,
                                 const uint64_t* const* masks_mont, const unsigned char* packed, uint32_t n_out,
                                 uint32_t n_terms, uint32_t level, int accumulate, void* stream);
 /* Resident mask compaction: n_masks Montgomery rows [n][level+1][N] ->
- * (8 + 6 level) N bytes each (limb 0 as u64, limbs 1.. as u32 + u16 planes);
- * only for chains whose q_1..q_level are < 2^48 (HCNN_E_BASIS otherwise).
- * Lossless; hcnn_unpack_mask restores one mask's rows. */
+ * (8 + 4 level + sum_r hb_r) N bytes each: limb 0 as u64, limbs 1.. as u32
+ * low-word planes, then one high plane per limb, u8 when q_r < 2^40 and u16
+ * otherwise (hb_r = 1 or 2); only for chains whose q_1..q_level are < 2^48
+ * (HCNN_E_BASIS otherwise).  Lossless; hcnn_unpack_mask restores one mask's rows. */
 int hcnn_pack_masks(hcnn_ctx* ctx, void* out, const uint64_t* in, uint32_t n_masks, uint32_t level, void* stream);
 int hcnn_unpack_mask(hcnn_ctx* ctx, uint64_t* out, const void* in, uint32_t level, void* stream);
 

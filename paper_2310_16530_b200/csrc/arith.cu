@@ -822,7 +822,8 @@ __global__ void __launch_bounds__(256) k_mac_multi(MacMulti M, int nt, u32 nq, u
     const u32 k = VEC * kv;
     // byte offsets of this thread's coefficient in a packed mask's planes (limb r > 0)
     const size_t lo_off = 8 * (size_t)N + 4 * ((size_t)(r - 1) * N + k);
-    const size_t hi_off = 8 * (size_t)N + 4 * (size_t)(nq - 1) * N + 2 * ((size_t)(r - 1) * N + k);
+    const unsigned hb = r > 0 ? packed_hb(r, M.wide) : 2u;
+    const size_t hi_plane = r > 0 ? packed_hi_off(r, nq, N, M.wide) : 0;
     u64 hi[G][2][VEC], lo[G][2][VEC];
 #pragma unroll
     for (int g = 0; g < G; ++g)
@@ -851,14 +852,13 @@ __global__ void __launch_bounds__(256) k_mac_multi(MacMulti M, int nt, u32 nq, u
         const u64* mp = M.mask[g][t];
         if (mp && M.packed[g][t] && r > 0) {  // 48-bit packed limb: u32 low plane + u16 high plane
           const char* b = reinterpret_cast<const char*>(mp);
+          const unsigned char* hp = reinterpret_cast<const unsigned char*>(b + hi_plane);
           if (VEC == 2) {
             const uint2 l2 = *reinterpret_cast<const uint2*>(b + lo_off);
-            const unsigned h2 = *reinterpret_cast<const unsigned*>(b + hi_off);
-            m[g][0] = (u64)l2.x | ((u64)(h2 & 0xffffu) << 32);
-            m[g][VEC - 1] = (u64)l2.y | ((u64)(h2 >> 16) << 32);
+            m[g][0] = (u64)l2.x | (packed_hi(hp, k, hb) << 32);
+            m[g][VEC - 1] = (u64)l2.y | (packed_hi(hp, k + 1, hb) << 32);
           } else {
-            m[g][0] = (u64)*reinterpret_cast<const unsigned*>(b + lo_off) |
-                      ((u64)*reinterpret_cast<const unsigned short*>(b + hi_off) << 32);
+            m[g][0] = (u64)*reinterpret_cast<const unsigned*>(b + lo_off) | (packed_hi(hp, k, hb) << 32);
           }
           continue;
         }
@@ -894,48 +894,58 @@ __global__ void __launch_bounds__(256) k_mac_multi(MacMulti M, int nt, u32 nq, u
   }
 }
 
-__global__ void k_pack_masks(unsigned char* __restrict__ out, const u64* __restrict__ in, u32 nq, u32 logN) {
+__global__ void k_pack_masks(unsigned char* __restrict__ out, const u64* __restrict__ in, u32 nq, u32 logN,
+                             unsigned long long wide, size_t mbytes) {
   const u32 N = 1u << logN, r = blockIdx.y, m = blockIdx.z;
-  const size_t mbytes = (8 + 6 * (size_t)(nq - 1)) * N;
   unsigned char* base = out + (size_t)m * mbytes;
   const u64* src = in + ((size_t)m * nq + r) * N;
+  const unsigned hb = r > 0 ? packed_hb(r, wide) : 0u;
+  unsigned char* hp = r > 0 ? base + packed_hi_off(r, nq, N, wide) : nullptr;
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
     const u64 v = src[k];
     if (r == 0) {
       reinterpret_cast<u64*>(base)[k] = v;
     } else {
       reinterpret_cast<unsigned*>(base + 8 * (size_t)N)[(size_t)(r - 1) * N + k] = (unsigned)v;
-      reinterpret_cast<unsigned short*>(base + 8 * (size_t)N + 4 * (size_t)(nq - 1) * N)[(size_t)(r - 1) * N + k] =
-          (unsigned short)(v >> 32);
+      if (hb == 2) reinterpret_cast<unsigned short*>(hp)[k] = (unsigned short)(v >> 32);
+      else hp[k] = (unsigned char)(v >> 32);
     }
   }
 }
 
-__global__ void k_unpack_mask(u64* __restrict__ out, const unsigned char* __restrict__ in, u32 nq, u32 logN) {
+__global__ void k_unpack_mask(u64* __restrict__ out, const unsigned char* __restrict__ in, u32 nq, u32 logN,
+                              unsigned long long wide) {
   const u32 N = 1u << logN, r = blockIdx.y;
+  const unsigned hb = r > 0 ? packed_hb(r, wide) : 0u;
+  const unsigned char* hp = r > 0 ? in + packed_hi_off(r, nq, N, wide) : nullptr;
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
     u64 v;
     if (r == 0) {
       v = reinterpret_cast<const u64*>(in)[k];
     } else {
       v = (u64)reinterpret_cast<const unsigned*>(in + 8 * (size_t)N)[(size_t)(r - 1) * N + k] |
-          ((u64)reinterpret_cast<const unsigned short*>(in + 8 * (size_t)N + 4 * (size_t)(nq - 1) * N)[(size_t)(r - 1) * N + k]
-           << 32);
+          (packed_hi(hp, k, hb) << 32);
     }
     out[(size_t)r * N + k] = v;
   }
 }
 
-cudaError_t launch_pack_masks(unsigned char* out, const u64* in, u32 nm, u32 nq, u32 logN, cudaStream_t st) {
+static size_t packed_bytes(u32 nq, size_t N, unsigned long long wide) {
+  return nq > 1 ? packed_hi_off(nq, nq, N, wide) : 8 * N;  // offset one past the last limb's high plane
+}
+
+cudaError_t launch_pack_masks(unsigned char* out, const u64* in, u32 nm, u32 nq, u32 logN, unsigned long long wide,
+                              cudaStream_t st) {
   if (!nm || !nq) return cudaSuccess;
   dim3 g = row_grid(1u << logN, nq, 256);
   g.z = nm;
-  k_pack_masks<<<g, 256, 0, st>>>(out, in, nq, logN);
+  k_pack_masks<<<g, 256, 0, st>>>(out, in, nq, logN, wide, packed_bytes(nq, 1u << logN, wide));
   return cudaGetLastError();
 }
 
-cudaError_t launch_unpack_mask(u64* out, const unsigned char* in, u32 nq, u32 logN, cudaStream_t st) {
-  k_unpack_mask<<<row_grid(1u << logN, nq, 256), 256, 0, st>>>(out, in, nq, logN);
+cudaError_t launch_unpack_mask(u64* out, const unsigned char* in, u32 nq, u32 logN, unsigned long long wide,
+                               cudaStream_t st) {
+  k_unpack_mask<<<row_grid(1u << logN, nq, 256), 256, 0, st>>>(out, in, nq, logN, wide);
   return cudaGetLastError();
 }
 
@@ -953,7 +963,8 @@ __global__ void __launch_bounds__(256) k_mac_multi_lanes(MacMulti M, int ng, int
   const u64 q = mc[r].q, ninv = mc[r].ninv;
   const size_t pst = (size_t)nq * N, off = (size_t)r * N;
   const size_t lo_off = 8 * (size_t)N + 4 * ((size_t)(r - 1) * N + k);
-  const size_t hi_off = 8 * (size_t)N + 4 * (size_t)(nq - 1) * N + 2 * ((size_t)(r - 1) * N + k);
+  const unsigned hb = r > 0 ? packed_hb(r, M.wide) : 2u;
+  const size_t hi_plane = r > 0 ? packed_hi_off(r, nq, N, M.wide) : 0;
   u64 h00 = 0, l00 = 0, h01 = 0, l01 = 0, h10 = 0, l10 = 0, h11 = 0, l11 = 0;
 #pragma unroll 4
   for (int t = 0; t < nt; ++t) {
@@ -962,10 +973,10 @@ __global__ void __launch_bounds__(256) k_mac_multi_lanes(MacMulti M, int ng, int
     u64 m0, m1;
     if (M.packed[g][t] && r > 0) {
       const char* b = reinterpret_cast<const char*>(mp);
+      const unsigned char* hp = reinterpret_cast<const unsigned char*>(b + hi_plane);
       const uint2 l2 = *reinterpret_cast<const uint2*>(b + lo_off);
-      const unsigned h2 = *reinterpret_cast<const unsigned*>(b + hi_off);
-      m0 = (u64)l2.x | ((u64)(h2 & 0xffffu) << 32);
-      m1 = (u64)l2.y | ((u64)(h2 >> 16) << 32);
+      m0 = (u64)l2.x | (packed_hi(hp, k, hb) << 32);
+      m1 = (u64)l2.y | (packed_hi(hp, k + 1, hb) << 32);
     } else {
       const ulonglong2 m2 = *reinterpret_cast<const ulonglong2*>(M.packed[g][t] ? mp + k : mp + off + k);
       m0 = m2.x;
@@ -1032,10 +1043,12 @@ __device__ __forceinline__ void mac_stage_issue(MacStage& S, const MacMulti& M, 
     if (M.packed[g][t] && r > 0) {
       const char* b = reinterpret_cast<const char*>(mp);
       const char* lo = b + 8 * (size_t)N + 4 * ((size_t)(r - 1) * N + k0);
-      const char* hi = b + 8 * (size_t)N + 4 * (size_t)(nq - 1) * N + 2 * ((size_t)(r - 1) * N + k0);
+      const unsigned hb = packed_hb(r, M.wide);
+      const char* hi = b + packed_hi_off(r, nq, N, M.wide) + (size_t)hb * k0;
       char* dst = reinterpret_cast<char*>(S.mask[g]);
-      if (tid < 64) cp_async16(dst + 16 * tid, lo + 16 * tid);                       // 1 KB low words
-      else if (tid < 96) cp_async16(dst + 1024 + 16 * (tid - 64), hi + 16 * (tid - 64));  // 512 B high
+      const u32 nhi = 16 * hb;  // 16-byte chunks of the 256-coefficient high plane
+      if (tid < 64) cp_async16(dst + 16 * tid, lo + 16 * tid);                            // 1 KB low words
+      else if (tid < 64 + nhi) cp_async16(dst + 1024 + 16 * (tid - 64), hi + 16 * (tid - 64));  // 256 / 512 B high
     } else {
       const u64* src = M.packed[g][t] ? mp + k0 : mp + off;  // packed limb 0 is a plain u64 row
       if (tid < 128) cp_async16(&S.mask[g][2 * tid], src + 2 * tid);
@@ -1072,9 +1085,8 @@ __global__ void __launch_bounds__(256) k_mac_multi_async(MacMulti M, int ng, int
       u64 m;
       if (M.packed[g][t] && r > 0) {
         const unsigned* lo = reinterpret_cast<const unsigned*>(C.mask[g]);
-        const unsigned short* hi = reinterpret_cast<const unsigned short*>(
-            reinterpret_cast<const unsigned char*>(C.mask[g]) + 1024);
-        m = (u64)lo[tid] | ((u64)hi[tid] << 32);
+        m = (u64)lo[tid] | (packed_hi(reinterpret_cast<const unsigned char*>(C.mask[g]) + 1024, tid,
+                                      packed_hb(r, M.wide)) << 32);
       } else {
         m = C.mask[g][tid];
       }
@@ -1141,8 +1153,9 @@ __device__ __forceinline__ void mac_stage_bulk(MacStage& S, u64* bar, const MacM
                                                u32 nq, u32 N, u32 k0) {
   const size_t off = (size_t)r * N + k0, pst = (size_t)nq * N;
   u32 bytes = 2 * kMacTile * 8;
+  const u32 pk = kMacTile * (4 + (r > 0 ? packed_hb(r, M.wide) : 2u));  // packed tile bytes of this limb
   for (int g = 0; g < kMultiG; ++g)
-    if (fl >> g & 1u) bytes += (fl >> (4 + g) & 1u) ? kMacTile * 6 : kMacTile * 8;
+    if (fl >> g & 1u) bytes += (fl >> (4 + g) & 1u) ? pk : kMacTile * 8;
   mbar_expect_tx(bar, bytes);
   bulk_g2s(S.ct[0], M.ct[t] + off, kMacTile * 8, bar);
   bulk_g2s(S.ct[1], M.ct[t] + pst + off, kMacTile * 8, bar);
@@ -1152,9 +1165,9 @@ __device__ __forceinline__ void mac_stage_bulk(MacStage& S, u64* bar, const MacM
     if (fl >> (4 + g) & 1u) {
       const char* b = reinterpret_cast<const char*>(mp);
       char* dst = reinterpret_cast<char*>(S.mask[g]);
+      const unsigned hb = packed_hb(r, M.wide);
       bulk_g2s(dst, b + 8 * (size_t)N + 4 * ((size_t)(r - 1) * N + k0), kMacTile * 4, bar);
-      bulk_g2s(dst + kMacTile * 4, b + 8 * (size_t)N + 4 * (size_t)(nq - 1) * N + 2 * ((size_t)(r - 1) * N + k0),
-               kMacTile * 2, bar);
+      bulk_g2s(dst + kMacTile * 4, b + packed_hi_off(r, nq, N, M.wide) + (size_t)hb * k0, kMacTile * hb, bar);
     } else {
       bulk_g2s(S.mask[g], M.packed[g][t] ? mp + k0 : mp + off, kMacTile * 8, bar);  // packed limb 0: u64 row
     }
@@ -1170,6 +1183,7 @@ __global__ void __launch_bounds__(256) k_mac_multi_tma(MacMulti M, int ng, int n
   __shared__ unsigned char flags[kMultiT];
   const u32 N = 1u << logN, r = blockIdx.y, k0 = blockIdx.x * kMacTile, tid = threadIdx.x;
   const u64 q = mc[r].q, ninv = mc[r].ninv, one_sh = mc[r].one_sh;
+  const unsigned hb = r > 0 ? packed_hb(r, M.wide) : 2u;
   if (tid < (u32)nt) {
     u32 fl = 0;
     for (int g = 0; g < ng; ++g)
@@ -1202,9 +1216,7 @@ __global__ void __launch_bounds__(256) k_mac_multi_tma(MacMulti M, int ng, int n
       u64 m;
       if (fl >> (4 + g) & 1u) {
         const unsigned* lo = reinterpret_cast<const unsigned*>(C.mask[g]);
-        const unsigned short* hi =
-            reinterpret_cast<const unsigned short*>(reinterpret_cast<const unsigned char*>(C.mask[g]) + kMacTile * 4);
-        m = (u64)lo[tid] | ((u64)hi[tid] << 32);
+        m = (u64)lo[tid] | (packed_hi(reinterpret_cast<const unsigned char*>(C.mask[g]) + kMacTile * 4, tid, hb) << 32);
       } else {
         m = C.mask[g][tid];
       }

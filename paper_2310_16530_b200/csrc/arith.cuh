@@ -101,13 +101,34 @@ struct MacMulti {
   const u64* ct[kMultiT];
   const u64* mask[kMultiG][kMultiT];
   u64* out[kMultiG];
-  unsigned char packed[kMultiG][kMultiT];  // 1: mask in the 48-bit packed layout (launch_pack_masks)
+  unsigned char packed[kMultiG][kMultiT];  // 1: mask in the packed layout (launch_pack_masks)
+  unsigned long long wide;                 // packed layout: bit r set = limb r needs a 16-bit high plane
 };
-// 48-bit packed masks: limb 0 as u64 [N], limbs 1..nq-1 as u32 low words
-// [nq-1][N] then u16 high words [nq-1][N] -- (8 + 6 (nq-1)) N bytes, for
-// chains whose q_1..q_{nq-1} are < 2^48 (the application primes)
-cudaError_t launch_pack_masks(unsigned char* out, const u64* in, u32 nm, u32 nq, u32 logN, cudaStream_t st);
-cudaError_t launch_unpack_mask(u64* out, const unsigned char* in, u32 nq, u32 logN, cudaStream_t st);
+// Packed resident masks: limb 0 as u64 [N]; limbs 1..nq-1 as u32 low words
+// [nq-1][N]; then each limb's high bits as its own plane, u8 for moduli
+// below 2^40 and u16 up to 2^48 (`wide` bit r) -- (8 + 4 (nq-1) + sum hb) N
+// bytes, lossless.  Byte offset of limb r's high plane and its width:
+__host__ __device__ __forceinline__ unsigned packed_hb(unsigned r, unsigned long long wide) {
+  return ((wide >> r) & 1ull) ? 2u : 1u;
+}
+__host__ __device__ __forceinline__ size_t packed_hi_off(unsigned r, unsigned nq, size_t N, unsigned long long wide) {
+  unsigned hb = 0;
+#ifdef __CUDA_ARCH__
+  hb = (r - 1) + __popcll(wide & ((1ull << r) - 2ull));
+#else
+  hb = (r - 1) + (unsigned)__builtin_popcountll(wide & ((1ull << r) - 2ull));
+#endif
+  return 8 * N + 4 * (size_t)(nq - 1) * N + (size_t)hb * N;
+}
+// the high bits of coefficient k of limb r (u8 or u16 plane)
+__device__ __forceinline__ u64 packed_hi(const unsigned char* plane, size_t k, unsigned hb) {
+  return hb == 2 ? (u64)reinterpret_cast<const unsigned short*>(plane)[k] : (u64)plane[k];
+}
+// packing (chains whose q_1..q_{nq-1} are < 2^48, the application primes)
+cudaError_t launch_pack_masks(unsigned char* out, const u64* in, u32 nm, u32 nq, u32 logN, unsigned long long wide,
+                              cudaStream_t st);
+cudaError_t launch_unpack_mask(u64* out, const unsigned char* in, u32 nq, u32 logN, unsigned long long wide,
+                               cudaStream_t st);
 cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN, int accumulate,
                              const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_gather_limb(u64* out, const u64* in, u32 limb, u32 nlimbs, u32 logN, u32 npolys,

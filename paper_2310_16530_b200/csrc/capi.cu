@@ -51,7 +51,8 @@ struct hcnn_ctx {
   u64 *d_tw = nullptr, *d_twp = nullptr, *d_itw = nullptr, *d_itwp = nullptr;
   ulonglong2 *d_ctw = nullptr, *d_ictw = nullptr;
   bool ntt2_ok = false;
-  std::vector<unsigned char> small;  // q < 2^47
+  std::vector<unsigned char> small;  // NTT modulus class per modulus (see ctx_create)
+  unsigned long long wide = 0;       // packed masks: bit r = q_r >= 2^40 (16-bit high plane)
   FbcStore moddown;                  // P -> q_0..q_{Lq-1}
   u64 *d_pinv = nullptr, *d_pinv_sh = nullptr;  // P^-1 mod q_i
   u64* d_pR = nullptr;                            // P R mod q_i (Montgomery form of P)
@@ -336,6 +337,8 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
   CK(cudaMemcpy(c->d_twp, twp.data(), tb, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_itw, itw.data(), tb, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_itwp, itwp.data(), tb, cudaMemcpyHostToDevice));
+  for (u32 r = 0; r < c->Lq && r < 64; ++r)
+    if (c->mods[r] >> 40) c->wide |= 1ull << r;
   u64 qmax = 0;
   for (u64 q : c->mods) {
     qmax = q > qmax ? q : qmax;
@@ -1015,6 +1018,7 @@ static int mac_terms_impl(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts
 }
 
 static int masks_packable(const hcnn_ctx* c, u32 nq) {
+  if (nq > 64) return 0;
   for (u32 r = 1; r < nq; ++r)
     if (c->mods[r] >> 48) return 0;
   return 1;
@@ -1024,16 +1028,16 @@ int hcnn_pack_masks(hcnn_ctx* c, void* out, const uint64_t* in, uint32_t n_masks
   if (!c) return fail(HCNN_E_PARAMETER, "null context");
   if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
   if (!masks_packable(c, level + 1)) return fail(HCNN_E_BASIS, "a modulus above 2^48: masks not packable");
-  PK("pack_masks", (8.0 + 8.0 + 6.0 * level) * n_masks * c->n, 1, STREAM(s),
-     launch_pack_masks((unsigned char*)out, in, n_masks, level + 1, c->logN, STREAM(s)));
+  PK("pack_masks", (8.0 * (level + 1) + packed_hi_off(level + 1, level + 1, 1, c->wide)) * n_masks * c->n, 1,
+     STREAM(s), launch_pack_masks((unsigned char*)out, in, n_masks, level + 1, c->logN, c->wide, STREAM(s)));
   return HCNN_OK;
 }
 
 int hcnn_unpack_mask(hcnn_ctx* c, uint64_t* out, const void* in, uint32_t level, void* s) {
   if (!c) return fail(HCNN_E_PARAMETER, "null context");
   if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
-  PK("unpack_mask", (8.0 + 8.0 + 6.0 * level) * c->n, 1, STREAM(s),
-     launch_unpack_mask(out, (const unsigned char*)in, level + 1, c->logN, STREAM(s)));
+  PK("unpack_mask", (8.0 * (level + 1) + packed_hi_off(level + 1, level + 1, 1, c->wide)) * c->n, 1, STREAM(s),
+     launch_unpack_mask(out, (const unsigned char*)in, level + 1, c->logN, c->wide, STREAM(s)));
   return HCNN_OK;
 }
 
@@ -1059,7 +1063,10 @@ int hcnn_mac_terms_multi_packed(hcnn_ctx* c, uint64_t* const* outs, const uint64
     for (u32 t0 = 0; t0 < n_terms; t0 += kMultiT) {
       const u32 nt = std::min<u32>(kMultiT, n_terms - t0);
       MacMulti M;
+      M.wide = c->wide;
       for (u32 t = 0; t < nt; ++t) M.ct[t] = cts[t0 + t];
+      // packed bytes relative to u64 rows, averaged over the limbs
+      const double pf = nq > 1 ? (double)packed_hi_off(nq, nq, 1, c->wide) / (8.0 * nq) : 1.0;
       double used = 0;
       for (u32 g = 0; g < (u32)kMultiG; ++g) {
         M.out[g] = g < ng ? outs[g0 + g] : nullptr;
@@ -1067,7 +1074,7 @@ int hcnn_mac_terms_multi_packed(hcnn_ctx* c, uint64_t* const* outs, const uint64
           const size_t idx = (size_t)(g0 + g) * n_terms + t0 + t;
           M.mask[g][t] = g < ng ? masks[idx] : nullptr;
           M.packed[g][t] = (g < ng && packed) ? packed[idx] : 0;
-          used += M.mask[g][t] ? (M.packed[g][t] ? 0.75 : 1.0) : 0.0;
+          used += M.mask[g][t] ? (M.packed[g][t] ? pf : 1.0) : 0.0;
         }
       }
       PK("mac_multi", 8.0 * (2.0 * nt + used + 2.0 * ng * (accumulate || t0 ? 2 : 1)) * nq * c->n, 1, STREAM(s),

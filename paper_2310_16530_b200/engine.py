@@ -272,13 +272,14 @@ class DeviceContext:
         return list(outs)
 
     def packed_mask_bytes(self, level: int) -> int:
-        return (8 + 6 * level) * self.n
+        """limb 0 as u64, limbs 1..level as u32 low words + a u8 (q < 2^40) or u16 high plane"""
+        return (8 + 4 * level + sum(2 if q >> 40 else 1 for q in self.q_list[1:level + 1])) * self.n
 
     def masks_packable(self, level: int) -> bool:
-        return all(q < (1 << 48) for q in self.q_list[1:level + 1])
+        return level < 64 and all(q < (1 << 48) for q in self.q_list[1:level + 1])
 
     def pack_masks(self, rows: torch.Tensor, level: int) -> torch.Tensor:
-        """Montgomery rows [k, l+1, N] -> uint8 [k, (8 + 6 l) N] (lossless 48-bit planes)."""
+        """Montgomery rows [k, l+1, N] -> uint8 [k, packed_mask_bytes(l)] (lossless 40/48-bit planes)."""
         rows = rows.contiguous()
         k = rows.numel() // ((level + 1) * self.n)
         out = torch.empty(k, self.packed_mask_bytes(level), dtype=torch.uint8, device=self.torch_device)
