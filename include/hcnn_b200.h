@@ -202,6 +202,14 @@ int hcnn_mac_terms_ext_batch(hcnn_ctx* ctx, uint64_t* out_ext, const uint64_t* c
  * clobbered; ws: hcnn_ks_workspace_bytes_batch(level, nb) */
 int hcnn_moddown_batch(hcnn_ctx* ctx, uint64_t* out, uint64_t* in_ext, uint32_t level, uint32_t nb, void* ws,
                        void* stream);
+/* ModDown and the following rescale fused: Q_level||P ciphertexts ->
+ * round(x / (P q_level)) over Q_{level-1} with one centred base conversion
+ * from the K+1 limbs (q_level, P).  One rounding instead of two, so residues
+ * differ from hcnn_moddown_batch + hcnn_rescale (no reference counterpart;
+ * bootstrapping's linear transforms).  out [nb][2][level][N]; in_ext's limbs
+ * level..level+K are clobbered; ws: hcnn_ks_workspace_bytes_batch(level, nb) */
+int hcnn_moddown_rescale_batch(hcnn_ctx* ctx, uint64_t* out, uint64_t* in_ext, uint32_t level, uint32_t nb, void* ws,
+                               void* stream);
 
 /* rescale ckks.py:506-528 for npolys polys at `level` -> level-1 */
 size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* ctx, uint32_t npolys);

@@ -77,6 +77,9 @@ class BootConfig:
     # (a ModUp each), so more babies / fewer giants wins.
     bsgs_baby: int | None = 16
     double_hoist: bool = True
+    # linear-transform levels end with one base conversion dividing by P q_l
+    # (ModDown + rescale fused, hcnn_moddown_rescale_batch)
+    fused_moddown_rescale: bool = True
 
     def evalmod_depth(self) -> int:
         return max(1, math.ceil(math.log2(self.degree))) + 1 + self.double_angle
@@ -532,8 +535,13 @@ class Bootstrapper:
                     part = ctx.rotate_hoisted_ext(inner, lvl, [ckks.galois_element(gamt, ct.n)],
                                                   [(ks.gks[gamt].rows_b, ks.gks[gamt].rows_a)])[0]
                 acc = part if acc is None else ctx.binop("add", acc, part, nq, K)
-            out = ctx.moddown(acc, lvl)
-            ct = ckks.rescale(Ciphertext(out, ct.scale * s_d, ct.n, ct.params), self.params)
+            if self.cfg.fused_moddown_rescale:
+                # ModDown and the rescale in one base conversion: divide by P q_l at once
+                out = ctx.moddown_rescale(acc, lvl)
+                ct = Ciphertext(out, ct.scale * s_d / q, ct.n, ct.params)
+            else:
+                out = ctx.moddown(acc, lvl)
+                ct = ckks.rescale(Ciphertext(out, ct.scale * s_d, ct.n, ct.params), self.params)
         return ct
 
     def _apply(self, ct: Ciphertext, plans: list[DiagPlan], ks: KeySet, tag,

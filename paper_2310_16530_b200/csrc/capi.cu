@@ -60,6 +60,13 @@ struct hcnn_ctx {
   u64* d_qmod = nullptr;                         // [l][i] q_l mod q_i
   std::mutex mu;
   std::map<u32, ModupSet> modup;
+  // fused ModDown + rescale at level l: FBC from (q_l, P) to q_0..q_{l-1},
+  // (P q_l)^-1 mod q_i (+ Shoup companions)
+  struct MdrSet {
+    FbcStore fbc;
+    u64 *d_inv = nullptr, *d_inv_sh = nullptr;
+  };
+  std::map<u32, MdrSet> mdr;
   std::map<std::vector<u32>, FbcStore> generic;
   NttTables tables() const {
     NttTables T;
@@ -169,6 +176,42 @@ static int build_fbc(hcnn_ctx* c, const std::vector<u32>& src, const std::vector
   st->dev.nored = bound < ((unsigned __int128)1 << 64) ? 1 : 0;
   CK(cudaMalloc(&st->d_dev, sizeof(FbcDev)));
   CK(cudaMemcpy(st->d_dev, &st->dev, sizeof(FbcDev), cudaMemcpyHostToDevice));
+  return HCNN_OK;
+}
+
+// Fused ModDown + rescale tables for level l >= 1: the K special limbs and
+// q_l together are the modulus divided away (no reference counterpart:
+// bootstrapping only, where one rounding instead of two is fine)
+static int get_mdr(hcnn_ctx* c, u32 level, hcnn_ctx::MdrSet** out) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  auto it = c->mdr.find(level);
+  if (it != c->mdr.end()) {
+    *out = &it->second;
+    return HCNN_OK;
+  }
+  hcnn_ctx::MdrSet set;
+  std::vector<u32> src{level}, dst, pos;
+  for (u32 j = 0; j < c->K; ++j) src.push_back(c->Lq + j);
+  for (u32 i = 0; i < level; ++i) {
+    dst.push_back(i);
+    pos.push_back(i);
+  }
+  int rc = build_fbc(c, src, dst, pos, &set.fbc);
+  if (rc) return rc;
+  std::vector<u64> inv(level), inv_sh(level);
+  for (u32 i = 0; i < level; ++i) {
+    const u64 qi = c->mods[i];
+    u64 prod = c->mods[level] % qi;
+    for (u32 j = 0; j < c->K; ++j) prod = h_mulmod(prod, c->mods[c->Lq + j] % qi, qi);
+    inv[i] = h_invmod(prod, qi);
+    inv_sh[i] = h_shoup(inv[i], qi);
+  }
+  CK(cudaMalloc(&set.d_inv, level * 8));
+  CK(cudaMalloc(&set.d_inv_sh, level * 8));
+  CK(cudaMemcpy(set.d_inv, inv.data(), level * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(set.d_inv_sh, inv_sh.data(), level * 8, cudaMemcpyHostToDevice));
+  auto res = c->mdr.emplace(level, set);
+  *out = &res.first->second;
   return HCNN_OK;
 }
 
@@ -952,6 +995,43 @@ int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* c, uint64_t* const* outs, const uint
        launch_ks_inner(outs[i], c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd, c->logN, g,
                        c->d_mc, STREAM(s), nb, ct, cts, ct, c->d_pR, key_lqs ? key_lqs[i] : 0));
   }
+  return HCNN_OK;
+}
+
+// (Q_l||P ciphertexts) -> round(x / (P q_l)) over Q_{l-1}: ModDown and the
+// following rescale with one base conversion -- iNTT of the K+1 limbs
+// (q_l, P), centred FBC to q_0..q_{l-1}, NTT of l limbs, combine.
+int hcnn_moddown_rescale_batch(hcnn_ctx* c, uint64_t* out, uint64_t* in_ext, uint32_t level, uint32_t nb, void* ws,
+                               void* s) {
+  int rc = check_level(c, level);
+  if (rc) return rc;
+  if (level == 0) return fail(HCNN_E_LEVEL, "no limb left to rescale away");
+  if (nb == 0) return HCNN_OK;
+  if (c->K + 1 > 6) return fail(HCNN_E_PARAMETER, "fused ModDown+rescale needs K + 1 <= 6");
+  hcnn_ctx::MdrSet* md;
+  rc = get_mdr(c, level, &md);
+  if (rc) return rc;
+  const u32 nq = level + 1, n_ext = nq + c->K, l = level;
+  const size_t N = c->n;
+  KsWs w = ks_layout(c, level, ws, nb);
+  LimbMap m{};
+  m.base = in_ext + (size_t)l * N;
+  m.poly_stride = (size_t)n_ext * N;
+  m.basis = c->basis(nq, c->K);
+  m.first_limb = l;
+  PK("ntt_inv_moddown", 16.0 * 2 * nb * (c->K + 1) * N, ntt_nk(c), STREAM(s),
+     launch_ntt(c->tables(), m, c->K + 1, 2 * nb, true, STREAM(s)));
+  PK("moddown_fbc", 8.0 * 2 * nb * (c->K + 1 + l) * N, 1, STREAM(s),
+     launch_fbc(md->fbc.dev, md->fbc.d_dev, c->d_mc, in_ext + (size_t)l * N, (size_t)n_ext * N, w.lift, (size_t)l * N,
+                c->logN, 2 * nb, l, STREAM(s)));
+  LimbMap f{};
+  f.base = w.lift;
+  f.poly_stride = (size_t)l * N;
+  f.basis = c->basis(l, 0);
+  PK("ntt_fwd_moddown", 16.0 * 2 * nb * l * N, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), f, l, 2 * nb, false, STREAM(s)));
+  PK("moddown_combine", 8.0 * 2 * nb * 3 * l * N, 1, STREAM(s),
+     launch_moddown_combine(out, out + (size_t)l * N, in_ext, w.lift, nullptr, nullptr, 1, l, n_ext, c->logN,
+                            md->d_inv, md->d_inv_sh, c->d_mc, STREAM(s), nb, 2 * (size_t)l * N, 0));
   return HCNN_OK;
 }
 

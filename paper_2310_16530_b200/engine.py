@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .errors import BasisError, NativeError
+from .errors import BasisError, LevelError, NativeError
 
 _ctx_cache: dict[tuple, "DeviceContext"] = {}
 _ctx_lock = threading.Lock()
@@ -332,6 +332,19 @@ class DeviceContext:
         out = self.empty(*ext.shape[:-2], level + 1, self.n)
         ws = self.ks_workspace(level, nb)
         self._chk(self.lib.hcnn_moddown_batch(self.handle, _ptr(out), _ptr(ext), level, nb, _ptr(ws), _stream()))
+        return out
+
+    def moddown_rescale(self, ext: torch.Tensor, level: int) -> torch.Tensor:
+        """Q_l||P ciphertext(s) -> round(x / (P q_l)) over Q_{l-1} in one base conversion (ext clobbered)."""
+        if not ext.is_contiguous() or ext.shape[-2:] != (level + 1 + self.K, self.n):
+            raise BasisError("moddown_rescale expects a contiguous [(nb,) 2, l+1+K, N] tensor")
+        if level < 1:
+            raise LevelError("no limb left to rescale away")
+        nb = 1 if ext.dim() == 3 else int(ext.shape[0])
+        out = self.empty(*ext.shape[:-2], level, self.n)
+        ws = self.ks_workspace(level, nb)
+        self._chk(self.lib.hcnn_moddown_rescale_batch(self.handle, _ptr(out), _ptr(ext), level, nb, _ptr(ws),
+                                                      _stream()))
         return out
 
     def mac_terms(self, cts: Sequence[torch.Tensor], masks: Sequence[torch.Tensor], level: int,

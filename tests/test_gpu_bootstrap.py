@@ -160,3 +160,23 @@ def test_graph_refresh_slot_bootstraps():
     err = float(np.max(np.abs(dec - ref)))
     print("stack(2) with bootstrapping: max abs err", err)
     assert err < 1e-3
+
+
+def test_fused_moddown_rescale(boot12):
+    """hcnn_moddown_rescale_batch divides a Q||P ciphertext by P q_l in one
+    base conversion: on the lifted P*ct it decrypts to rescale(ct) up to the
+    rounding, for a single ciphertext and a batch."""
+    from paper_2310_16530_b200 import ckks
+    from paper_2310_16530_b200.ckks import Ciphertext
+    params, cfg, b, ks = boot12
+    rng = np.random.default_rng(21)
+    lvl = params.max_level - 1
+    cts = [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl), ks, rng) for _ in range(3)]
+    for ct in (cts[0], ckks.stack(cts)):
+        want = ckks.rescale(ct, params)
+        got = Ciphertext(params.ctx.moddown_rescale(b._lift_ext(ct), lvl), want.scale, ct.n, params)
+        assert got.level == want.level
+        for g, w in zip(ckks.unstack(got), ckks.unstack(want)):
+            dg = ckks.decode(ckks.decrypt(g, ks), params, imag_tol=None)
+            dw = ckks.decode(ckks.decrypt(w, ks), params, imag_tol=None)
+            assert np.max(np.abs(dg - dw)) < 1e-7
