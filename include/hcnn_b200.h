@@ -210,6 +210,13 @@ int hcnn_moddown_batch(hcnn_ctx* ctx, uint64_t* out, uint64_t* in_ext, uint32_t 
  * level..level+K are clobbered; ws: hcnn_ks_workspace_bytes_batch(level, nb) */
 int hcnn_moddown_rescale_batch(hcnn_ctx* ctx, uint64_t* out, uint64_t* in_ext, uint32_t level, uint32_t nb, void* ws,
                                void* stream);
+/* hmult + relinearisation + rescale with one ModDown (the key-switch sum and
+ * P (d0, d1) are divided by P q_level together): out [nb][2][level][N].
+ * Residues differ from hcnn_hmult_batch + hcnn_rescale (one rounding);
+ * bootstrapping's EvalMod products.  ws: hcnn_hmult_rescale_workspace_bytes */
+size_t hcnn_hmult_rescale_workspace_bytes(const hcnn_ctx* ctx, uint32_t level, uint32_t nb);
+int hcnn_hmult_rescale_batch(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t level,
+                             uint32_t nb, const uint64_t* kb, const uint64_t* ka, void* ws, void* stream);
 
 /* rescale ckks.py:506-528 for npolys polys at `level` -> level-1 */
 size_t hcnn_rescale_workspace_bytes(const hcnn_ctx* ctx, uint32_t npolys);

@@ -82,6 +82,8 @@ SIGNATURES = {
                                         _INT, _VP]),
     "hcnn_moddown_batch": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP, _VP]),
     "hcnn_moddown_rescale_batch": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP, _VP]),
+    "hcnn_hmult_rescale_workspace_bytes": (ctypes.c_size_t, [_VP, _U32, _U32]),
+    "hcnn_hmult_rescale_batch": (_INT, [_VP, _VP, _VP, _VP, _U32, _U32, _VP, _VP, _VP, _VP]),
     "hcnn_rescale_workspace_bytes": (_SZ, [_VP, _U32]),
     "hcnn_rescale": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP, _VP]),
     "hcnn_scalar_mac": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_U32), _PU64, _U32, _U32, _U32, _INT,

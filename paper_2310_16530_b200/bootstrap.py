@@ -251,9 +251,10 @@ class _Exact:
     """hmult / constants with scales tracked so that additions always meet
     equal scales (to float precision)."""
 
-    def __init__(self, params: CkksParams, ks: KeySet):
+    def __init__(self, params: CkksParams, ks: KeySet, fused: bool = False):
         self.params, self.ks = params, ks
         self.ctx = params.ctx
+        self.fused = fused  # products through hcnn_hmult_rescale_batch (one ModDown for relin + rescale)
 
     def drop(self, a: Ciphertext, level: int) -> Ciphertext:
         return a if a.level == level else ckks.mod_drop(a, level)
@@ -262,7 +263,11 @@ class _Exact:
         lvl = min(a.level, b.level)
         if lvl < 1:
             raise LevelError("bootstrap evaluator ran out of levels")
-        return ckks.rescale(ckks.hmult(self.drop(a, lvl), self.drop(b, lvl), self.ks), self.params)
+        a, b = self.drop(a, lvl), self.drop(b, lvl)
+        if self.fused:
+            out = self.ctx.hmult_rescale(a.data, b.data, lvl, self.ks.rlk.rows_b, self.ks.rlk.rows_a)
+            return Ciphertext(out, a.scale * b.scale / self.params.q_mods[lvl].q, a.n, a.params)
+        return ckks.rescale(ckks.hmult(a, b, self.ks), self.params)
 
     def double(self, a: Ciphertext) -> Ciphertext:
         return Ciphertext(self.ctx.binop("add", a.data, a.data, a.level + 1), a.scale, a.n, a.params)
@@ -597,7 +602,7 @@ class Bootstrapper:
 
     def eval_mod(self, y: Ciphertext, ks: KeySet) -> Ciphertext:
         """slots y = x/B (x = t/q0) -> sin(2 pi x)."""
-        ev = _Exact(self.params, ks)
+        ev = _Exact(self.params, ks, fused=self.cfg.fused_moddown_rescale)
         c = eval_chebyshev(ev, y, self.cheb, self.eval_scale)
         for _ in range(self.cfg.double_angle):
             c = ev.cheb_product(c, c, None)  # cos(2t) = 2 cos(t)^2 - 1

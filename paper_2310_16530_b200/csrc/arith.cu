@@ -651,6 +651,34 @@ __global__ void __launch_bounds__(256) k_moddown_combine_steps(ComboSteps S, con
   }
 }
 
+// acc_{b,p}[r] += P * d_{b,p}[r] mod q_r on the Q limbs of nb extended-basis
+// accumulators ([nb][2][n_ext]); d is [nb][2][nq] (the tensor product's d0,
+// d1), pR = P R mod q_r (Montgomery form, so one REDC gives P d).  Fused
+// hmult + rescale: the key-switch sum and P (d0, d1) share one ModDown.
+__global__ void __launch_bounds__(256) k_add_pmul(u64* __restrict__ acc, const u64* __restrict__ d, u32 nq,
+                                                  u32 n_ext, u32 logN, const u64* __restrict__ pR,
+                                                  const ModConsts* __restrict__ mc) {
+  const u32 N = 1u << logN, r = blockIdx.y, z = blockIdx.z;
+  const u64 q = mc[r].q, ninv = mc[r].ninv, w = pR[r];
+  u64* A = acc + ((size_t)z * n_ext + r) * N;
+  const u64* D = d + ((size_t)z * nq + r) * N;
+  for (u32 k2 = blockIdx.x * blockDim.x + threadIdx.x; k2 < N / 2; k2 += gridDim.x * blockDim.x) {
+    const u32 k = 2 * k2;
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(A + k);
+    const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(D + k);
+    *reinterpret_cast<ulonglong2*>(A + k) =
+        make_ulonglong2(add_mod(a.x, mont_mul(x.x, w, q, ninv), q), add_mod(a.y, mont_mul(x.y, w, q, ninv), q));
+  }
+}
+
+cudaError_t launch_add_pmul(u64* acc, const u64* d, u32 nb, u32 nq, u32 n_ext, u32 logN, const u64* pR,
+                            const ModConsts* mc, cudaStream_t st) {
+  dim3 g = row_grid((1u << logN) / 2, nq, 256);
+  g.z = 2 * nb;
+  k_add_pmul<<<g, 256, 0, st>>>(acc, d, nq, n_ext, logN, pR, mc);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_moddown_combine_steps(const ComboSteps& S, u32 n_rot, const u64* acc, const u64* lift,
                                          const u64* add0, u32 nb, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
                                          const u64* pinv_sh, const ModConsts* mc, size_t out_bst, size_t add_bst,

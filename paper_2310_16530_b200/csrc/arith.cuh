@@ -56,6 +56,8 @@ struct ComboSteps {
   u64* out[kComboMax];
   u64 g[kComboMax];
 };
+cudaError_t launch_add_pmul(u64* acc, const u64* d, u32 nb, u32 nq, u32 n_ext, u32 logN, const u64* pR,
+                            const ModConsts* mc, cudaStream_t st);
 cudaError_t launch_moddown_combine_steps(const ComboSteps& S, u32 n_rot, const u64* acc, const u64* lift,
                                          const u64* add0, u32 nb, u32 nq, u32 n_ext, u32 logN, const u64* pinv,
                                          const u64* pinv_sh, const ModConsts* mc, size_t out_bst, size_t add_bst,

@@ -1001,38 +1001,76 @@ int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* c, uint64_t* const* outs, const uint
 // (Q_l||P ciphertexts) -> round(x / (P q_l)) over Q_{l-1}: ModDown and the
 // following rescale with one base conversion -- iNTT of the K+1 limbs
 // (q_l, P), centred FBC to q_0..q_{l-1}, NTT of l limbs, combine.
+static int moddown_rescale(hcnn_ctx* c, u32 level, u64* in_ext, u64* lift, u64* out, u32 nb, cudaStream_t st) {
+  if (c->K + 1 > 6) return fail(HCNN_E_PARAMETER, "fused ModDown+rescale needs K + 1 <= 6");
+  hcnn_ctx::MdrSet* md;
+  int rc = get_mdr(c, level, &md);
+  if (rc) return rc;
+  const u32 nq = level + 1, n_ext = nq + c->K, l = level;
+  const size_t N = c->n;
+  LimbMap m{};
+  m.base = in_ext + (size_t)l * N;
+  m.poly_stride = (size_t)n_ext * N;
+  m.basis = c->basis(nq, c->K);
+  m.first_limb = l;
+  PK("ntt_inv_moddown", 16.0 * 2 * nb * (c->K + 1) * N, ntt_nk(c), st,
+     launch_ntt(c->tables(), m, c->K + 1, 2 * nb, true, st));
+  PK("moddown_fbc", 8.0 * 2 * nb * (c->K + 1 + l) * N, 1, st,
+     launch_fbc(md->fbc.dev, md->fbc.d_dev, c->d_mc, in_ext + (size_t)l * N, (size_t)n_ext * N, lift, (size_t)l * N,
+                c->logN, 2 * nb, l, st));
+  LimbMap f{};
+  f.base = lift;
+  f.poly_stride = (size_t)l * N;
+  f.basis = c->basis(l, 0);
+  PK("ntt_fwd_moddown", 16.0 * 2 * nb * l * N, ntt_nk(c), st, launch_ntt(c->tables(), f, l, 2 * nb, false, st));
+  PK("moddown_combine", 8.0 * 2 * nb * 3 * l * N, 1, st,
+     launch_moddown_combine(out, out + (size_t)l * N, in_ext, lift, nullptr, nullptr, 1, l, n_ext, c->logN,
+                            md->d_inv, md->d_inv_sh, c->d_mc, st, nb, 2 * (size_t)l * N, 0));
+  return HCNN_OK;
+}
+
+// (Q_l||P ciphertexts) -> round(x / (P q_l)) over Q_{l-1}: ModDown and the
+// following rescale with one base conversion -- iNTT of the K+1 limbs
+// (q_l, P), centred FBC to q_0..q_{l-1}, NTT of l limbs, combine.
 int hcnn_moddown_rescale_batch(hcnn_ctx* c, uint64_t* out, uint64_t* in_ext, uint32_t level, uint32_t nb, void* ws,
                                void* s) {
   int rc = check_level(c, level);
   if (rc) return rc;
   if (level == 0) return fail(HCNN_E_LEVEL, "no limb left to rescale away");
   if (nb == 0) return HCNN_OK;
-  if (c->K + 1 > 6) return fail(HCNN_E_PARAMETER, "fused ModDown+rescale needs K + 1 <= 6");
-  hcnn_ctx::MdrSet* md;
-  rc = get_mdr(c, level, &md);
-  if (rc) return rc;
-  const u32 nq = level + 1, n_ext = nq + c->K, l = level;
-  const size_t N = c->n;
   KsWs w = ks_layout(c, level, ws, nb);
-  LimbMap m{};
-  m.base = in_ext + (size_t)l * N;
-  m.poly_stride = (size_t)n_ext * N;
-  m.basis = c->basis(nq, c->K);
-  m.first_limb = l;
-  PK("ntt_inv_moddown", 16.0 * 2 * nb * (c->K + 1) * N, ntt_nk(c), STREAM(s),
-     launch_ntt(c->tables(), m, c->K + 1, 2 * nb, true, STREAM(s)));
-  PK("moddown_fbc", 8.0 * 2 * nb * (c->K + 1 + l) * N, 1, STREAM(s),
-     launch_fbc(md->fbc.dev, md->fbc.d_dev, c->d_mc, in_ext + (size_t)l * N, (size_t)n_ext * N, w.lift, (size_t)l * N,
-                c->logN, 2 * nb, l, STREAM(s)));
-  LimbMap f{};
-  f.base = w.lift;
-  f.poly_stride = (size_t)l * N;
-  f.basis = c->basis(l, 0);
-  PK("ntt_fwd_moddown", 16.0 * 2 * nb * l * N, ntt_nk(c), STREAM(s), launch_ntt(c->tables(), f, l, 2 * nb, false, STREAM(s)));
-  PK("moddown_combine", 8.0 * 2 * nb * 3 * l * N, 1, STREAM(s),
-     launch_moddown_combine(out, out + (size_t)l * N, in_ext, w.lift, nullptr, nullptr, 1, l, n_ext, c->logN,
-                            md->d_inv, md->d_inv_sh, c->d_mc, STREAM(s), nb, 2 * (size_t)l * N, 0));
-  return HCNN_OK;
+  return moddown_rescale(c, level, in_ext, w.lift, out, nb, STREAM(s));
+}
+
+size_t hcnn_hmult_rescale_workspace_bytes(const hcnn_ctx* c, uint32_t level, uint32_t nb) {
+  return hcnn_ks_workspace_bytes_batch(c, level, nb) + 2ull * (nb ? nb : 1) * (level + 1) * c->n * 8;
+}
+
+// tensor + relinearisation + rescale with one ModDown: the key-switch sum and
+// P (d0, d1) are accumulated over Q_l||P and divided by P q_l at once
+// (bootstrapping's EvalMod products; no reference counterpart).
+int hcnn_hmult_rescale_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t level,
+                             uint32_t nb, const uint64_t* kb, const uint64_t* ka, void* ws, void* s) {
+  int rc = check_level(c, level);
+  if (rc) return rc;
+  if (level == 0) return fail(HCNN_E_LEVEL, "no limb left to rescale away");
+  if (nb == 0) return HCNN_OK;
+  const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
+  const size_t N = c->n, ct = 2 * (size_t)nq * N;
+  KsWs w = ks_layout(c, level, ws, nb);
+  u64* d01 = (u64*)((char*)ws + hcnn_ks_workspace_bytes_batch(c, level, nb));  // [nb][2][nq]
+  for (u32 e = 0; e < nb; ++e)
+    PK("tensor", 8.0 * 7 * nq * N, 1, STREAM(s),
+       launch_tensor(d01 + e * ct, d01 + e * ct + nq * N, w.lift + e * ct, a + e * ct, b + e * ct, nq, c->logN,
+                     c->d_mc, STREAM(s)));
+  rc = ks_modup(c, level, w.lift, w, STREAM(s), nb, ct);
+  if (rc) return rc;
+  PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
+     launch_ks_inner(w.acc, w.lift, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, 1, c->d_mc,
+                     STREAM(s), nb, ct, nullptr, 0, nullptr, 0));
+  PK("add_pmul", 8.0 * 2 * nb * 3 * nq * N, 1, STREAM(s),
+     launch_add_pmul(w.acc, d01, nb, nq, n_ext, c->logN, c->d_pR, c->d_mc, STREAM(s)));
+  return moddown_rescale(c, level, w.acc, w.lift, out, nb, STREAM(s));
 }
 
 int hcnn_moddown_batch(hcnn_ctx* c, uint64_t* out, uint64_t* in_ext, uint32_t level, uint32_t nb, void* ws, void* s) {

@@ -334,6 +334,21 @@ class DeviceContext:
         self._chk(self.lib.hcnn_moddown_batch(self.handle, _ptr(out), _ptr(ext), level, nb, _ptr(ws), _stream()))
         return out
 
+    def hmult_rescale(self, a: torch.Tensor, b: torch.Tensor, level: int, key_b: torch.Tensor,
+                      key_a: torch.Tensor) -> torch.Tensor:
+        """rescale(hmult(a, b)) with the relinearisation's ModDown and the rescale fused
+        (one rounding; bootstrapping only).  -> [(nb,) 2, l, N]"""
+        nb = self._batch(a, level)
+        if b.shape != a.shape or not b.is_contiguous():
+            raise BasisError("hmult operands differ in shape")
+        if level < 1:
+            raise LevelError("no limb left to rescale away")
+        out = self.empty(*a.shape[:-2], level, self.n)
+        ws = self.empty(int(self.lib.hcnn_hmult_rescale_workspace_bytes(self.handle, level, nb)) // 8)
+        self._chk(self.lib.hcnn_hmult_rescale_batch(self.handle, _ptr(out), _ptr(a), _ptr(b), level, nb,
+                                                    _ptr(key_b), _ptr(key_a), _ptr(ws), _stream()))
+        return out
+
     def moddown_rescale(self, ext: torch.Tensor, level: int) -> torch.Tensor:
         """Q_l||P ciphertext(s) -> round(x / (P q_l)) over Q_{l-1} in one base conversion (ext clobbered)."""
         if not ext.is_contiguous() or ext.shape[-2:] != (level + 1 + self.K, self.n):
