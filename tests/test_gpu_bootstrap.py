@@ -180,3 +180,23 @@ def test_fused_moddown_rescale(boot12):
             dg = ckks.decode(ckks.decrypt(g, ks), params, imag_tol=None)
             dw = ckks.decode(ckks.decrypt(w, ks), params, imag_tol=None)
             assert np.max(np.abs(dg - dw)) < 1e-7
+
+
+def test_fused_hmult_rescale(boot12):
+    """hcnn_hmult_rescale_batch == rescale(hmult(a, b)) up to one rounding
+    (decrypt-and-compare, single ciphertext and batch)."""
+    from paper_2310_16530_b200 import ckks
+    from paper_2310_16530_b200.ckks import Ciphertext
+    params, cfg, b, ks = boot12
+    rng = np.random.default_rng(22)
+    lvl = params.max_level
+    xs = [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl), ks, rng) for _ in range(3)]
+    ys = [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl), ks, rng) for _ in range(3)]
+    for x, y in ((xs[0], ys[0]), (ckks.stack(xs), ckks.stack(ys))):
+        want = ckks.rescale(ckks.hmult(x, y, ks), params)
+        got = Ciphertext(params.ctx.hmult_rescale(x.data, y.data, lvl, ks.rlk.rows_b, ks.rlk.rows_a), want.scale,
+                         x.n, params)
+        for g, w in zip(ckks.unstack(got), ckks.unstack(want)):
+            dg = ckks.decode(ckks.decrypt(g, ks), params, imag_tol=None)
+            dw = ckks.decode(ckks.decrypt(w, ks), params, imag_tol=None)
+            assert np.max(np.abs(dg - dw)) < 1e-6
