@@ -190,8 +190,12 @@ def test_fused_hmult_rescale(boot12):
     params, cfg, b, ks = boot12
     rng = np.random.default_rng(22)
     lvl = params.max_level
-    xs = [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl), ks, rng) for _ in range(3)]
-    ys = [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl), ks, rng) for _ in range(3)]
+    # EvalMod multiplies at scale ~ q_l, so the product keeps scale ~ q_l after the
+    # rescale; at Delta = 2^40 it would land at 2^22 and the two paths' (different)
+    # rounding points alone differ by ~1e-4 in the slots
+    sc = float(params.q_mods[lvl].q)
+    xs = [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl, sc), ks, rng) for _ in range(3)]
+    ys = [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl, sc), ks, rng) for _ in range(3)]
     for x, y in ((xs[0], ys[0]), (ckks.stack(xs), ckks.stack(ys))):
         want = ckks.rescale(ckks.hmult(x, y, ks), params)
         got = Ciphertext(params.ctx.hmult_rescale(x.data, y.data, lvl, ks.rlk.rows_b, ks.rlk.rows_a), want.scale,
