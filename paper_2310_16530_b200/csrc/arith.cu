@@ -1273,6 +1273,97 @@ __global__ void __launch_bounds__(256) k_mac_multi_tma(MacMulti M, int ng, int n
   }
 }
 
+// k_mac_multi_tma with TPB threads per CTA, kMacTile / TPB coefficients per thread (TPB = 128:
+// two independent coefficient chains per thread, a cheaper CTA barrier and
+// more resident CTAs per SM for the same ring).  MINB = 1 leaves the
+// minimum-blocks hint at 0: ptxas then settles at 96 registers (5 CTAs of
+// 128 per SM) where an explicit 1 lets it take 166 (measured 25 % slower).
+template <int ST, int TPB, int MINB = 1>
+__global__ void __launch_bounds__(TPB, MINB > 1 ? MINB : 0) k_mac_multi_tma2(MacMulti M, int ng, int nt, u32 nq, u32 logN,
+                                                       int accumulate, const ModConsts* __restrict__ mc) {
+  constexpr int CPT = kMacTile / TPB;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MacStage* S = reinterpret_cast<MacStage*>(smem_raw);
+  __shared__ __align__(8) u64 full[ST];
+  __shared__ unsigned char flags[kMultiT];
+  const u32 N = 1u << logN, r = blockIdx.y, k0 = blockIdx.x * kMacTile, tid = threadIdx.x;
+  const u64 q = mc[r].q, ninv = mc[r].ninv, one_sh = mc[r].one_sh;
+  const unsigned hb = r > 0 ? packed_hb(r, M.wide) : 2u;
+  for (u32 i = tid; i < (u32)nt; i += TPB) {
+    u32 fl = 0;
+    for (int g = 0; g < ng; ++g)
+      if (M.mask[g][i]) fl |= (1u << g) | ((M.packed[g][i] && r > 0) ? (16u << g) : 0u);
+    flags[i] = (unsigned char)fl;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < ST - 1 && s < nt; ++s) mac_stage_bulk(S[s], &full[s], M, s, flags[s], r, nq, N, k0);
+  u64 h[kMultiG][2 * CPT], l[kMultiG][2 * CPT];
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g)
+#pragma unroll
+    for (int p = 0; p < 2 * CPT; ++p) h[g][p] = l[g][p] = 0;
+  for (int t = 0; t < nt; ++t) {
+    if (t > 0) __syncthreads();  // every thread is done with slot (t-1) % ST
+    if (tid == 0) {
+      const int tn = t + ST - 1;
+      if (tn < nt) mac_stage_bulk(S[tn % ST], &full[tn % ST], M, tn, flags[tn], r, nq, N, k0);
+    }
+    const u32 fl = flags[t];
+    mbar_wait(&full[t % ST], (u32)(t / ST) & 1u);
+    const MacStage& C = S[t % ST];
+    u64 x[2 * CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      x[2 * c] = C.ct[0][tid + c * TPB];
+      x[2 * c + 1] = C.ct[1][tid + c * TPB];
+    }
+#pragma unroll
+    for (int g = 0; g < kMultiG; ++g) {
+      if (!(fl >> g & 1u)) continue;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const u32 i = tid + c * TPB;
+        u64 m;
+        if (fl >> (4 + g) & 1u) {
+          const unsigned* lo = reinterpret_cast<const unsigned*>(C.mask[g]);
+          m = (u64)lo[i] | (packed_hi(reinterpret_cast<const unsigned char*>(C.mask[g]) + kMacTile * 4, i, hb) << 32);
+        } else {
+          m = C.mask[g][i];
+        }
+        mac128_lazy(h[g][2 * c], l[g][2 * c], x[2 * c], m);
+        mac128_lazy(h[g][2 * c + 1], l[g][2 * c + 1], x[2 * c + 1], m);
+      }
+    }
+    if ((t + 1) % kLazyTerms == 0 || t + 1 == nt) {
+#pragma unroll
+      for (int g = 0; g < kMultiG; ++g)
+#pragma unroll
+        for (int p = 0; p < 2 * CPT; ++p) h[g][p] = fold_hi(h[g][p], q, one_sh);
+    }
+  }
+  const size_t pst = (size_t)nq * N;
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g) {
+    if (g >= ng) break;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const size_t off = (size_t)r * N + k0 + tid + c * TPB;
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        u64* d = M.out[g] + p * pst + off;
+        u64 y = redc128(h[g][2 * c + p], l[g][2 * c + p], q, ninv);
+        if (accumulate) y = add_mod(y, *d, q);
+        *d = y;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Key-switch inner product with TMA-staged operands.  A CTA owns one
 // 256-coefficient tile of one output limb r for up to kKsEntries batch
@@ -1295,6 +1386,8 @@ struct KsStage {
 };
 int g_ks_tma = 1;
 int g_ks_tma_min = 3;  // smallest batch routed to k_ks_inner_tma
+int g_ks_tpb = 128;    // threads per key-switch inner-product CTA: 128 (k_ks_inner_tma2, two coefficients per thread) or 256
+int g_ks_stages = 3;   // ring depth of k_ks_inner_tma2 (3 or 4)
 
 template <int ST>
 __global__ void __launch_bounds__(256) k_ks_inner_tma(u64* __restrict__ acc, const u64* __restrict__ x_eval,
@@ -1391,8 +1484,124 @@ __global__ void __launch_bounds__(256) k_ks_inner_tma(u64* __restrict__ acc, con
   }
 }
 
+// k_ks_inner_tma with TPB threads per CTA and kMacTile / TPB output
+// coefficients per thread (independent MAC chains per thread).
+template <int ST, int TPB>
+__global__ void __launch_bounds__(TPB) k_ks_inner_tma2(u64* __restrict__ acc, const u64* __restrict__ x_eval,
+                                                      const u64* __restrict__ raised, const u64* __restrict__ key_b,
+                                                      const u64* __restrict__ key_a, Basis basis, u32 alpha,
+                                                      u32 ndig, u32 logN, u64 g, const ModConsts* __restrict__ mc,
+                                                      u32 nb, size_t x_bst, const u64* __restrict__ c0,
+                                                      size_t c0_bst, const u64* __restrict__ pR, u32 key_lq) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  KsStage* S = reinterpret_cast<KsStage*>(smem_raw);
+  __shared__ __align__(8) u64 full[ST];
+  const u32 N = 1u << logN, r = blockIdx.y, tile = blockIdx.x, tid = threadIdx.x;
+  const u32 b0 = blockIdx.z * kKsEntries;
+  const u32 ne = nb - b0 < (u32)kKsEntries ? nb - b0 : (u32)kKsEntries;
+  const u32 n_ext = basis.nlimbs();
+  const u32 mod = basis.mod_of(r);
+  const u64 q = mc[mod].q, ninv = mc[mod].ninv, one_sh = mc[mod].one_sh;
+  const u32 klq = key_lq ? key_lq : basis.Lq;
+  const size_t key_dst = (size_t)(klq + basis.np) * N;
+  const u32 kmod = mod < basis.Lq ? mod : klq + (mod - basis.Lq);
+  const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;
+  constexpr int CPT = kMacTile / TPB;
+  const u32 k = tile * kMacTile + tid;
+  const u32 src = g == 1 ? k : galois_src(k, g, logN);
+  u32 s_in[CPT];  // positions inside the source tile
+  s_in[0] = src & (kMacTile - 1);
+#pragma unroll
+  for (int c = 1; c < CPT; ++c) s_in[c] = (g == 1 ? k + c * TPB : galois_src(k + c * TPB, g, logN)) & (kMacTile - 1);
+  const size_t t_src = (size_t)(src & ~(u32)(kMacTile - 1));  // same block for the whole CTA
+  const size_t r_bst = (size_t)ndig * n_ext * N;
+  const bool ext = c0 != nullptr && r < basis.nq;
+  const u32 nst = ndig + (ext ? 1u : 0u);
+  auto issue = [&](u32 j) {
+    KsStage& T = S[j % ST];
+    u64* bar = &full[j % ST];
+    if (j < ndig) {
+      mbar_expect_tx(bar, (2 + ne) * kMacTile * 8);
+      const size_t kofs = (size_t)j * key_dst + (size_t)kmod * N + (size_t)tile * kMacTile;
+      bulk_g2s(T.kb, key_b + kofs, kMacTile * 8, bar);
+      bulk_g2s(T.ka, key_a + kofs, kMacTile * 8, bar);
+      for (u32 e = 0; e < ne; ++e) {
+        const u64* sp = j == own ? x_eval + (size_t)(b0 + e) * x_bst + (size_t)r * N
+                                 : raised + (size_t)(b0 + e) * r_bst + ((size_t)j * n_ext + r) * N;
+        bulk_g2s(T.x[e], sp + t_src, kMacTile * 8, bar);
+      }
+    } else {  // extended-basis term: c0 tiles
+      mbar_expect_tx(bar, ne * kMacTile * 8);
+      for (u32 e = 0; e < ne; ++e)
+        bulk_g2s(T.x[e], c0 + (size_t)(b0 + e) * c0_bst + (size_t)r * N + t_src, kMacTile * 8, bar);
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (u32 j = 0; j < (u32)ST - 1 && j < nst; ++j) issue(j);
+  u64 bh[kKsEntries][CPT], bl[kKsEntries][CPT], ah[kKsEntries][CPT], al[kKsEntries][CPT];
+#pragma unroll
+  for (int e = 0; e < kKsEntries; ++e)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) bh[e][c] = bl[e][c] = ah[e][c] = al[e][c] = 0;
+  for (u32 j = 0; j < nst; ++j) {
+    if (j > 0) __syncthreads();  // slot (j-1) % ST is free
+    if (tid == 0 && j + ST - 1 < nst) issue(j + ST - 1);
+    mbar_wait(&full[j % ST], (j / ST) & 1u);
+    const KsStage& T = S[j % ST];
+    if (j < ndig) {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const u64 kb = T.kb[tid + c * TPB], ka = T.ka[tid + c * TPB];
+#pragma unroll
+        for (int e = 0; e < kKsEntries; ++e) {
+          if ((u32)e >= ne) break;
+          const u64 x = T.x[e][s_in[c]];
+          mac128_lazy(bh[e][c], bl[e][c], x, kb);
+          mac128_lazy(ah[e][c], al[e][c], x, ka);
+        }
+      }
+    } else {
+      const u64 w = pR[r];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int e = 0; e < kKsEntries; ++e) {
+          if ((u32)e >= ne) break;
+          mac128_lazy(bh[e][c], bl[e][c], T.x[e][s_in[c]], w);
+        }
+    }
+    if ((j + 1) % kLazyTerms == 0 || j + 1 == nst) {
+#pragma unroll
+      for (int e = 0; e < kKsEntries; ++e)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          bh[e][c] = fold_hi(bh[e][c], q, one_sh);
+          ah[e][c] = fold_hi(ah[e][c], q, one_sh);
+        }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < kKsEntries; ++e) {
+    if ((u32)e >= ne) break;
+    u64* A = acc + (size_t)(b0 + e) * 2 * n_ext * N;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const u32 kc = k + c * TPB;
+      A[(size_t)r * N + kc] = redc128(bh[e][c], bl[e][c], q, ninv);
+      A[((size_t)n_ext + r) * N + kc] = redc128(ah[e][c], al[e][c], q, ninv);
+    }
+  }
+}
+
 int g_mac_tma = 1;    // 1: bulk-copy (TMA) staged k_mac_multi_tma
-int g_tma_stages = 4;  // ring depth of the TMA-staged MAC / key-switch kernels (4, 6, 8)
+int g_mac_minb = 1;  // minimum resident CTAs per SM (register cap) of k_mac_multi_tma: 1, 4, 5, 6
+int g_mac_tpb = 128;  // threads per plane-MAC CTA: 128 (k_mac_multi_tma2, two coefficients per thread) or 256
+int g_tma_stages = 3;  // ring depth of the TMA-staged plane MAC (128 threads: 2, 3, 4; 256: 4, 6, 8; the 256-thread key-switch kernel takes max(4, this))
 int g_mac_async = 1;  // 1: cp.async pipeline (k_mac_multi_async), 0: k_mac_multi_lanes
 
 int g_mac_lanes = 1;  // 1: k_mac_multi_lanes, 0: register-blocked k_mac_multi
@@ -1402,20 +1611,31 @@ cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN
   if (ng < 1 || ng > kMultiG) return cudaErrorInvalidValue;
   if (g_mac_tma && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
     dim3 g((1u << logN) / kMacTile, nq, 1);
-    static bool attr_done[9] = {};
-    auto go = [&](auto kern, int stages) -> cudaError_t {
+    static bool attr_done[2][9][8] = {};
+    auto go = [&](auto kern, int stages, int tpb) -> cudaError_t {
       const size_t sm = sizeof(MacStage) * stages;
-      if (!attr_done[stages]) {
+      if (!attr_done[tpb == 128][stages][g_mac_minb & 7]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e) return e;
-        attr_done[stages] = true;
+        attr_done[tpb == 128][stages][g_mac_minb & 7] = true;
       }
-      kern<<<g, 256, sm, st>>>(M, ng, nt, nq, logN, accumulate, mc);
+      kern<<<g, tpb, sm, st>>>(M, ng, nt, nq, logN, accumulate, mc);
       return cudaGetLastError();
     };
-    if (g_tma_stages >= 8) return go(k_mac_multi_tma<8>, 8);
-    if (g_tma_stages >= 6) return go(k_mac_multi_tma<6>, 6);
-    return go(k_mac_multi_tma<4>, 4);
+    if (g_mac_tpb == 128) {
+      if (g_tma_stages >= 4) return go(k_mac_multi_tma2<4, 128>, 4, 128);
+      if (g_tma_stages == 2) return go(k_mac_multi_tma2<2, 128, 6>, 2, 128);
+      switch (g_mac_minb) {
+        case 4: return go(k_mac_multi_tma2<3, 128, 4>, 3, 128);
+        case 5: return go(k_mac_multi_tma2<3, 128, 5>, 3, 128);
+        case 6: return go(k_mac_multi_tma2<3, 128, 6>, 3, 128);
+        default: return go(k_mac_multi_tma2<3, 128>, 3, 128);
+      }
+    }
+    if (g_tma_stages >= 8) return go(k_mac_multi_tma<8>, 8, 256);
+    if (g_tma_stages >= 6) return go(k_mac_multi_tma<6>, 6, 256);
+    if (g_mac_minb == 4) return go(k_mac_multi_tma2<4, 256, 4>, 4, 256);
+    return go(k_mac_multi_tma<4>, 4, 256);
   }
   if (g_mac_async && (1u << logN) % kMacTile == 0) {
     static bool attr = false;
@@ -1582,19 +1802,21 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
   if (g_ks_tma && nb >= (u32)g_ks_tma_min && (1u << logN) % kMacTile == 0) {
     const u32 nbb = nb ? nb : 1;
     dim3 grid((1u << logN) / kMacTile, basis.nlimbs(), (nbb + kKsEntries - 1) / kKsEntries);
-    static bool attr_done[9] = {};
+    static bool attr_done[2][9] = {};
+    const int tpb = g_ks_tpb == 128 ? 128 : 256;
     auto go = [&](auto kern, int stages) -> cudaError_t {
       const size_t sm = sizeof(KsStage) * stages;
-      if (!attr_done[stages]) {
+      if (!attr_done[tpb == 128][stages]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e) return e;
-        attr_done[stages] = true;
+        attr_done[tpb == 128][stages] = true;
       }
-      kern<<<grid, 256, sm, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nbb, x_bst, c0,
+      kern<<<grid, tpb, sm, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nbb, x_bst, c0,
                                   c0_bst, pR, key_lq);
       return cudaGetLastError();
     };
-    cudaError_t e = g_tma_stages >= 8 ? go(k_ks_inner_tma<8>, 8)
+    cudaError_t e = tpb == 128 ? (g_ks_stages == 3 ? go(k_ks_inner_tma2<3, 128>, 3) : go(k_ks_inner_tma2<4, 128>, 4))
+                    : g_tma_stages >= 8 ? go(k_ks_inner_tma<8>, 8)
                     : g_tma_stages >= 6 ? go(k_ks_inner_tma<6>, 6) : go(k_ks_inner_tma<4>, 4);
     if (e) return e;
   } else if ((nb <= 1 || g_ks_batch <= 1) && g_ks_pipe > 0) {

@@ -35,6 +35,10 @@ extern int g_mac_batch;
 extern int g_mac_lanes;
 extern int g_mac_async;
 extern int g_mac_tma;
+extern int g_mac_tpb;
+extern int g_mac_minb;
+extern int g_ks_tpb;
+extern int g_ks_stages;
 extern int g_tma_stages;
 // c0 (nullable): adds P * sigma_g(c0) on the Q limbs (pR[i] = P R mod q_i) --
 // the extended-basis (ModDown-free) rotation of double hoisting

@@ -1257,6 +1257,10 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "mac_async") g_mac_async = (int)value;
   else if (k == "mac_tma") g_mac_tma = (int)value;
   else if (k == "tma_stages") g_tma_stages = (int)value;
+  else if (k == "ks_tpb") g_ks_tpb = value == 128 ? 128 : 256;
+  else if (k == "ks_stages") g_ks_stages = (int)value;
+  else if (k == "mac_minb") g_mac_minb = (int)value;
+  else if (k == "mac_tpb") g_mac_tpb = value == 128 ? 128 : 256;
   else if (k == "merge_moddown") g_merge_moddown = (int)value;
   else return fail(HCNN_E_PARAMETER, "unknown option " + k);
   return HCNN_OK;

@@ -269,3 +269,58 @@ def test_lazy_mac_worst_case_residues(small):
         for out in (got[0], got[1], got_terms):
             row = out[:, i].cpu().numpy().view(np.uint64)
             assert (row == np.uint64(want)).all(), (i, q)
+
+
+# launch-shape knobs of the TMA-staged plane MAC and key-switch inner product
+# (threads per CTA, ring depth, register cap) and the values the engine ships with
+_KNOB_DEFAULTS = {"mac_tpb": 128, "tma_stages": 3, "mac_minb": 1, "ks_tpb": 128, "ks_stages": 3}
+_KNOB_VARIANTS = [
+    {"mac_tpb": 256, "tma_stages": 4, "ks_tpb": 256},
+    {"mac_tpb": 256, "tma_stages": 6, "ks_tpb": 256},
+    {"mac_tpb": 256, "tma_stages": 4, "mac_minb": 4},
+    {"mac_tpb": 128, "tma_stages": 4},
+    {"mac_tpb": 128, "tma_stages": 3, "mac_minb": 5},
+    {"mac_tpb": 128, "tma_stages": 2},
+    {"ks_tpb": 128, "ks_stages": 4},
+]
+
+
+def test_launch_shape_variants_bit_identical(small, cts):
+    """Every launch shape of k_mac_multi_tma(2) / k_ks_inner_tma(2) gives the
+    residues of the shipped shape: plane MACs over mixed packed / unpacked /
+    absent masks, and batched (>= 3 entries: TMA path) hoisted rotations."""
+    import torch
+    from paper_2310_16530_b200 import _native, ckks
+    params, ks = small
+    _, ct1, ct2 = cts
+    ctx = params.ctx
+    rng = np.random.default_rng(21)
+    lvl = ct1.level
+    srcs = [ct1.data, ct2.data] + [ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl), ks,
+                                                 rng).data for _ in range(11)]
+    mk = lambda: ctx.unop("to_mont", ckks.encode(rng.uniform(-1, 1, params.slots), params, lvl).data, lvl + 1)
+    masks = [[mk() if (g + t) % 3 else None for t in range(len(srcs))] for g in range(4)]
+    masks = [[(ctx.pack_masks(m, lvl)[0] if (m is not None and (g + t) % 2) else m) for t, m in enumerate(row)]
+             for g, row in enumerate(masks)]
+    batch = ckks.stack([ct1, ct2, ct1, ct2, ct1])
+
+    def run():
+        outs = [o.clone() for o in ctx.mac_terms_multi(srcs, masks, lvl)]
+        outs += [r.data.clone() for r in ckks.rotate_many(batch, [1, 2, 4], ks)]
+        torch.cuda.synchronize()
+        return outs
+
+    for k, v in _KNOB_DEFAULTS.items():
+        _native.set_option(k, v)
+    want = run()
+    try:
+        for var in _KNOB_VARIANTS:
+            for k, v in var.items():
+                _native.set_option(k, v)
+            got = run()
+            assert all(torch.equal(a, b) for a, b in zip(got, want)), var
+            for k, v in _KNOB_DEFAULTS.items():
+                _native.set_option(k, v)
+    finally:
+        for k, v in _KNOB_DEFAULTS.items():
+            _native.set_option(k, v)
