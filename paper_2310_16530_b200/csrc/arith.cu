@@ -1385,7 +1385,7 @@ struct KsStage {
   u64 x[kKsEntries][kMacTile];
 };
 int g_ks_tma = 1;
-int g_ks_tma_min = 3;  // smallest batch routed to k_ks_inner_tma
+int g_ks_tma_min = 2;  // smallest batch routed to the TMA inner product (measured: 2 beats 1 and 3 with k_ks_inner_tma2)
 int g_ks_tpb = 128;    // threads per key-switch inner-product CTA: 128 (k_ks_inner_tma2, two coefficients per thread) or 256
 int g_ks_stages = 3;   // ring depth of k_ks_inner_tma2 (3 or 4)
 

@@ -273,7 +273,7 @@ def test_lazy_mac_worst_case_residues(small):
 
 # launch-shape knobs of the TMA-staged plane MAC and key-switch inner product
 # (threads per CTA, ring depth, register cap) and the values the engine ships with
-_KNOB_DEFAULTS = {"mac_tpb": 128, "tma_stages": 3, "mac_minb": 1, "ks_tpb": 128, "ks_stages": 3}
+_KNOB_DEFAULTS = {"mac_tpb": 128, "tma_stages": 3, "mac_minb": 1, "ks_tpb": 128, "ks_stages": 3, "ks_tma_min": 2}
 _KNOB_VARIANTS = [
     {"mac_tpb": 256, "tma_stages": 4, "ks_tpb": 256},
     {"mac_tpb": 256, "tma_stages": 6, "ks_tpb": 256},
