@@ -326,8 +326,155 @@ def gen_hcnk():
     print("hcnk done")
 
 
+# ---------------------------------------------------------------------------
+def gen_packing():
+    """Layer goldens on the reference's own packing-unit setup
+    (test_packing.py:74-119, pack-unit N=512, L=7) for every HyPHEN layer
+    function on the ResNet20 path that the layer digests do not already
+    cover: stride-2 conv in both directions (test_packing.py:363-383),
+    downsample (packing.py:714-740, test_packing.py:515-525),
+    conv2d_fixed_baseline (packing.py:620-673, test_packing.py:447-477),
+    he_activation / avgpool / fc (test_packing.py:483-575); plus
+    cost_report_compare on the graph-unit tiny-cnn (graph.py:637-682,
+    test_graph.py:86-117, 504-508)."""
+    from hcnn import packing as P
+    from hcnn.aespa import AespaChannelParams, fold_channels, hermite_coeffs
+    obj = load_json()
+    res = {}
+    params = ckks.CkksParams.build("pack-unit", 512, 50, 40, 7, 50, 2)
+    slots = params.slots
+    A, B = P.FORMAT_A, P.FORMAT_B
+    m4A, m4B = P.PackingFormat(A, 4, 1, 16), P.PackingFormat(B, 4, 1, 16)
+    m2A, m2B = P.PackingFormat(A, 2, 1, 16), P.PackingFormat(B, 2, 1, 16)
+    m2A2, m2B2 = P.PackingFormat(A, 2, 2, 16), P.PackingFormat(B, 2, 2, 16)
+    w4, w2 = np.ones((4, 4, 3, 3)), np.ones((2, 2, 3, 3))
+    sh4, sh2 = P.TensorShape(4, 4, 4), P.TensorShape(2, 4, 4)
+    layers = [
+        (P.ConvLayerSpec(w4, 1, m4A, m4B), sh4, False),
+        (P.ConvLayerSpec(w4, 1, m4A, m4A), sh4, True),
+        (P.ConvLayerSpec(w2, 2, m2A, m2B2), sh2, False),
+        (P.ConvLayerSpec(w2, 2, m2B, m2A2), sh2, False),
+        (P.ConvLayerSpec(w2, 1, m2B2, m2A2), P.TensorShape(2, 2, 2), False),
+        (P.ConvLayerSpec(w2, 1, m2A2, m2B2), P.TensorShape(2, 2, 2), False),
+    ]
+    steps = set()
+    for layer, shape, fixed in layers:
+        steps |= P.conv_rotation_steps(layer, shape, slots, fixed=fixed)
+    steps |= P.pool_fc_rotation_steps(sh4, m4A, slots, 4, 3)
+    steps |= P.pool_fc_rotation_steps(sh4, m4B, slots, 4, 3)
+    steps = sorted(steps)
+    ks = ckks.keygen(params, np.random.default_rng(0xBEEF), rotations=steps)
+    res["params"] = {"n": params.n, "q": [m.q for m in params.q_mods], "p": [m.q for m in params.p_mods]}
+    res["steps"], res["key_seed"] = steps, 0xBEEF
+
+    def cts(x):
+        return h(np.stack([ct_arr(c) for c in x.cts]))
+
+    def rec(name, x_in, y, tally=None, extra=None):
+        d = {"input": cts(x_in), "output": cts(y) if hasattr(y, "cts") else h(ct_arr(y)),
+             "level": y.level, "scale": y.scale}
+        if hasattr(y, "cts"):
+            d["fmt"] = [y.fmt.variant, y.fmt.multiplex, y.fmt.gap, y.fmt.span]
+            d["shape"] = [y.shape.c, y.shape.h, y.shape.w]
+            d["dec"] = [float(v) for v in P.decrypt_tensor(y, ks).ravel()]
+        if tally is not None:
+            d["tally"] = tally.as_dict()
+        if extra:
+            d.update(extra)
+        res[name] = d
+
+    # stride 2, A -> B (test_packing.py:363-374) and B -> A
+    for name, seed, fin, fout in (("stride2_a2b", 11, m2A, m2B2), ("stride2_b2a", 13, m2B, m2A2)):
+        rng = np.random.default_rng(seed)
+        t = rng.standard_normal((2, 4, 4))
+        w = rng.standard_normal((2, 2, 3, 3)) * 0.4
+        b = rng.standard_normal(2) * 0.2
+        x = P.encrypt_tensor(t, fin, ks, rng, params.max_level)
+        tally = P.OpTally()
+        y = P.conv2d(x, P.ConvLayerSpec(w, 2, fin, fout, bias=b), ks, tally)
+        rec(name, x, y, tally)
+    # conv at the doubled gap (test_packing.py:376-383), both directions
+    rng = np.random.default_rng(12)
+    t = rng.standard_normal((2, 4, 4))
+    w = rng.standard_normal((2, 2, 3, 3)) * 0.4
+    x = P.encrypt_tensor(t, m2A, ks, rng, params.max_level)
+    mid = P.conv2d(x, P.ConvLayerSpec(w, 2, m2A, m2B2), ks)
+    tally = P.OpTally()
+    out = P.conv2d(mid, P.ConvLayerSpec(w, 1, m2B2, m2A2), ks, tally)
+    rec("gap2_b2a", mid, out, tally)
+    tally = P.OpTally()
+    out2 = P.conv2d(out, P.ConvLayerSpec(w, 1, m2A2, m2B2), ks, tally)
+    rec("gap2_a2b", out, out2, tally)
+    # fixed baseline (test_packing.py:447-477)
+    rng = np.random.default_rng(21)
+    t = rng.standard_normal((4, 4, 4))
+    w = rng.standard_normal((4, 4, 3, 3)) * 0.4
+    b = rng.standard_normal(4) * 0.2
+    xa = P.encrypt_tensor(t, m4A, ks, rng, params.max_level)
+    t_alt, t_fix = P.OpTally(), P.OpTally()
+    y_alt = P.conv2d(xa, P.ConvLayerSpec(w, 1, m4A, m4B, bias=b), ks, t_alt)
+    y_fix = P.conv2d_fixed_baseline(xa, P.ConvLayerSpec(w, 1, m4A, m4A, bias=b), ks, t_fix)
+    rec("alt_a2b", xa, y_alt, t_alt)
+    rec("fixed", xa, y_fix, t_fix)
+    rng = np.random.default_rng(22)
+    t = rng.standard_normal((4, 4, 4))
+    w = rng.standard_normal((4, 4, 3, 3)) * 0.4
+    x = P.encrypt_tensor(t, m4A, ks, rng, 4)
+    tally = P.OpTally()
+    y = P.conv2d_fixed_baseline(x, P.ConvLayerSpec(w, 1, m4A, m4A), ks, tally)
+    rec("fixed_l4", x, y, tally)
+    # activation (test_packing.py:483-500)
+    rng = np.random.default_rng(31)
+    t = rng.standard_normal((4, 4, 4))
+    chans = [AespaChannelParams(gamma=0.8 + 0.1 * i, beta=0.05 * i, mu=(0.1, -0.05, 0.02),
+                                sigma2=(1.1, 0.9, 1.3)) for i in range(4)]
+    quads = fold_channels(chans, hermite_coeffs(2))
+    x = P.encrypt_tensor(t, m4B, ks, rng, 4)
+    tally = P.OpTally()
+    y = P.he_activation(x, quads, ks, tally)
+    rec("act", x, y, tally)
+    # downsample (test_packing.py:515-525) on both formats
+    for name, seed, fmt in (("down_a", 32, m2A), ("down_b", 36, m2B)):
+        rng = np.random.default_rng(seed)
+        t = rng.standard_normal((2, 4, 4))
+        x = P.encrypt_tensor(t, fmt, ks, rng, 4)
+        tally = P.OpTally()
+        y = P.downsample(x, ks, tally)
+        rec(name, x, y, tally)
+    # pool + fc (test_packing.py:537-562)
+    for variant in (A, B):
+        rng = np.random.default_rng(34)
+        t = rng.standard_normal((4, 4, 4))
+        wfc = rng.standard_normal((3, 4)) * 0.5
+        bfc = rng.standard_normal(3) * 0.2
+        fmt = P.PackingFormat(variant, 4, 1, 16)
+        x = P.encrypt_tensor(t, fmt, ks, rng, 4)
+        tally = P.OpTally()
+        pooled = P.avgpool_global(x, ks, tally)
+        rec(f"pool_{variant}", x, pooled, tally)
+        tally = P.OpTally()
+        out = P.fully_connected(pooled, wfc, bfc, ks, tally)
+        rec(f"fc_{variant}", pooled, out, tally,
+            {"logits": [float(v) for v in P.read_logits(out, 3, fmt, ks)]})
+
+    # cost_report_compare on the graph-unit tiny-cnn (test_graph.py:86-117, 504-508)
+    gp = ckks.CkksParams.build("graph-unit", 2048, 50, 40, 11, 50, 2)
+    fx = graph.gen_fixture("tiny-cnn", 7, gp, golden_count=2)
+    g = graph.build_graph("tiny-cnn", fx, multiplex=4)
+    gsteps = sorted(graph.required_rotation_steps(g, gp.slots, include_fixed=True))
+    gks = ckks.keygen(gp, np.random.default_rng(0xD00D), rotations=gsteps)
+    plan = graph.plan_levels(g, gp.max_level)
+    x = np.array(fx["golden"][0]["input"])
+    cmp = graph.cost_report_compare(g, plan, x, gks, np.random.default_rng(9))
+    res["compare"] = {"steps": gsteps, "key_seed": 0xD00D, "report": cmp}
+    res["meta"] = meta()
+    obj["packing"] = res
+    save_json(obj)
+    print("packing done")
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "deskA", "bench16", "layers", "host", "hcnk"]
     for w in which:
         {"small": gen_small, "deskA": gen_deska, "bench16": gen_bench16, "layers": gen_layers,
-         "host": gen_host, "hcnk": gen_hcnk}[w]()
+         "host": gen_host, "hcnk": gen_hcnk, "packing": gen_packing}[w]()
