@@ -253,6 +253,10 @@ int hcnn_ntt_butterfly_peak(int device, int fast, double* bfly_per_s);
 /* limbs transformed since the last reset, by class:
  * [forward q<2^47, forward full, inverse q<2^47, inverse full] */
 void hcnn_ntt_limb_counts(unsigned long long* out4, int reset);
+/* key-switch accounting since the last reset (bench roofline row, no
+ * reference counterpart): [key switches, minimal HBM bytes (digits read
+ * once + switch keys + outputs), forward limb-NTTs, inverse limb-NTTs] */
+void hcnn_ks_counters(unsigned long long* out4, int reset);
 /* process-wide tuning knobs: "ntt_group_limbs" (NTT pass pairs run on groups
  * of this many limbs so the inter-pass data stays in L2; 0 = whole batch),
  * "ntt_hints" (1 = evict-last twiddles / streaming data loads) */

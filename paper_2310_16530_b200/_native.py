@@ -93,6 +93,7 @@ SIGNATURES = {
     "hcnn_profile_enable": (None, [_INT]),
     "hcnn_ntt_butterfly_peak": (_INT, [_INT, _INT, ctypes.POINTER(ctypes.c_double)]),
     "hcnn_ntt_limb_counts": (None, [ctypes.POINTER(ctypes.c_ulonglong), _INT]),
+    "hcnn_ks_counters": (None, [ctypes.POINTER(ctypes.c_ulonglong), _INT]),
     "hcnn_set_option": (_INT, [ctypes.c_char_p, ctypes.c_longlong]),
     "hcnn_profile_read": (_INT, [ctypes.c_char_p, _SZ, _INT]),
 }
@@ -161,6 +162,13 @@ def ntt_limb_counts(reset: bool = True) -> dict:
     buf = (ctypes.c_ulonglong * 4)()
     load().hcnn_ntt_limb_counts(buf, 1 if reset else 0)
     return {"fwd_fast": buf[0], "fwd_full": buf[1], "inv_fast": buf[2], "inv_full": buf[3]}
+
+
+def ks_counters(reset: bool = True) -> dict:
+    """Key switches since the last reset with their minimal HBM bytes and limb-NTT counts."""
+    buf = (ctypes.c_ulonglong * 4)()
+    load().hcnn_ks_counters(buf, 1 if reset else 0)
+    return {"keyswitches": buf[0], "min_bytes": buf[1], "fwd_limbs": buf[2], "inv_limbs": buf[3]}
 
 
 def set_option(name: str, value: int) -> None:

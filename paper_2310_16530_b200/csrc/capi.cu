@@ -289,6 +289,12 @@ static std::atomic<unsigned long long> g_kernels{0};
 
 static int ntt_nk(const hcnn_ctx* c) { return c->logN > 12 ? 2 : 1; }
 
+// key-switch accounting for the bench's key-switch roofline:
+// [key switches, minimal HBM bytes (digits read once + keys + outputs),
+//  forward limb-NTTs, inverse limb-NTTs] -- ModUp, inner product, ModDown
+static std::atomic<unsigned long long> g_ks_acc[4];
+static inline void ks_acc(int i, double v) { g_ks_acc[i] += (unsigned long long)v; }
+
 extern "C" {
 
 const char* hcnn_last_error(void) { return g_err.c_str(); }
@@ -805,6 +811,9 @@ static int ks_modup(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, cu
   m.base = w.xc;
   m.poly_stride = nq * N;
   m.basis = c->basis(nq, 0);
+  ks_acc(1, 8.0 * nb * nq * N);
+  ks_acc(2, (double)nb * ((double)nd * n_ext - nq));
+  ks_acc(3, (double)nb * nq);
   PK("ntt_inv_modup", 16.0 * nb * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), m, nq, nb, true, st));
   PK("modup", 8.0 * nb * (nq + (double)nd * (n_ext - c->alpha)) * N, 1, st,
      launch_modup(mu->d_tabs, mu->host.data(), nd, c->d_mc, w.xc, w.raised, c->alpha, n_ext, c->logN, st, nb,
@@ -831,6 +840,8 @@ static int ks_moddown(hcnn_ctx* c, u32 level, u64* acc, u64* lift, u64* out0, u6
   m.poly_stride = (size_t)n_ext * N;
   m.basis = c->basis(nq, c->K);
   m.first_limb = nq;
+  ks_acc(2, 2.0 * nb * nq);
+  ks_acc(3, 2.0 * nb * c->K);
   PK("ntt_inv_moddown", 16.0 * 2 * nb * c->K * N, ntt_nk(c), st, launch_ntt(c->tables(), m, c->K, 2 * nb, true, st));
   PK("moddown_fbc", 8.0 * 2 * nb * (c->K + nq) * N, 1, st,
      launch_fbc(c->moddown.dev, c->moddown.d_dev, c->d_mc, acc + nq * N, (size_t)n_ext * N, lift, nq * N,
@@ -854,6 +865,8 @@ static int ks_finish(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, u
                      u32 key_lq = 0) {
   const u32 nq = level + 1, n_ext = nq + c->K, nd = (nq + c->alpha - 1) / c->alpha;
   const size_t N = c->n;
+  ks_acc(0, nb);
+  ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * nq) * N);
   PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, st,
      launch_ks_inner(w.acc, x_eval, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, g, c->d_mc, st,
                      nb, x_bst, nullptr, 0, nullptr, key_lq));
@@ -945,6 +958,8 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
       const u64 g = galois[i] % (2ull * c->n);
       S.out[j] = outs[i];
       S.g[j] = g;
+      ks_acc(0, nb);
+      ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * nq) * N);
       PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
          launch_ks_inner(w.acc + j * a_step, c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd,
                          c->logN, g, c->d_mc, STREAM(s), nb, ct, nullptr, 0, nullptr, key_lqs ? key_lqs[i] : 0));
@@ -955,6 +970,8 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
     m.poly_stride = (size_t)n_ext * N;
     m.basis = c->basis(nq, c->K);
     m.first_limb = nq;
+    ks_acc(2, (double)np * nq);
+    ks_acc(3, (double)np * c->K);
     PK("ntt_inv_moddown", 16.0 * np * c->K * N, ntt_nk(c), STREAM(s),
        launch_ntt(c->tables(), m, c->K, np, true, STREAM(s)));
     PK("moddown_fbc", 8.0 * np * (c->K + nq) * N, 1, STREAM(s),
@@ -991,6 +1008,8 @@ int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* c, uint64_t* const* outs, const uint
   if (rc) return rc;
   for (u32 i = 0; i < n_rot; ++i) {
     const u64 g = galois[i] % (2ull * c->n);
+    ks_acc(0, nb);
+    ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * n_ext + nb * nq) * N);
     PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext + nb * nq) * N, 1, STREAM(s),
        launch_ks_inner(outs[i], c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd, c->logN, g,
                        c->d_mc, STREAM(s), nb, ct, cts, ct, c->d_pR, key_lqs ? key_lqs[i] : 0));
@@ -1013,6 +1032,8 @@ static int moddown_rescale(hcnn_ctx* c, u32 level, u64* in_ext, u64* lift, u64* 
   m.poly_stride = (size_t)n_ext * N;
   m.basis = c->basis(nq, c->K);
   m.first_limb = l;
+  ks_acc(2, 2.0 * nb * l);
+  ks_acc(3, 2.0 * nb * (c->K + 1));
   PK("ntt_inv_moddown", 16.0 * 2 * nb * (c->K + 1) * N, ntt_nk(c), st,
      launch_ntt(c->tables(), m, c->K + 1, 2 * nb, true, st));
   PK("moddown_fbc", 8.0 * 2 * nb * (c->K + 1 + l) * N, 1, st,
@@ -1065,6 +1086,8 @@ int hcnn_hmult_rescale_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* a, cons
                      c->d_mc, STREAM(s)));
   rc = ks_modup(c, level, w.lift, w, STREAM(s), nb, ct);
   if (rc) return rc;
+  ks_acc(0, nb);
+  ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * nq) * N);
   PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
      launch_ks_inner(w.acc, w.lift, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, 1, c->d_mc,
                      STREAM(s), nb, ct, nullptr, 0, nullptr, 0));
@@ -1273,6 +1296,13 @@ int hcnn_ntt_butterfly_peak(int device, int fast, double* bfly_per_s) {
   CK(cudaSetDevice(device));
   CK((cudaError_t)ntt_butterfly_peak(fast, bfly_per_s));
   return HCNN_OK;
+}
+
+void hcnn_ks_counters(unsigned long long* out4, int reset) {
+  for (int i = 0; i < 4; ++i) {
+    if (out4) out4[i] = g_ks_acc[i].load();
+    if (reset) g_ks_acc[i] = 0;
+  }
 }
 
 void hcnn_ntt_limb_counts(unsigned long long* out4, int reset) {

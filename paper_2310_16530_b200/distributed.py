@@ -13,6 +13,10 @@ decrypted results to rank 0.  Works over NCCL (GPU) and gloo (CPU tests).
 from __future__ import annotations
 
 import os
+import socket
+import subprocess
+import sys
+import time
 from dataclasses import dataclass
 from typing import Any, Callable, Sequence
 
@@ -73,3 +77,103 @@ def run_sharded(items: Sequence[Any], fn: Callable[[Any], Any], gather: bool = T
         for i, v in part:
             out[i] = v
     return out
+
+
+class Cluster:
+    """One process per GPU (torchrun environment): device binding, process
+    group (NCCL on GPUs, gloo on CPU), barrier, MAX over ranks, ordered
+    gather to rank 0 and the timed region every multi-rank number goes
+    through.  world_size 1 needs no process group and is the identity."""
+
+    def __init__(self, backend: str | None = None):
+        import torch
+        self.torch = torch
+        self.rank, self.local, self.world = env_rank()
+        self.cuda = torch.cuda.is_available() and backend != "gloo"
+        if self.cuda:
+            torch.cuda.set_device(self.local)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            be = backend or ("nccl" if self.cuda else "gloo")
+            if not dist.is_initialized():
+                kw = {"device_id": torch.device(f"cuda:{self.local}")} if be == "nccl" else {}
+                dist.init_process_group(be, rank=self.rank, world_size=self.world, **kw)
+            self.dist = dist
+
+    def sync(self):
+        if self.cuda:
+            self.torch.cuda.synchronize()
+
+    def barrier(self):
+        self.sync()
+        if self.dist is not None:
+            self.dist.barrier()
+        self.sync()
+
+    def max(self, v: float) -> float:
+        if self.dist is None:
+            return float(v)
+        dev = "cuda" if self.cuda else "cpu"
+        t = self.torch.tensor([float(v)], device=dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather(self, obj: Any) -> list[Any] | None:
+        """Rank 0 gets [obj of rank 0, obj of rank 1, ...]; others None."""
+        if self.dist is None:
+            return [obj]
+        parts: list[Any] = [None] * self.world
+        self.dist.all_gather_object(parts, obj)
+        return parts if self.rank == 0 else None
+
+    def shard(self, total: int) -> range:
+        return ShardPlan(total, self.world).indices(self.rank)
+
+    def timed(self, fn: Callable[[], Any], steps: int, nvtx: str | None = None) -> float:
+        """ms over `steps` calls of fn between two barriers (+ device syncs),
+        CUDA events on the current stream (wall clock on CPU); MAX over ranks."""
+        torch = self.torch
+        self.barrier()
+        if self.cuda:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if nvtx:
+                torch.cuda.nvtx.range_push(nvtx)
+            e0.record()
+            for _ in range(steps):
+                fn()
+            e1.record()
+            if nvtx:
+                torch.cuda.nvtx.range_pop()
+            self.barrier()
+            ms = e0.elapsed_time(e1)
+        else:
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                fn()
+            self.barrier()
+            ms = (time.perf_counter() - t0) * 1e3
+        return self.max(ms)
+
+    def close(self):
+        if self.dist is not None and self.dist.is_initialized():
+            self.dist.destroy_process_group()
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(nproc: int, script: str, argv: Sequence[str]) -> int:
+    """Re-run `script argv` as `nproc` ranks under torch.distributed.run on
+    this node (one process per GPU, rendezvous on 127.0.0.1); returns the
+    launcher's exit code.  Used when a multi-GPU run is started without
+    torchrun (bench.py --gpus N)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", script, *argv]
+    return subprocess.call(cmd)

@@ -60,3 +60,29 @@ def test_gloo_world2_gather_and_max():
     # first 4 items on rank 0, last 3 on rank 1
     assert [r for _, r in out] == [0, 0, 0, 0, 1, 1, 1]
     assert t == 11.0
+
+
+def test_bench_multi_rank_path_gloo():
+    """bench.py --gpus 2 without torchrun re-launches itself as 2 ranks under
+    torch.distributed.run (127.0.0.1 rendezvous) and runs the same
+    Cluster -> shard -> timed -> gather skeleton the GPU workloads use
+    (here over gloo with a CPU stub step): one JSON line from rank 0 with
+    every image owned by exactly one rank."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--workload", "selftest",
+                        "--images-per-gpu", "3", "--steps", "2", "--warmup", "1"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["backend"] == "gloo" and line["warmup"] == 3
+    owned = sorted(i for p in line["per_rank"] for i in p["images"])
+    assert owned == list(range(6))
+    assert [p["images"] for p in sorted(line["per_rank"], key=lambda p: p["rank"])] == [[0, 1, 2], [3, 4, 5]]
+    assert line["ms_per_step"] > 0 and line["value"] > 0

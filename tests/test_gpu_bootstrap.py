@@ -204,3 +204,37 @@ def test_fused_hmult_rescale(boot12):
             dg = ckks.decode(ckks.decrypt(g, ks), params, imag_tol=None)
             dw = ckks.decode(ckks.decrypt(w, ks), params, imag_tol=None)
             assert np.max(np.abs(dg - dw)) < 1e-6
+
+
+def test_boot16_full_slot_precision():
+    """BASELINE cfg 3 at full size: N=2^16, 32768 slots, the bench's
+    boot16 chain.  A single bootstrap and a 2-entry batched bootstrap
+    (entry-wise identical to it) keep >= 19 bits of precision, and the
+    CUDA-graph replay bench.py times gives the eager residues."""
+    import torch
+    from paper_2310_16530_b200 import bootstrap as bt, ckks
+    cfg = bt.BootConfig()
+    params = bt.boot_params("boot16", 1 << 16, 8, cfg)
+    b = bt.Bootstrapper(params, cfg)
+    ks = b.keygen(np.random.default_rng(16), rotations=[1])
+    rng = np.random.default_rng(3)
+    vals = [rng.uniform(-1, 1, params.slots) for _ in range(2)]
+    cts = [ckks.encrypt(ckks.encode(v, params, 0), ks, rng) for v in vals]
+    single = b.bootstrap(cts[0], ks)
+    assert single.level == b.output_level
+    err = float(np.max(np.abs(ckks.decode(ckks.decrypt(single, ks), params, imag_tol=None) - vals[0])))
+    print("boot16 bits", -np.log2(err))
+    assert -np.log2(err) >= 19.0
+    x = ckks.stack(cts)
+    batch = ckks.unstack(b.bootstrap(x, ks))
+    assert torch.equal(batch[0].data, single.data)
+    err1 = float(np.max(np.abs(ckks.decode(ckks.decrypt(batch[1], ks), params, imag_tol=None) - vals[1])))
+    assert -np.log2(err1) >= 19.0
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = b.bootstrap(x, ks)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ckks.unstack(out)[0].data, single.data)
+    assert torch.equal(ckks.unstack(out)[1].data, batch[1].data)

@@ -82,7 +82,9 @@ def r20_bench():
                                   s.graph.formats[-1], s.ks) for d, sc, _ in replay]
     plain = [graph.execute(s.graph, s.plan, x, mode="plaintext-ref")[0] for x in raw]
     res = {"eager": eager, "replay": replay, "logits": logits, "plain": plain, "tally": tally,
-           "runner_tally": runner.report.totals().as_dict()}
+           "runner_tally": runner.report.totals().as_dict(),
+           "per_layer": [{"name": r["name"], "kind": r["kind"], "tally": r["tally"], "entry_level": r["entry_level"]}
+                         for r in runner.report.per_layer]}
     yield res
     del runner, cache, s, imgs
     _free_setup()
@@ -94,6 +96,20 @@ def test_replay_equals_eager(r20_bench):
     for (de, se, le), (dr, sr, lr) in zip(r20_bench["eager"], r20_bench["replay"]):
         assert le == lr and se == sr
         assert torch.equal(de, dr), "CUDA-graph replay differs from eager execution"
+
+
+def test_committed_tally_matches_executor(r20_bench):
+    """bench.py --impl reference extrapolates the CPU oracle over the
+    committed per-layer tally (paper_2310_16530_b200/data/resnet20_tally.json);
+    it must be exactly what the executor runs."""
+    path = ROOT / "paper_2310_16530_b200" / "data" / "resnet20_tally.json"
+    saved = json.loads(path.read_text())
+    if saved["per_layer"] != r20_bench["per_layer"]:
+        (ROOT / "gpurun_out").mkdir(exist_ok=True)
+        (ROOT / "gpurun_out" / "resnet20_tally.json").write_text(
+            json.dumps({"per_layer": r20_bench["per_layer"], "totals": r20_bench["tally"]}, indent=1) + "\n")
+    assert saved["per_layer"] == r20_bench["per_layer"]
+    assert saved["totals"] == r20_bench["tally"]
 
 
 def test_bench_config_logits(r20_bench):

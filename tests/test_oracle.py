@@ -83,3 +83,23 @@ def test_desk_a_hashes(golden_hashes):
     coeff_rng = np.random.default_rng(0)
     coeff = np.stack([coeff_rng.integers(0, q, size=P.n, dtype=np.uint64) for q in P.ext])
     assert h(O.ntt(coeff, P.ext)) == g["ntt_out_seed0"]
+
+
+def test_cpu_bench_sampler_and_extrapolation():
+    """bench.py's CPU-baseline leg: the pinned single-threaded sampler runs
+    the reference's five primitives per level (oracle/cpu_bench.py) and the
+    extrapolation multiplies a per-layer tally by level-interpolated times."""
+    from oracle import cpu_bench
+    from oracle import ckks_oracle as O
+    P = O.OParams.build(256, 50, 40, 5, 50, 2)
+    spec = {"n": P.n, "qs": P.qs, "ps": P.ps, "delta": P.delta, "levels": [1, 5], "reps": 1}
+    out = cpu_bench.launch(spec, sorted(__import__("os").sched_getaffinity(0))[:1])[0]
+    assert out["threads"] == 1 and set(out["levels"]) == {"1", "5"}
+    for lv in out["levels"].values():
+        assert all(lv[op] > 0 for op in cpu_bench.OPS)
+    fake = {"1": {op: 1.0 for op in cpu_bench.OPS}, "5": {op: 3.0 for op in cpu_bench.OPS}}
+    rows = [{"entry_level": 3, "tally": {"rotations": 2, "hadds": 1}},
+            {"entry_level": 5, "tally": {"pmults": 4}}, {"entry_level": 0, "tally": {"rescales": 1}}]
+    x = cpu_bench.extrapolate(fake, rows)
+    # level 3 -> 2.0 s per op; level 5 -> 3.0; level 0 -> 0.5 (linear below the lowest sample)
+    assert x["s_per_image"] == 2 * 2.0 + 1 * 2.0 + 4 * 3.0 + 0.5
