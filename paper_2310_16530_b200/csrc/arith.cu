@@ -1365,6 +1365,150 @@ __global__ void __launch_bounds__(TPB, MINB > 1 ? MINB : 0) k_mac_multi_tma2(Mac
 }
 
 // ---------------------------------------------------------------------------
+// k_mac_multi_tma3: the plane MAC with a full / empty mbarrier ring (no
+// CTA-wide barrier per term: warps run up to ST terms apart, the producer
+// thread refills a slot once every warp has arrived on its "empty"
+// barrier) and, for limbs with q < 2^42 (FAST: the 40-bit application
+// primes), a 96-bit carry-chain accumulator fed by 32-bit halves:
+//   a m = a0 m0 + (a0 m1 + a1 m0) 2^32 + a1 m1 2^64   (a1, m1 < 2^10)
+// into T = (hi:lo) + mid 2^32 -- 5 IMADs per product instead of the 128-bit
+// product's ~11, no lazy folds (T < 2^90 < q 2^64 for <= 48 terms), one
+// REDC at the end: the same canonical sum * R^-1 mod q as mac128.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mac96(u64& lh, u64& mid, u32 a0, u32 a1, u32 m0, u32 m1) {
+  asm("{\n\t.reg .u32 lo, hi, ml, mh;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "mov.b64 {ml, mh}, %1;\n\t"
+      "mad.lo.cc.u32 lo, %2, %4, lo;\n\t"
+      "madc.hi.cc.u32 hi, %2, %4, hi;\n\t"
+      "madc.lo.u32 mh, %3, %5, mh;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t"
+      "mov.b64 %1, {ml, mh};\n\t"
+      "mad.wide.u32 %1, %2, %5, %1;\n\t"
+      "mad.wide.u32 %1, %3, %4, %1;\n\t"
+      "}"
+      : "+l"(lh), "+l"(mid)
+      : "r"(a0), "r"(a1), "r"(m0), "r"(m1));
+}
+// T = lh + mid 2^32 (< 2^90) -> T R^-1 mod q
+__device__ __forceinline__ u64 redc96(u64 lh, u64 mid, u64 q, u64 ninv) {
+  const u64 L2 = lh + (mid << 32);
+  const u64 H = (mid >> 32) + (L2 < lh ? 1ull : 0ull);
+  return redc128(H, L2, q, ninv);
+}
+
+template <int ST, int TPB, bool FAST>
+__global__ void __launch_bounds__(TPB + 32) k_mac_multi_tma3(MacMulti M, int ng, int nt, u32 nq, u32 logN, u32 r0,
+                                                             int accumulate, const ModConsts* __restrict__ mc) {
+  // TPB consumer threads + one producer warp (warp TPB/32) that only issues the bulk copies
+  constexpr int CPT = kMacTile / TPB, NW = TPB / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MacStage* S = reinterpret_cast<MacStage*>(smem_raw);
+  __shared__ __align__(8) u64 full[ST];
+  __shared__ __align__(8) u64 empty[ST];
+  __shared__ unsigned char flags[kMultiT];
+  const u32 N = 1u << logN, r = blockIdx.y + r0, k0 = blockIdx.x * kMacTile, tid = threadIdx.x;
+  const u64 q = mc[r].q, ninv = mc[r].ninv, one_sh = mc[r].one_sh;
+  const unsigned hb = r > 0 ? packed_hb(r, M.wide) : 2u;
+  for (u32 i = tid; i < (u32)nt; i += TPB + 32) {
+    u32 fl = 0;
+    for (int g = 0; g < ng; ++g)
+      if (M.mask[g][i]) fl |= (1u << g) | ((M.packed[g][i] && r > 0) ? (16u << g) : 0u);
+    flags[i] = (unsigned char)fl;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= (u32)TPB) {  // producer warp
+    if (tid == (u32)TPB) {
+      for (int t = 0; t < nt; ++t) {
+        const int slot = t % ST;
+        if (t >= ST) mbar_wait(&empty[slot], (u32)(t / ST - 1) & 1u);  // consumers released term t - ST
+        mac_stage_bulk(S[slot], &full[slot], M, t, flags[t], r, nq, N, k0);
+      }
+    }
+    return;
+  }
+  // per output poly-coefficient: FAST (lh, mid) of the 96-bit sum; generic
+  // the lazy 128-bit (l, h)
+  u64 AL[kMultiG][2 * CPT], AH[kMultiG][2 * CPT];
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g)
+#pragma unroll
+    for (int p = 0; p < 2 * CPT; ++p) AL[g][p] = AH[g][p] = 0;
+  for (int t = 0; t < nt; ++t) {
+    const int slot = t % ST;
+    const u32 fl = flags[t];
+    mbar_wait(&full[slot], (u32)(t / ST) & 1u);
+    const MacStage& C = S[slot];
+    u64 x[2 * CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      x[2 * c] = C.ct[0][tid + c * TPB];
+      x[2 * c + 1] = C.ct[1][tid + c * TPB];
+    }
+#pragma unroll
+    for (int g = 0; g < kMultiG; ++g) {
+      if (!(fl >> g & 1u)) continue;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const u32 i = tid + c * TPB;
+        u32 m0, m1;
+        if (fl >> (4 + g) & 1u) {
+          m0 = reinterpret_cast<const unsigned*>(C.mask[g])[i];
+          m1 = (u32)packed_hi(reinterpret_cast<const unsigned char*>(C.mask[g]) + kMacTile * 4, i, hb);
+        } else {
+          const u64 m = C.mask[g][i];
+          m0 = (u32)m;
+          m1 = (u32)(m >> 32);
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const u64 a = x[2 * c + p];
+          if constexpr (FAST) mac96(AL[g][2 * c + p], AH[g][2 * c + p], (u32)a, (u32)(a >> 32), m0, m1);
+          else mac128_lazy(AH[g][2 * c + p], AL[g][2 * c + p], a, ((u64)m1 << 32) | m0);
+        }
+      }
+    }
+    if constexpr (!FAST) {
+      if ((t + 1) % kLazyTerms == 0 || t + 1 == nt) {
+#pragma unroll
+        for (int g = 0; g < kMultiG; ++g)
+#pragma unroll
+          for (int p = 0; p < 2 * CPT; ++p) AH[g][p] = fold_hi(AH[g][p], q, one_sh);
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
+  }
+  const size_t pst = (size_t)nq * N;
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g) {
+    if (g >= ng) break;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const size_t off = (size_t)r * N + k0 + tid + c * TPB;
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        u64* d = M.out[g] + p * pst + off;
+        const int k = 2 * c + p;
+        u64 y = FAST ? redc96(AL[g][k], AH[g][k], q, ninv) : redc128(AH[g][k], AL[g][k], q, ninv);
+        if (accumulate) y = add_mod(y, *d, q);
+        *d = y;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Key-switch inner product with TMA-staged operands.  A CTA owns one
 // 256-coefficient tile of one output limb r for up to kKsEntries batch
 // entries; per digit j one elected thread bulk-copies the two key rows'
@@ -1598,7 +1742,9 @@ __global__ void __launch_bounds__(TPB) k_ks_inner_tma2(u64* __restrict__ acc, co
   }
 }
 
-int g_mac_tma = 1;    // 1: bulk-copy (TMA) staged k_mac_multi_tma
+int g_mac_tma = 3;    // 1: bulk-copy (TMA) staged k_mac_multi_tma(2), 3: warp-specialised k_mac_multi_tma3
+int g_mac3_stages = 4;  // k_mac_multi_tma3 ring depth (2, 3, 4, 6); tools/mac_probe.py: 4 = 3 < 2, 6
+int g_mac3_tpb = 128;   // k_mac_multi_tma3 threads per CTA (128 or 256)
 int g_mac_minb = 1;  // minimum resident CTAs per SM (register cap) of k_mac_multi_tma: 1, 4, 5, 6
 int g_mac_tpb = 128;  // threads per plane-MAC CTA: 128 (k_mac_multi_tma2, two coefficients per thread) or 256
 int g_tma_stages = 3;  // ring depth of the TMA-staged plane MAC (128 threads: 2, 3, 4; 256: 4, 6, 8; the 256-thread key-switch kernel takes max(4, this))
@@ -1609,6 +1755,29 @@ int g_mac_lanes = 1;  // 1: k_mac_multi_lanes, 0: register-blocked k_mac_multi
 cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN, int accumulate,
                              const ModConsts* mc, cudaStream_t st) {
   if (ng < 1 || ng > kMultiG) return cudaErrorInvalidValue;
+  if (g_mac_tma == 3 && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
+    // rows [0, fast_from): generic 128-bit MACs; [fast_from, nq): 96-bit carry chains
+    static bool attr3[2][9][2] = {};
+    const int stages = g_mac3_stages, tpb = g_mac3_tpb;
+    auto go3 = [&](auto kern, int fast, u32 r0, u32 rows, int kst, int ktpb) -> cudaError_t {
+      if (rows == 0) return cudaSuccess;
+      const size_t sm = sizeof(MacStage) * kst;
+      if (!attr3[fast][kst][ktpb == 256]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e) return e;
+        attr3[fast][kst][ktpb == 256] = true;
+      }
+      kern<<<dim3((1u << logN) / kMacTile, rows, 1), ktpb + 32, sm, st>>>(M, ng, nt, nq, logN, r0, accumulate, mc);
+      return cudaGetLastError();
+    };
+    const u32 ff = M.fast_from < 1 ? 1 : (M.fast_from > nq ? nq : M.fast_from);
+    cudaError_t e = go3(k_mac_multi_tma3<3, 128, false>, 0, 0, ff, 3, 128);
+    if (e) return e;
+#define MAC3(ST, TPB) if (stages == ST && tpb == TPB) return go3(k_mac_multi_tma3<ST, TPB, true>, 1, ff, nq - ff, ST, TPB)
+    MAC3(2, 128); MAC3(4, 128); MAC3(6, 128); MAC3(2, 256); MAC3(3, 256); MAC3(4, 256); MAC3(6, 256);
+#undef MAC3
+    return go3(k_mac_multi_tma3<3, 128, true>, 1, ff, nq - ff, 3, 128);
+  }
   if (g_mac_tma && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
     dim3 g((1u << logN) / kMacTile, nq, 1);
     static bool attr_done[2][9][8] = {};

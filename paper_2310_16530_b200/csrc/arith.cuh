@@ -35,6 +35,8 @@ extern int g_mac_batch;
 extern int g_mac_lanes;
 extern int g_mac_async;
 extern int g_mac_tma;
+extern int g_mac3_stages;
+extern int g_mac3_tpb;
 extern int g_mac_tpb;
 extern int g_mac_minb;
 extern int g_ks_tpb;
@@ -108,6 +110,7 @@ struct MacMulti {
   const u64* mask[kMultiG][kMultiT];
   u64* out[kMultiG];
   unsigned char packed[kMultiG][kMultiT];  // 1: mask in the packed layout (launch_pack_masks)
+  unsigned fast_from;  // limbs r >= fast_from (>= 1) have q < 2^42: 96-bit carry-chain MACs (k_mac_multi_tma3)
   unsigned long long wide;                 // packed layout: bit r set = limb r needs a 16-bit high plane
 };
 // Packed resident masks: limb 0 as u64 [N]; limbs 1..nq-1 as u32 low words

@@ -391,7 +391,7 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
   u64 qmax = 0;
   for (u64 q : c->mods) {
     qmax = q > qmax ? q : qmax;
-    // NTT modulus class: 2 = FP64-quotient forward path, 1 = q < 2^47 fast path, 0 = full width
+    // NTT modulus class: 2 = FP64 network, 1 = q < 2^47 integer fast path, 0 = full width
     c->small.push_back(q < (1ull << kFpBits) ? 2 : q < (1ull << 47) ? 1 : 0);
   }
   c->ntt2_ok = ntt2_supported(c->logN) && qmax < (1ull << 61);  // 8q < 2^64 (approximate-quotient NTT)
@@ -402,15 +402,16 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
     const u32 N1 = n >> 8;
     std::vector<ulonglong2> ctw((size_t)c->nmods * N), ictw((size_t)c->nmods * N);
     for (u32 m = 0; m < c->nmods; ++m) {
-      // FP64-quotient forward butterflies (ntt2.cu, q < 2^kFpBits): the
-      // companion is double(wp * 2^-64) ~ w/q instead of the Shoup word
+      // FP64 network (ntt2.cu, q < 2^kFpBits), both directions: a twiddle
+      // is the pair (double(w), double(wp * 2^-64) ~ w/q) as bit patterns
       const bool fp = kNttFp && c->mods[m] < (1ull << kFpBits);
-      auto fwd_comp = [&](u64 wp) -> u64 {
-        if (!fp) return wp;
-        const double d = (double)wp * 0x1p-64;
+      auto dbits = [](double d) -> u64 {
         u64 bits;
         std::memcpy(&bits, &d, 8);
         return bits;
+      };
+      auto pair_of = [&](u64 w, u64 wp) -> ulonglong2 {
+        return fp ? make_ulonglong2(dbits((double)w), dbits((double)wp * 0x1p-64)) : make_ulonglong2(w, wp);
       };
       for (u32 g = 0; g < N1; ++g) {
         ulonglong2* F = &ctw[((size_t)m * N1 + g) * 256];
@@ -420,10 +421,10 @@ int hcnn_ctx_create(hcnn_ctx** out, int device, uint32_t n, const uint64_t* q_mo
         for (u32 s = 0; s < 8; ++s)
           for (u32 i = 0; i < (1u << s); ++i) {
             size_t src = (size_t)(N1 + g) * (1u << s) + i;
-            F[(1u << s) - 1 + i] = make_ulonglong2(tw[m * N + src], fwd_comp(twp[m * N + src]));
+            F[(1u << s) - 1 + i] = pair_of(tw[m * N + src], twp[m * N + src]);
             u32 nb = 1u << s;  // inverse stage with nb blocks
             size_t isrc = (size_t)nb * (N1 + g) + i;
-            I[nb - 1 + i] = make_ulonglong2(itw[m * N + isrc], itwp[m * N + isrc]);
+            I[nb - 1 + i] = pair_of(itw[m * N + isrc], itwp[m * N + isrc]);
           }
       }
     }
@@ -1205,6 +1206,8 @@ int hcnn_mac_terms_multi_packed(hcnn_ctx* c, uint64_t* const* outs, const uint64
       const u32 nt = std::min<u32>(kMultiT, n_terms - t0);
       MacMulti M;
       M.wide = c->wide;
+      M.fast_from = nq;
+      while (M.fast_from > 1 && c->mods[M.fast_from - 1] < (1ull << 42)) --M.fast_from;
       for (u32 t = 0; t < nt; ++t) M.ct[t] = cts[t0 + t];
       // packed bytes relative to u64 rows, averaged over the limbs
       const double pf = nq > 1 ? (double)packed_hi_off(nq, nq, 1, c->wide) / (8.0 * nq) : 1.0;
@@ -1271,6 +1274,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_hints") g_ntt_tuning.hints = (int)value;
   else if (k == "ntt_occupancy") g_ntt_tuning.occupancy = (int)value;
   else if (k == "ntt_split") g_ntt_tuning.split = (int)value;
+  else if (k == "ntt_f64_minb") g_ntt_tuning.f64_minb = (int)value;
   else if (k == "ks_batch") g_ks_batch = (int)value;
   else if (k == "ks_pipe") g_ks_pipe = (int)value;
   else if (k == "ks_tma") g_ks_tma = (int)value;
@@ -1279,6 +1283,8 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "mac_lanes") g_mac_lanes = (int)value;
   else if (k == "mac_async") g_mac_async = (int)value;
   else if (k == "mac_tma") g_mac_tma = (int)value;
+  else if (k == "mac3_stages") g_mac3_stages = (int)value;
+  else if (k == "mac3_tpb") g_mac3_tpb = (int)value;
   else if (k == "tma_stages") g_tma_stages = (int)value;
   else if (k == "ks_tpb") g_ks_tpb = value == 128 ? 128 : 256;
   else if (k == "ks_stages") g_ks_stages = (int)value;

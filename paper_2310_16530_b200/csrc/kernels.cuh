@@ -35,6 +35,7 @@ struct NttTuning {
   int hints = 1;
   int occupancy = 0;  // 1: register-capped kernels (more resident warps)
   int split = 2;      // 1: separate launches per modulus class, 2: forward transforms only
+  int f64_minb = 1;   // FP64 chunk passes: min CTAs per SM hint (1, 5 or 6)
 };
 extern NttTuning g_ntt_tuning;
 
@@ -56,9 +57,11 @@ cudaError_t launch_ntt(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 n
 cudaError_t ntt_configure_smem();
 bool ntt2_supported(u32 logN);
 int ntt_butterfly_peak(int fast, double* bfly_per_s);
-// moduli below 2^kFpBits run the forward fast path with an FP64 quotient;
-// their forward chunk-twiddle companions are double(w/q) bit patterns
-constexpr int kFpBits = 44;
+// moduli below 2^kFpBits run both transforms on the FP64 network
+// (ntt2.cu); their chunk twiddles are (double(w), double(w/q)) bit patterns.
+// 2^41 keeps the unreduced inverse pass (inputs < 4q, 2^8 growth) and the
+// forward pass pair inside the exact window (|operand| < 2^51).
+constexpr int kFpBits = 41;
 constexpr bool kNttFp = true;
 extern unsigned long long g_ntt_limbs[4];
 extern std::atomic<unsigned long long> g_ntt_extra_launches;  // split NTT launches beyond one pair per call

@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256, MINB) ntt2_fwd_cols(LimbMap map, const Mo
   // MODE 0: full-width, 1: q < 2^47 integer fast path, 3: FP64-quotient
   // path (q < 2^kFpBits), 2: chosen per limb at run time
   const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1 || MODE == 3);
-  const bool fp = MODE == 3 || (MODE == 2 && kNttFp && q < (1ull << kFpBits));
+  const bool fp = MODE == 3;  // (unused: class-2 limbs launch the FP64 kernels)
   for (int i = tid; i < N1; i += 256) {
     const u64 wp = twp[(size_t)mod * N + i];
     sw[i] = make_ulonglong2(tw[(size_t)mod * N + i], fp ? (u64)__double_as_longlong(__ull2double_rn(wp) * 0x1p-64) : wp);
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(128, MINB) ntt2_fwd_chunks(LimbMap map, const 
     for (int b = 0; b < (1 << d); ++b) tb[(1 << d) - 1 + b] = ld_tw<HINT>(&T[(16 << d) - 1 + (j << d) + b], pol);
   __syncwarp();
   const bool fast = MODE == 2 ? (q < (1ull << 47)) : (MODE == 1 || MODE == 3);
-  const bool fp = MODE == 3 || (MODE == 2 && kNttFp && q < (1ull << kFpBits));  // ctw companions hold double(w/q)
+  const bool fp = MODE == 3;  // (unused: class-2 limbs launch the FP64 kernels)
   auto twA = [&](int d, int b) { return twa[cc][(1 << d) - 1 + b]; };
   if (fp) ct16<0, true, decltype(twA), true>(x, q, q2, twA);
   else if (fast) ct16<0, true>(x, q, q2, twA);
@@ -483,6 +483,303 @@ __global__ void __launch_bounds__(128, MINB) ntt2_inv_chunks(LimbMap map, const 
 }
 
 // ---------------------------------------------------------------------------
+// FP64 network for the moduli below 2^kFpBits (the 40/41-bit application
+// primes): residues live as signed integer-valued doubles between the load
+// and the final store, so every butterfly runs on the FP64 pipe alone.
+//   t = a*w mod q:  hi = fl(a w), lo = fma(a, w, -hi)  (a w = hi + lo exactly),
+//   qe = round(a * fl(w/q)) by the 1.5*2^52 magic constant, t = fma(-qe, q, hi) + lo.
+// For |a| < 2^51 and q < 2^44: |a fl(w/q) - a w/q| < 1/4, so t lies in
+// (-3q/4, 3q/4) and both the fma and the final add are exact (integers
+// below 2^53).  Forward CT values grow by < 3q/4 per stage (|x| < 7q after
+// a pass of 8 stages from [0,q), < 13q after the second); inverse GS values
+// double per stage (< 2^8 q after a pass) and are centred between passes.
+// The final canonical reduction returns exactly the residues of the
+// integer networks (kernels.py:232-281), so outputs are bit-identical.
+// ---------------------------------------------------------------------------
+constexpr double kMagicRound = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kTwo52 = 4503599627370496.0;
+
+__device__ __forceinline__ double u2d(u64 v) {  // 0 <= v < 2^52
+  return __longlong_as_double((long long)(v | 0x4330000000000000ull)) - kTwo52;
+}
+__device__ __forceinline__ u64 d2u(double d) {  // integer 0 <= d < 2^52
+  return (u64)__double_as_longlong(d + kTwo52) & 0x000FFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ double bits_d(u64 b) { return __longlong_as_double((long long)b); }
+__device__ __forceinline__ u64 d_bits(double d) { return (u64)__double_as_longlong(d); }
+
+__device__ __forceinline__ double fmulmod(double a, double w, double wq, double q) {
+  const double hi = a * w;
+  const double lo = fma(a, w, -hi);
+  const double qe = fma(a, wq, kMagicRound) - kMagicRound;
+  return fma(-qe, q, hi) + lo;
+}
+// |v| < 2^51 -> (-q/2 - 1, q/2 + 1)
+__device__ __forceinline__ double fcentre(double v, double q, double qinv) {
+  return fma(-(fma(v, qinv, kMagicRound) - kMagicRound), q, v);
+}
+// |v| < 2^51 -> [0, q)
+__device__ __forceinline__ double fcanon(double v, double q, double qinv) {
+  const double r = fcentre(v, q, qinv);
+  return r < 0.0 ? r + q : (r >= q ? r - q : r);
+}
+
+template <int d, class TW>
+__device__ __forceinline__ void ct_stage_f64(double (&x)[16], double q, TW& tw) {
+  constexpr int h = 8 >> d;
+#pragma unroll
+  for (int b = 0; b < (1 << d); ++b) {
+    const ulonglong2 W = tw(d, b);
+    const double w = bits_d(W.x), wq = bits_d(W.y);
+#pragma unroll
+    for (int r = 0; r < h; ++r) {
+      double& X = x[2 * h * b + r];
+      double& Y = x[2 * h * b + r + h];
+      const double t = fmulmod(Y, w, wq, q);
+      const double u = X;
+      X = u + t;
+      Y = u - t;
+    }
+  }
+}
+template <int D0, class TW>
+__device__ __forceinline__ void ct16_f64(double (&x)[16], double q, TW tw) {
+  if constexpr (D0 <= 0) ct_stage_f64<0>(x, q, tw);
+  if constexpr (D0 <= 1) ct_stage_f64<1>(x, q, tw);
+  if constexpr (D0 <= 2) ct_stage_f64<2>(x, q, tw);
+  if constexpr (D0 <= 3) ct_stage_f64<3>(x, q, tw);
+}
+template <int d, class TW>
+__device__ __forceinline__ void gs_stage_f64(double (&x)[16], double q, TW& tw) {
+  constexpr int h = 1 << d;
+#pragma unroll
+  for (int b = 0; b < (8 >> d); ++b) {
+    const ulonglong2 W = tw(d, b);
+    const double w = bits_d(W.x), wq = bits_d(W.y);
+#pragma unroll
+    for (int r = 0; r < h; ++r) {
+      double& X = x[2 * h * b + r];
+      double& Y = x[2 * h * b + r + h];
+      const double u = X, v = Y;
+      X = u + v;
+      Y = fmulmod(u - v, w, wq, q);
+    }
+  }
+}
+struct FoldF {
+  double ninvN, ninvN_q, ilast, ilast_q;
+};
+// GS stages d in [D0,4); FOLD: stage 3 is the transform's last (N^-1 folded)
+template <int D0, bool FOLD, class TW>
+__device__ __forceinline__ void gs16_f64(double (&x)[16], double q, TW tw, const FoldF& C) {
+  if constexpr (D0 <= 0) gs_stage_f64<0>(x, q, tw);
+  if constexpr (D0 <= 1) gs_stage_f64<1>(x, q, tw);
+  if constexpr (D0 <= 2) gs_stage_f64<2>(x, q, tw);
+  if constexpr (FOLD) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const double u = x[r], v = x[r + 8];
+      x[r] = fmulmod(u + v, C.ninvN, C.ninvN_q, q);
+      x[r + 8] = fmulmod(u - v, C.ilast, C.ilast_q, q);
+    }
+  } else {
+    gs_stage_f64<3>(x, q, tw);
+  }
+}
+__device__ __forceinline__ FoldF fold_f64(const ModConsts& m) {
+  return FoldF{(double)m.ninvN, (double)m.ninvN_sh * 0x1p-64, (double)m.ilast, (double)m.ilast_sh * 0x1p-64};
+}
+// twiddle staging for the column passes: (w, w/q) as double bit patterns
+__device__ __forceinline__ ulonglong2 tw_f64(u64 w, u64 wp) {
+  return make_ulonglong2(d_bits((double)w), d_bits((double)wp * 0x1p-64));
+}
+
+template <int LOGN1, bool HINT, int MINB>
+__global__ void __launch_bounds__(256, MINB) ntt2_fwd_cols_f64(LimbMap map, const ModConsts* __restrict__ mc,
+                                                           const u64* __restrict__ tw, const u64* __restrict__ twp,
+                                                           u32 logN) {
+  constexpr int N1 = 1 << LOGN1, T1 = N1 / 16, COLS = 256 / T1, NSB = LOGN1 - 4;
+  __shared__ u64 tile[N1 * COLS];
+  __shared__ ulonglong2 sw[N1];
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
+  if (limb_skipped2(map, r, z)) return;
+  const u32 N = 1u << logN, N2 = N >> LOGN1;
+  const u32 mod = map.basis.mod_of(r + map.first_limb);
+  const u64 qi = mc[mod].q;
+  const double q = (double)qi;
+  u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + blockIdx.x * COLS;
+  const int tid = threadIdx.x, c = tid % COLS, j = tid / COLS;
+  for (int i = tid; i < N1; i += 256) sw[i] = tw_f64(tw[(size_t)mod * N + i], twp[(size_t)mod * N + i]);
+  double x[16];
+  if (map.sin) {
+    const long long* s = map.sin + (size_t)z * N + blockIdx.x * COLS;
+    const u64 kr = map.smont ? mc[mod].r2 : mc[mod].one_m, ninv = mc[mod].ninv;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      long long v = s[(size_t)(j + T1 * k) * N2 + c];
+      if (map.sin_center) {  // centred lift of a residue mod sin_center (fused rescale, ckks.py:506-528)
+        const u64 t = (u64)v;
+        v = t > (map.sin_center >> 1) ? (long long)(t - map.sin_center) : (long long)t;
+      }
+      const u64 mag = v >= 0 ? (u64)v : (u64)(-(v + 1)) + 1ull;
+      const u64 red = mont_mul(mag, kr, qi, ninv);
+      x[k] = u2d(v >= 0 ? red : neg_mod(red, qi));
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = u2d(ld_last<HINT>(&a[(size_t)(j + T1 * k) * N2 + c]));
+  }
+  __syncthreads();
+  auto twA = [&](int d, int b) { return sw[(1 << d) + b]; };
+  ct16_f64<0>(x, q, twA);
+  if (NSB > 0) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[(j + T1 * k) * COLS + c] = d_bits(x[k]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = bits_d(tile[(16 * j + k) * COLS + c]);
+    auto twB = [&](int d, int b) { return sw[(1 << (d + NSB)) + (j << d) + b]; };
+    ct16_f64<4 - NSB>(x, q, twB);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[(size_t)(16 * j + k) * N2 + c] = d_bits(x[k]);  // |x| < 7q, double bits
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[(size_t)(j + T1 * k) * N2 + c] = d_bits(x[k]);
+  }
+}
+
+template <bool HINT, int MINB>
+__global__ void __launch_bounds__(128, MINB) ntt2_fwd_chunks_f64(LimbMap map, const ModConsts* __restrict__ mc,
+                                                             const ulonglong2* __restrict__ ctw, u32 logN) {
+  __shared__ u64 tile[kChunksPerCta][16 * 17];
+  __shared__ ulonglong2 twa[kChunksPerCta][16];
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
+  if (limb_skipped2(map, r, z)) return;
+  const u32 N = 1u << logN, N1 = N >> 8;
+  const u32 mod = map.basis.mod_of(r + map.first_limb);
+  const double q = (double)mc[mod].q, qinv = 1.0 / q;
+  const int tid = threadIdx.x, cc = tid >> 4, j = tid & 15;
+  const u32 g = blockIdx.x * kChunksPerCta + cc;
+  u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + (size_t)g * 256;
+  const ulonglong2* T = ctw + ((size_t)mod * N1 + g) * 256;
+  u64* tl = tile[cc];
+  const u64 pol = HINT ? keep_policy() : 0;
+  double x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = bits_d(ld_last<HINT>(&a[j + 16 * k]));
+  if (j < 15) twa[cc][j] = ld_tw<HINT>(&T[j], pol);
+  __syncwarp();
+  auto twA = [&](int d, int b) { return twa[cc][(1 << d) - 1 + b]; };
+  ct16_f64<0>(x, q, twA);
+  // second-group twiddles loaded after the first group: not live across it
+  // (fewer registers), their latency overlaps the transpose
+  ulonglong2 tb[15];
+#pragma unroll
+  for (int d = 0; d < 4; ++d)
+#pragma unroll
+    for (int b = 0; b < (1 << d); ++b) tb[(1 << d) - 1 + b] = ld_tw<HINT>(&T[(16 << d) - 1 + (j << d) + b], pol);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) tl[17 * k + j] = d_bits(x[k]);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = bits_d(tl[17 * j + k]);
+  auto twB = [&](int d, int b) { return tb[(1 << d) - 1 + b]; };
+  ct16_f64<0>(x, q, twB);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) tl[17 * j + k] = d2u(fcanon(x[k], q, qinv));  // |x| < 13q -> [0, q)
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[j + 16 * k] = tl[17 * k + j];
+}
+
+template <bool HINT, int MINB>
+__global__ void __launch_bounds__(128, MINB) ntt2_inv_chunks_f64(LimbMap map, const ModConsts* __restrict__ mc,
+                                                             const ulonglong2* __restrict__ ctw, u32 logN) {
+  __shared__ u64 tile[kChunksPerCta][16 * 17];
+  __shared__ ulonglong2 twa[kChunksPerCta][16];
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
+  if (limb_skipped2(map, r, z)) return;
+  const u32 N = 1u << logN, N1 = N >> 8;
+  const u32 mod = map.basis.mod_of(r + map.first_limb);
+  const double q = (double)mc[mod].q, qinv = 1.0 / q;
+  const FoldF C{0, 0, 0, 0};
+  const int tid = threadIdx.x, cc = tid >> 4, j = tid & 15;
+  const u32 g = blockIdx.x * kChunksPerCta + cc;
+  u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + (size_t)g * 256;
+  const ulonglong2* T = ctw + ((size_t)mod * N1 + g) * 256;
+  u64* tl = tile[cc];
+  const u64 pol = HINT ? keep_policy() : 0;
+  u64 v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = ld_last<HINT>(&a[j + 16 * k]);
+  ulonglong2 tb[15];
+#pragma unroll
+  for (int d = 0; d < 4; ++d)
+#pragma unroll
+    for (int b = 0; b < (8 >> d); ++b)
+      tb[16 - (16 >> d) + b] = ld_tw<HINT>(&T[(128 >> d) - 1 + j * (8 >> d) + b], pol);
+  if (j < 15) twa[cc][j] = ld_tw<HINT>(&T[j], pol);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) tl[17 * k + j] = v[k];
+  __syncwarp();
+  double x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = u2d(tl[17 * j + k]);  // canonical input residues
+  auto twB = [&](int d, int b) { return tb[16 - (16 >> d) + b]; };
+  gs16_f64<0, false>(x, q, twB, C);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) tl[17 * j + k] = d_bits(x[k]);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = bits_d(tl[17 * k + j]);
+  auto twA = [&](int d, int b) { return twa[cc][(8 >> d) - 1 + b]; };
+  gs16_f64<0, false>(x, q, twA, C);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[j + 16 * k] = d_bits(fcentre(x[k], q, qinv));  // |x| < 2^8 q -> centred, double bits
+}
+
+template <int LOGN1, bool HINT, int MINB>
+__global__ void __launch_bounds__(256, MINB) ntt2_inv_cols_f64(LimbMap map, const ModConsts* __restrict__ mc,
+                                                           const u64* __restrict__ itw, const u64* __restrict__ itwp,
+                                                           u32 logN) {
+  constexpr int N1 = 1 << LOGN1, T1 = N1 / 16, COLS = 256 / T1, NSA = LOGN1 - 4;
+  __shared__ u64 tile[N1 * COLS];
+  __shared__ ulonglong2 sw[N1];
+  const u32 r = blockIdx.y + map.r0, z = blockIdx.z + map.z0;
+  if (limb_skipped2(map, r, z)) return;
+  const u32 N = 1u << logN, N2 = N >> LOGN1;
+  const u32 mod = map.basis.mod_of(r + map.first_limb);
+  const double q = (double)mc[mod].q, qinv = 1.0 / q;
+  const FoldF C = fold_f64(mc[mod]);
+  u64* a = map.base + (size_t)z * map.poly_stride + (size_t)r * N + blockIdx.x * COLS;
+  const int tid = threadIdx.x, c = tid % COLS, j = tid / COLS;
+  for (int i = tid; i < N1; i += 256) sw[i] = tw_f64(itw[(size_t)mod * N + i], itwp[(size_t)mod * N + i]);
+  double x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = bits_d(ld_last<HINT>(&a[(size_t)(16 * j + k) * N2 + c]));
+  __syncthreads();
+  auto twB = [&](int d, int b) { return sw[(N1 >> (d + 1)) + j * (8 >> d) + b]; };
+  auto twA = [&](int d, int b) { return sw[(8 >> d) + b]; };
+  if (NSA == 0) {
+    gs16_f64<0, true>(x, q, twB, C);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[(size_t)(16 * j + k) * N2 + c] = d2u(fcanon(x[k], q, qinv));
+  } else {
+    gs16_f64<0, false>(x, q, twB, C);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[(16 * j + k) * COLS + c] = d_bits(x[k]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = bits_d(tile[(j + T1 * k) * COLS + c]);
+    gs16_f64<4 - NSA, true>(x, q, twA, C);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[(size_t)(j + T1 * k) * N2 + c] = d2u(fcanon(x[k], q, qinv));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Integer-pipe ceiling of the NTT: the same radix-16 register network
 // (ct16, 32 butterflies per call, approximate-Shoup products) iterated on
 // register-resident data with register twiddles -- no memory traffic, no
@@ -545,6 +842,56 @@ __global__ void __launch_bounds__(256) k_bfly_peak_fp(u64* __restrict__ out, con
   out[t] = acc;
 }
 
+// Pure FP64 network (probe): residues held as signed doubles, exact
+// products by the FMA two-product (a*w = hi + lo), quotient by the magic
+// round-to-integer constant, no integer ops in the butterfly.
+__device__ __forceinline__ double f64_mulmod(double a, double w, double wq, double q) {
+  const double C = 6755399441055744.0;  // 1.5 * 2^52
+  const double hi = a * w;
+  const double lo = fma(a, w, -hi);
+  const double qe = fma(a, wq, C) - C;
+  return fma(-qe, q, hi) + lo;
+}
+__global__ void __launch_bounds__(256) k_bfly_peak_f64(u64* __restrict__ out, const ulonglong2* __restrict__ tws,
+                                                       u64 qi, int iters) {
+  const double q = (double)qi;
+  double tw[15], wq[15];
+#pragma unroll
+  for (int i = 0; i < 15; ++i) {
+    tw[i] = (double)tws[i].x;
+    wq[i] = (double)tws[i].x / q;
+  }
+  double x[16];
+  const u64 t = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = (double)((t * 16 + k) % qi);
+  const double qinv = 1.0 / q, C = 6755399441055744.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const int h = 8 >> d;
+#pragma unroll
+      for (int b = 0; b < (1 << d); ++b)
+#pragma unroll
+        for (int r = 0; r < h; ++r) {
+          double& X = x[2 * h * b + r];
+          double& Y = x[2 * h * b + r + h];
+          const double tt = f64_mulmod(Y, tw[(1 << d) - 1 + b], wq[(1 << d) - 1 + b], q);
+          const double xx = X;
+          X = xx + tt;
+          Y = xx - tt;
+        }
+    }
+    // centre every value once per 4 stages (the real network reduces per pass)
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] -= (fma(x[k], qinv, C) - C) * q;
+  }
+  u64 acc = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc ^= (u64)(long long)x[k];
+  out[t] = acc;
+}
+
 // butterflies per second of k_bfly_peak (fast: q < 2^47 unreduced network)
 int ntt_butterfly_peak(int fast, double* bfly_per_s) {
   int dev = 0, sms = 0;
@@ -570,7 +917,8 @@ int ntt_butterfly_peak(int fast, double* bfly_per_s) {
   float ms = 0.f;
   if (!err) {
     auto go = [&]() {
-      if (fast == 3) k_bfly_peak_fp<true><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
+      if (fast == 4) k_bfly_peak_f64<<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
+      else if (fast == 3) k_bfly_peak_fp<true><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
       else if (fast == 2) k_bfly_peak_fp<false><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
       else if (fast) k_bfly_peak<true><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
       else k_bfly_peak<false><<<blocks, threads, 0, st>>>(d_out, d_tw, q, iters);
@@ -614,9 +962,49 @@ static void launch_cols_t(bool inv, dim3 g, const LimbMap& map, const NttTables&
   else ntt2_fwd_cols<L, H, OCC == 1 ? 3 : 1, F><<<g, 256, 0, st>>>(map, T.mc, T.tw, T.twp, T.logN);
 }
 
+template <int L, bool H>
+static void launch_cols_f64(bool inv, dim3 g, const LimbMap& map, const NttTables& T, cudaStream_t st) {
+  if (inv) ntt2_inv_cols_f64<L, H, 1><<<g, 256, 0, st>>>(map, T.mc, T.itw, T.itwp, T.logN);
+  else ntt2_fwd_cols_f64<L, H, 1><<<g, 256, 0, st>>>(map, T.mc, T.tw, T.twp, T.logN);
+}
+
+// FP64-network pass pair (class-2 moduli, both directions)
+template <bool H>
+static cudaError_t launch_pair_f64(const NttTables& T, const LimbMap& map, u32 ny, u32 nz, bool inverse,
+                                   cudaStream_t st) {
+  const u32 logN = T.logN, logN1 = logN - 8, N1 = 1u << logN1;
+  const u32 cols = 256 / (N1 / 16);
+  dim3 gc(256 / cols, ny, nz);
+  dim3 gk(N1 / kChunksPerCta, ny, nz);
+  auto cols_launch = [&](bool inv) -> bool {
+    switch (logN1) {
+      case 4: launch_cols_f64<4, H>(inv, gc, map, T, st); return true;
+      case 5: launch_cols_f64<5, H>(inv, gc, map, T, st); return true;
+      case 6: launch_cols_f64<6, H>(inv, gc, map, T, st); return true;
+      case 7: launch_cols_f64<7, H>(inv, gc, map, T, st); return true;
+      case 8: launch_cols_f64<8, H>(inv, gc, map, T, st); return true;
+      default: return false;
+    }
+  };
+  const int mb = g_ntt_tuning.f64_minb;
+  if (!inverse) {
+    if (!cols_launch(false)) return cudaErrorInvalidValue;
+    if (mb == 5) ntt2_fwd_chunks_f64<H, 5><<<gk, 128, 0, st>>>(map, T.mc, T.ctw, logN);
+    else if (mb == 6) ntt2_fwd_chunks_f64<H, 6><<<gk, 128, 0, st>>>(map, T.mc, T.ctw, logN);
+    else ntt2_fwd_chunks_f64<H, 1><<<gk, 128, 0, st>>>(map, T.mc, T.ctw, logN);
+  } else {
+    if (mb == 5) ntt2_inv_chunks_f64<H, 5><<<gk, 128, 0, st>>>(map, T.mc, T.ictw, logN);
+    else if (mb == 6) ntt2_inv_chunks_f64<H, 6><<<gk, 128, 0, st>>>(map, T.mc, T.ictw, logN);
+    else ntt2_inv_chunks_f64<H, 1><<<gk, 128, 0, st>>>(map, T.mc, T.ictw, logN);
+    if (!cols_launch(true)) return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 template <bool H, int OCC, int F>
 static cudaError_t launch_pair(const NttTables& T, const LimbMap& map, u32 ny, u32 nz, bool inverse,
                                cudaStream_t st) {
+  if constexpr (F == 3) return launch_pair_f64<H>(T, map, ny, nz, inverse, st);
   const u32 logN = T.logN, logN1 = logN - 8, N1 = 1u << logN1;
   const u32 cols = 256 / (N1 / 16);
   dim3 gc(256 / cols, ny, nz);
@@ -653,7 +1041,10 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
   // split 1: per-class launches both directions, 2: forward only (the
   // forward variants differ -- FP64 vs integer quotient -- so per-class
   // kernels are smaller; the inverse keeps one run-time-dispatch launch)
-  const bool split = g_ntt_tuning.split == 1 || (g_ntt_tuning.split == 2 && !inverse);
+  // FP64-network moduli (class 2) always launch their own kernels: their
+  // chunk twiddles are stored as doubles
+  const bool split = g_ntt_tuning.split == 1 || (g_ntt_tuning.split == 2 && !inverse) ||
+                     (kNttFp && T.small != nullptr);
   auto one = [&](const LimbMap& m, u32 ny, u32 nz, int mode) -> cudaError_t {
     if (mode == 0) return g_ntt_tuning.occupancy == 2 ? launch_pair<true, 2, 0>(T, m, ny, nz, inverse, st)
                           : occ ? launch_pair<true, 1, 0>(T, m, ny, nz, inverse, st)
@@ -668,14 +1059,23 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
   auto pair = [&](const LimbMap& m, u32 ny, u32 nz) -> cudaError_t {
     if (!split || !T.small) return one(m, ny, nz, 2);
     u32 r = 0;
+    // launch class of a limb: the FP64 network (class 2) always alone; the
+    // integer classes merge into one run-time-dispatch inverse unless split == 1
+    auto cls = [&](u32 rr) -> int {
+      const int f = T.small[m.basis.mod_of(m.r0 + rr + m.first_limb)];
+      if (f == 2 && kNttFp) return 2;
+      return inverse && g_ntt_tuning.split != 1 ? -1 : f;
+    };
     while (r < ny) {
-      const unsigned char f = T.small[m.basis.mod_of(m.r0 + r + m.first_limb)];
+      const int f = cls(r);
       u32 e = r + 1;
-      while (e < ny && T.small[m.basis.mod_of(m.r0 + e + m.first_limb)] == f) ++e;
+      while (e < ny && cls(e) == f) ++e;
       LimbMap mm = m;
       mm.r0 = m.r0 + r;
-      // class 2 (FP64-quotient moduli): MODE 3 forward, integer fast inverse
-      cudaError_t err = one(mm, e - r, nz, f == 2 ? (kNttFp ? 3 : 1) : f);
+      // class 2: the FP64 network both ways; other classes keep one
+      // run-time-dispatch inverse launch unless split == 1
+      const int mode = f == 2 ? 3 : f < 0 ? 2 : f;
+      cudaError_t err = one(mm, e - r, nz, mode);
       if (r > 0) g_ntt_extra_launches += 2;  // launch accounting counts one pair per call
       if (err) return err;
       r = e;

@@ -273,20 +273,27 @@ def test_lazy_mac_worst_case_residues(small):
 
 # launch-shape knobs of the TMA-staged plane MAC and key-switch inner product
 # (threads per CTA, ring depth, register cap) and the values the engine ships with
-_KNOB_DEFAULTS = {"mac_tpb": 128, "tma_stages": 3, "mac_minb": 1, "ks_tpb": 128, "ks_stages": 3, "ks_tma_min": 2}
+_KNOB_DEFAULTS = {"mac_tma": 3, "mac3_stages": 4, "mac3_tpb": 128, "mac_tpb": 128, "tma_stages": 3, "mac_minb": 1,
+                  "ks_tpb": 128, "ks_stages": 3, "ks_tma_min": 2}
 _KNOB_VARIANTS = [
-    {"mac_tpb": 256, "tma_stages": 4, "ks_tpb": 256},
-    {"mac_tpb": 256, "tma_stages": 6, "ks_tpb": 256},
-    {"mac_tpb": 256, "tma_stages": 4, "mac_minb": 4},
-    {"mac_tpb": 128, "tma_stages": 4},
-    {"mac_tpb": 128, "tma_stages": 3, "mac_minb": 5},
-    {"mac_tpb": 128, "tma_stages": 2},
+    {"mac_tma": 1},
+    {"mac3_stages": 2},
+    {"mac3_stages": 3},
+    {"mac3_stages": 6},
+    {"mac3_tpb": 256},
+    {"mac3_tpb": 256, "mac3_stages": 4},
+    {"mac_tma": 1, "mac_tpb": 256, "tma_stages": 4, "ks_tpb": 256},
+    {"mac_tma": 1, "mac_tpb": 256, "tma_stages": 6, "ks_tpb": 256},
+    {"mac_tma": 1, "mac_tpb": 256, "tma_stages": 4, "mac_minb": 4},
+    {"mac_tma": 1, "mac_tpb": 128, "tma_stages": 4},
+    {"mac_tma": 1, "mac_tpb": 128, "tma_stages": 3, "mac_minb": 5},
+    {"mac_tma": 1, "mac_tpb": 128, "tma_stages": 2},
     {"ks_tpb": 128, "ks_stages": 4},
 ]
 
 
 def test_launch_shape_variants_bit_identical(small, cts):
-    """Every launch shape of k_mac_multi_tma(2) / k_ks_inner_tma(2) gives the
+    """Every launch shape of k_mac_multi_tma(2/3) / k_ks_inner_tma(2) gives the
     residues of the shipped shape: plane MACs over mixed packed / unpacked /
     absent masks, and batched (>= 3 entries: TMA path) hoisted rotations."""
     import torch
