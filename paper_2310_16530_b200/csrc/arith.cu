@@ -1742,6 +1742,149 @@ __global__ void __launch_bounds__(TPB) k_ks_inner_tma2(u64* __restrict__ acc, co
   }
 }
 
+// k_ks_inner_tma3: k_ks_inner_tma2 with a dedicated producer warp and a
+// full / empty mbarrier ring (consumer warps run up to ST digits apart, no
+// CTA-wide barrier per digit); FAST rows (Q limbs with q < 2^42) accumulate
+// with the 96-bit carry chains of k_mac_multi_tma3.  Rows r0 .. r0+gridDim.y-1.
+template <int ST, int TPB, bool FAST>
+__global__ void __launch_bounds__(TPB + 32) k_ks_inner_tma3(u64* __restrict__ acc, const u64* __restrict__ x_eval,
+                                                            const u64* __restrict__ raised, const u64* __restrict__ key_b,
+                                                            const u64* __restrict__ key_a, Basis basis, u32 alpha,
+                                                            u32 ndig, u32 logN, u64 g, const ModConsts* __restrict__ mc,
+                                                            u32 nb, size_t x_bst, const u64* __restrict__ c0,
+                                                            size_t c0_bst, const u64* __restrict__ pR, u32 key_lq,
+                                                            u32 r0) {
+  constexpr int NW = TPB / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  KsStage* S = reinterpret_cast<KsStage*>(smem_raw);
+  __shared__ __align__(8) u64 full[ST];
+  __shared__ __align__(8) u64 empty[ST];
+  const u32 N = 1u << logN, r = blockIdx.y + r0, tile = blockIdx.x, tid = threadIdx.x;
+  const u32 b0 = blockIdx.z * kKsEntries;
+  const u32 ne = nb - b0 < (u32)kKsEntries ? nb - b0 : (u32)kKsEntries;
+  const u32 n_ext = basis.nlimbs();
+  const u32 mod = basis.mod_of(r);
+  const u64 q = mc[mod].q, ninv = mc[mod].ninv, one_sh = mc[mod].one_sh;
+  const u32 klq = key_lq ? key_lq : basis.Lq;
+  const size_t key_dst = (size_t)(klq + basis.np) * N;
+  const u32 kmod = mod < basis.Lq ? mod : klq + (mod - basis.Lq);
+  const u32 own = r < basis.nq ? r / alpha : 0xffffffffu;
+  constexpr int CPT = kMacTile / TPB;
+  const u32 k = tile * kMacTile + (tid < (u32)TPB ? tid : 0);
+  const u32 src = g == 1 ? k : galois_src(k, g, logN);
+  const size_t t_src = (size_t)(src & ~(u32)(kMacTile - 1));  // same block for the whole CTA
+  const size_t r_bst = (size_t)ndig * n_ext * N;
+  const bool ext = c0 != nullptr && r < basis.nq;
+  const u32 nst = ndig + (ext ? 1u : 0u);
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= (u32)TPB) {  // producer warp
+    if (tid == (u32)TPB) {
+      for (u32 j = 0; j < nst; ++j) {
+        const u32 slot = j % ST;
+        if (j >= (u32)ST) mbar_wait(&empty[slot], (j / ST - 1) & 1u);
+        KsStage& T = S[slot];
+        u64* bar = &full[slot];
+        if (j < ndig) {
+          mbar_expect_tx(bar, (2 + ne) * kMacTile * 8);
+          const size_t kofs = (size_t)j * key_dst + (size_t)kmod * N + (size_t)tile * kMacTile;
+          bulk_g2s(T.kb, key_b + kofs, kMacTile * 8, bar);
+          bulk_g2s(T.ka, key_a + kofs, kMacTile * 8, bar);
+          for (u32 e = 0; e < ne; ++e) {
+            const u64* sp = j == own ? x_eval + (size_t)(b0 + e) * x_bst + (size_t)r * N
+                                     : raised + (size_t)(b0 + e) * r_bst + ((size_t)j * n_ext + r) * N;
+            bulk_g2s(T.x[e], sp + t_src, kMacTile * 8, bar);
+          }
+        } else {  // extended-basis term: c0 tiles
+          mbar_expect_tx(bar, ne * kMacTile * 8);
+          for (u32 e = 0; e < ne; ++e)
+            bulk_g2s(T.x[e], c0 + (size_t)(b0 + e) * c0_bst + (size_t)r * N + t_src, kMacTile * 8, bar);
+        }
+      }
+    }
+    return;
+  }
+  u32 s_in[CPT];  // positions inside the source tile
+  s_in[0] = src & (kMacTile - 1);
+#pragma unroll
+  for (int c = 1; c < CPT; ++c) s_in[c] = (g == 1 ? k + c * TPB : galois_src(k + c * TPB, g, logN)) & (kMacTile - 1);
+  // FAST: (lh, mid) 96-bit sums; generic: lazy 128-bit (l, h)
+  u64 bL[kKsEntries][CPT], bH[kKsEntries][CPT], aL[kKsEntries][CPT], aH[kKsEntries][CPT];
+#pragma unroll
+  for (int e = 0; e < kKsEntries; ++e)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) bL[e][c] = bH[e][c] = aL[e][c] = aH[e][c] = 0;
+  for (u32 j = 0; j < nst; ++j) {
+    const u32 slot = j % ST;
+    mbar_wait(&full[slot], (j / ST) & 1u);
+    const KsStage& T = S[slot];
+    if (j < ndig) {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const u64 kb = T.kb[tid + c * TPB], ka = T.ka[tid + c * TPB];
+#pragma unroll
+        for (int e = 0; e < kKsEntries; ++e) {
+          if ((u32)e >= ne) break;
+          const u64 x = T.x[e][s_in[c]];
+          if constexpr (FAST) {
+            mac96(bL[e][c], bH[e][c], (u32)x, (u32)(x >> 32), (u32)kb, (u32)(kb >> 32));
+            mac96(aL[e][c], aH[e][c], (u32)x, (u32)(x >> 32), (u32)ka, (u32)(ka >> 32));
+          } else {
+            mac128_lazy(bH[e][c], bL[e][c], x, kb);
+            mac128_lazy(aH[e][c], aL[e][c], x, ka);
+          }
+        }
+      }
+    } else {
+      const u64 w = pR[r];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int e = 0; e < kKsEntries; ++e) {
+          if ((u32)e >= ne) break;
+          const u64 x = T.x[e][s_in[c]];
+          if constexpr (FAST) mac96(bL[e][c], bH[e][c], (u32)x, (u32)(x >> 32), (u32)w, (u32)(w >> 32));
+          else mac128_lazy(bH[e][c], bL[e][c], x, w);
+        }
+    }
+    if constexpr (!FAST) {
+      if ((j + 1) % kLazyTerms == 0 || j + 1 == nst) {
+#pragma unroll
+        for (int e = 0; e < kKsEntries; ++e)
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            bH[e][c] = fold_hi(bH[e][c], q, one_sh);
+            aH[e][c] = fold_hi(aH[e][c], q, one_sh);
+          }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
+  }
+#pragma unroll
+  for (int e = 0; e < kKsEntries; ++e) {
+    if ((u32)e >= ne) break;
+    u64* A = acc + (size_t)(b0 + e) * 2 * n_ext * N;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const u32 kc = k + c * TPB;
+      A[(size_t)r * N + kc] = FAST ? redc96(bL[e][c], bH[e][c], q, ninv) : redc128(bH[e][c], bL[e][c], q, ninv);
+      A[((size_t)n_ext + r) * N + kc] = FAST ? redc96(aL[e][c], aH[e][c], q, ninv) : redc128(aH[e][c], aL[e][c], q, ninv);
+    }
+  }
+}
+
+// 0: off -- measured slower than k_ks_inner_tma2 (tools/ks_bench.py: 3.7 vs 4.3 TB/s
+// at level 14 nb 4, 4.0 vs 4.6 at level 30 nb 8; three row launches, 3 CTAs/SM)
+int g_ks_tma3 = 0;     // 1: k_ks_inner_tma3 (warp-specialised) for TMA-routed batches
+int g_ks3_stages = 3;  // its ring depth (2, 3, 4)
+
 int g_mac_tma = 3;    // 1: bulk-copy (TMA) staged k_mac_multi_tma(2), 3: warp-specialised k_mac_multi_tma3
 int g_mac3_stages = 4;  // k_mac_multi_tma3 ring depth (2, 3, 4, 6); tools/mac_probe.py: 4 = 3 < 2, 6
 int g_mac3_tpb = 128;   // k_mac_multi_tma3 threads per CTA (128 or 256)
@@ -1965,9 +2108,39 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
                             cudaStream_t st, u32 nb, size_t x_bst, const u64* c0, size_t c0_bst, const u64* pR,
-                            u32 key_lq) {
+                            u32 key_lq, u32 fast_from) {
   // TMA staging pays once a key tile feeds >= 3 entries; small batches keep
   // the register-pipelined kernel (measured: tools/ks_bench.py)
+  if (g_ks_tma && g_ks_tma3 && nb >= (u32)g_ks_tma_min && (1u << logN) % kMacTile == 0) {
+    // rows [0, ff) and [nq, n_ext): generic; [ff, nq): 96-bit carry chains
+    const u32 nbb = nb ? nb : 1, nq = basis.nq, nl = basis.nlimbs();
+    const u32 ff = fast_from < 1 ? 1 : (fast_from > nq ? nq : fast_from);
+    static bool attr3[2][5] = {};
+    const int stages = g_ks3_stages >= 2 && g_ks3_stages <= 4 ? g_ks3_stages : 3;
+    auto go3 = [&](auto kern, int fast, u32 r0, u32 rows) -> cudaError_t {
+      if (rows == 0) return cudaSuccess;
+      const size_t sm = sizeof(KsStage) * stages;
+      if (!attr3[fast][stages]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e) return e;
+        attr3[fast][stages] = true;
+      }
+      dim3 grid((1u << logN) / kMacTile, rows, (nbb + kKsEntries - 1) / kKsEntries);
+      kern<<<grid, 128 + 32, sm, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nbb, x_bst,
+                                      c0, c0_bst, pR, key_lq, r0);
+      return cudaGetLastError();
+    };
+    cudaError_t e;
+#define KS3(ST)                                                                          \
+    if (stages == ST) {                                                                  \
+      e = go3(k_ks_inner_tma3<ST, 128, false>, 0, 0, ff);                                \
+      if (!e) e = go3(k_ks_inner_tma3<ST, 128, true>, 1, ff, nq - ff);                   \
+      if (!e) e = go3(k_ks_inner_tma3<ST, 128, false>, 0, nq, nl - nq);                  \
+      return e;                                                                          \
+    }
+    KS3(2) KS3(3) KS3(4)
+#undef KS3
+  }
   if (g_ks_tma && nb >= (u32)g_ks_tma_min && (1u << logN) % kMacTile == 0) {
     const u32 nbb = nb ? nb : 1;
     dim3 grid((1u << logN) / kMacTile, basis.nlimbs(), (nbb + kKsEntries - 1) / kKsEntries);

@@ -35,6 +35,8 @@ extern int g_mac_batch;
 extern int g_mac_lanes;
 extern int g_mac_async;
 extern int g_mac_tma;
+extern int g_ks_tma3;
+extern int g_ks3_stages;
 extern int g_mac3_stages;
 extern int g_mac3_tpb;
 extern int g_mac_tpb;
@@ -47,7 +49,8 @@ extern int g_tma_stages;
 cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, const u64* key_b, const u64* key_a,
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
                             cudaStream_t st, u32 nb = 1, size_t x_bst = 0, const u64* c0 = nullptr,
-                            size_t c0_bst = 0, const u64* pR = nullptr, u32 key_lq = 0);
+                            size_t c0_bst = 0, const u64* pR = nullptr, u32 key_lq = 0,
+                            u32 fast_from = 0xffffffffu);  // Q rows >= fast_from: q < 2^42 (96-bit MACs)
 // acc [nb][2][n_ext], lift [nb][2][nq]; outputs / addends of entry b at +b*out_bst / +b*add_bst
 cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,
                                    const u64* add1, u64 g_add, u32 nq, u32 n_ext, u32 logN, const u64* pinv,

@@ -795,6 +795,14 @@ size_t hcnn_ks_workspace_bytes_rot(const hcnn_ctx* c, uint32_t level, uint32_t n
   return hcnn_ks_workspace_bytes_batch(c, level, nb) + extra * c->n * 8;
 }
 
+// first Q row from which every modulus of the first nq is below 2^42: the
+// key-switch inner product runs those rows with 96-bit carry-chain MACs
+static u32 ks_fast_from(const hcnn_ctx* c, u32 nq) {
+  u32 ff = nq;
+  while (ff > 1 && c->mods[ff - 1] < (1ull << 42)) --ff;
+  return ff;
+}
+
 // ModUp of nb polys (entry b at x_eval + b*x_bst): iNTT a copy, convert
 // every digit to Q_l||P, NTT the new limbs -- one launch per step for the batch
 static int ks_modup(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, cudaStream_t st, u32 nb = 1,
@@ -870,7 +878,7 @@ static int ks_finish(hcnn_ctx* c, u32 level, const u64* x_eval, const KsWs& w, u
   ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * nq) * N);
   PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, st,
      launch_ks_inner(w.acc, x_eval, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, g, c->d_mc, st,
-                     nb, x_bst, nullptr, 0, nullptr, key_lq));
+                     nb, x_bst, nullptr, 0, nullptr, key_lq, ks_fast_from(c, nq)));
   return ks_moddown(c, level, w.acc, w.lift, out0, out1, add0, add1, g_add, st, nb, out_bst, add_bst);
 }
 
@@ -963,7 +971,7 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
       ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * nq) * N);
       PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
          launch_ks_inner(w.acc + j * a_step, c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd,
-                         c->logN, g, c->d_mc, STREAM(s), nb, ct, nullptr, 0, nullptr, key_lqs ? key_lqs[i] : 0));
+                         c->logN, g, c->d_mc, STREAM(s), nb, ct, nullptr, 0, nullptr, key_lqs ? key_lqs[i] : 0, ks_fast_from(c, nq)));
     }
     const u32 np = 2 * nb * nr;
     LimbMap m{};
@@ -1013,7 +1021,7 @@ int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* c, uint64_t* const* outs, const uint
     ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * n_ext + nb * nq) * N);
     PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext + nb * nq) * N, 1, STREAM(s),
        launch_ks_inner(outs[i], c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd, c->logN, g,
-                       c->d_mc, STREAM(s), nb, ct, cts, ct, c->d_pR, key_lqs ? key_lqs[i] : 0));
+                       c->d_mc, STREAM(s), nb, ct, cts, ct, c->d_pR, key_lqs ? key_lqs[i] : 0, ks_fast_from(c, nq)));
   }
   return HCNN_OK;
 }
@@ -1091,7 +1099,7 @@ int hcnn_hmult_rescale_batch(hcnn_ctx* c, uint64_t* out, const uint64_t* a, cons
   ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * nq) * N);
   PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
      launch_ks_inner(w.acc, w.lift, w.raised, kb, ka, c->basis(nq, c->K), c->alpha, nd, c->logN, 1, c->d_mc,
-                     STREAM(s), nb, ct, nullptr, 0, nullptr, 0));
+                     STREAM(s), nb, ct, nullptr, 0, nullptr, 0, ks_fast_from(c, nq)));
   PK("add_pmul", 8.0 * 2 * nb * 3 * nq * N, 1, STREAM(s),
      launch_add_pmul(w.acc, d01, nb, nq, n_ext, c->logN, c->d_pR, c->d_mc, STREAM(s)));
   return moddown_rescale(c, level, w.acc, w.lift, out, nb, STREAM(s));
@@ -1283,6 +1291,8 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "mac_lanes") g_mac_lanes = (int)value;
   else if (k == "mac_async") g_mac_async = (int)value;
   else if (k == "mac_tma") g_mac_tma = (int)value;
+  else if (k == "ks_tma3") g_ks_tma3 = (int)value;
+  else if (k == "ks3_stages") g_ks3_stages = (int)value;
   else if (k == "mac3_stages") g_mac3_stages = (int)value;
   else if (k == "mac3_tpb") g_mac3_tpb = (int)value;
   else if (k == "tma_stages") g_tma_stages = (int)value;
