@@ -183,8 +183,9 @@ def int_roofline(roof: dict, prof: dict, limbs: dict, n: int) -> dict:
     ms = sum(v["ms"] for k, v in prof.items() if _kernel_family(k) == fam)
     if fast + full == 0 or ms <= 0:
         return roof
-    # fast limbs (q < 2^44 here) run the FP64-quotient network: its probe is their ceiling
-    pf, ps = _native.ntt_butterfly_peak(2), _native.ntt_butterfly_peak(0)
+    # class-2 limbs (q < 2^41: the 40-bit primes) run the pure FP64 network:
+    # its register-only probe is their ceiling; full-width limbs the integer one
+    pf, ps = _native.ntt_butterfly_peak(4), _native.ntt_butterfly_peak(0)
     per_limb = n // 2 * (n.bit_length() - 1)
     ideal_s = per_limb * (fast / pf + full / ps)
     bfly = per_limb * (fast + full)
@@ -202,9 +203,10 @@ def int_roofline(roof: dict, prof: dict, limbs: dict, n: int) -> dict:
                                  "(one launch = the cols + chunks pass pair)")
     out = {"kernel": fam, "bound": "int", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
            "unit": "Gbutterfly/s", "frac": round(ideal_s / (ms / 1e3), 4), "traffic": traffic,
-           "peak_source": (f"measured on this GPU: radix-16 register network without memory traffic "
-                           f"(hcnn_ntt_butterfly_peak) {pf/1e9:.1f} Gbfly/s for the FP64-quotient network of "
-                           f"q<2^44 limbs, {ps/1e9:.1f} for full-width limbs, weighted by this image's {fast} + {full} limbs"),
+           "peak_source": (f"measured on this GPU: the kernels' radix-16 register networks without memory traffic "
+                           f"(hcnn_ntt_butterfly_peak) {pf/1e9:.1f} Gbfly/s for the FP64 network of the "
+                           f"q<2^41 limbs, {ps/1e9:.1f} for the integer network of full-width limbs, weighted by "
+                           f"this run's {fast} + {full} limbs"),
            "limbs": {"fast": fast, "full": full}, "share_of_device_time": roof["share_of_device_time"],
            "hbm": hbm}
     return out
@@ -230,8 +232,8 @@ def keyswitch_roofline(prof: dict, ksc: dict, n: int) -> dict | None:
     hybrid key switch cannot avoid (ModUp iNTT + digit NTTs, ModDown iNTT of
     the specials + NTT of the lift); ideal = max(bytes / HBM peak,
     butterflies / butterfly peak), frac = ideal / measured device time of
-    every kernel of the chain.  The butterfly peak is the faster
-    (FP64-quotient) network's, so the integer bound is not flattered."""
+    every kernel of the chain.  The butterfly peak is the faster (FP64)
+    network's for every limb, so the integer bound is not flattered."""
     from paper_2310_16530_b200 import _native
     ms = sum(prof[k]["ms"] for k in KS_LABELS if k in prof)
     if ms <= 0 or not ksc.get("keyswitches"):
@@ -241,7 +243,7 @@ def keyswitch_roofline(prof: dict, ksc: dict, n: int) -> dict | None:
     per_limb = n // 2 * (n.bit_length() - 1)
     limbs = ksc["fwd_limbs"] + ksc["inv_limbs"]
     bfly = per_limb * limbs
-    pf = _native.ntt_butterfly_peak(2)
+    pf = _native.ntt_butterfly_peak(4)  # the FP64 network: the faster ceiling of the two
     t = ms / 1e3
     t_hbm = ksc["min_bytes"] / (peak_gbs * 1e9)
     t_int = bfly / pf
@@ -254,7 +256,7 @@ def keyswitch_roofline(prof: dict, ksc: dict, n: int) -> dict | None:
                     "frac": round(t_hbm / t, 4), "min_bytes": ksc["min_bytes"]},
             "int": {"achieved": round(bfly / t / 1e9, 1), "peak": round(pf / 1e9, 1), "unit": "Gbutterfly/s",
                     "frac": round(t_int / t, 4), "limb_ntts": limbs,
-                    "peak_source": "hcnn_ntt_butterfly_peak (FP64-quotient radix-16 network, measured here)"}}
+                    "peak_source": "hcnn_ntt_butterfly_peak(4): the FP64 radix-16 network, register-only, measured here"}}
 
 
 # ---------------------------------------------------------------------------

@@ -245,10 +245,12 @@ int hcnn_scalar_mac(hcnn_ctx* ctx, uint64_t* out, const uint64_t* const* srcs, c
 /* ---- instrumentation ------------------------------------------------------ */
 /* count of engine kernels launched since load (all contexts) */
 unsigned long long hcnn_kernel_launches(void);
-/* Integer-pipe ceiling of the NTT: butterflies/s of the radix-16 register
- * network run on register-resident data (no memory traffic) on `device`;
- * fast = 1 times the unreduced q < 2^47 network.  No reference counterpart
- * (roofline denominator for bench.py). */
+/* Compute ceiling of the NTT: butterflies/s of a radix-16 register network
+ * run on register-resident data (no memory traffic) on `device`.  fast:
+ * 0 full-width integer network, 1 unreduced q < 2^47 integer network,
+ * 2 FP64-quotient network, 3 its magic-constant variant, 4 the pure FP64
+ * network the q < 2^41 limbs run.  No reference counterpart (roofline
+ * denominator for bench.py). */
 int hcnn_ntt_butterfly_peak(int device, int fast, double* bfly_per_s);
 /* limbs transformed since the last reset, by class:
  * [forward q<2^47, forward full, inverse q<2^47, inverse full] */

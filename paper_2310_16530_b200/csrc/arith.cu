@@ -3,11 +3,32 @@
 // All of these are HBM-bound streaming kernels over [poly][limb][N] u64
 // residues.  Each maps one CTA row to one (poly, limb) pair so the modulus
 // constants are warp-uniform, and moves 16 B per thread per access.
+#include <mutex>
+#include <set>
+#include <tuple>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "arith.cuh"
 
 namespace hcnn {
+
+// Dynamic shared memory above 48 KB needs a per-kernel opt-in, and the
+// attribute is per device: cache (kernel, device, bytes) under a mutex so
+// contexts on several devices / threads each get it.
+static cudaError_t ensure_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, size_t>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(fn, dev, bytes);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (!e) done.insert(key);
+  return e;
+}
 
 static inline dim3 row_grid(u32 work_per_row, u32 rows, u32 threads) {
   u32 x = (work_per_row + threads - 1) / threads;
@@ -1900,16 +1921,13 @@ cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN
   if (ng < 1 || ng > kMultiG) return cudaErrorInvalidValue;
   if (g_mac_tma == 3 && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
     // rows [0, fast_from): generic 128-bit MACs; [fast_from, nq): 96-bit carry chains
-    static bool attr3[2][9][2] = {};
     const int stages = g_mac3_stages, tpb = g_mac3_tpb;
     auto go3 = [&](auto kern, int fast, u32 r0, u32 rows, int kst, int ktpb) -> cudaError_t {
+      (void)fast;
       if (rows == 0) return cudaSuccess;
       const size_t sm = sizeof(MacStage) * kst;
-      if (!attr3[fast][kst][ktpb == 256]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e) return e;
-        attr3[fast][kst][ktpb == 256] = true;
-      }
+      cudaError_t e = ensure_smem((const void*)kern, sm);
+      if (e) return e;
       kern<<<dim3((1u << logN) / kMacTile, rows, 1), ktpb + 32, sm, st>>>(M, ng, nt, nq, logN, r0, accumulate, mc);
       return cudaGetLastError();
     };
@@ -1923,14 +1941,10 @@ cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN
   }
   if (g_mac_tma && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
     dim3 g((1u << logN) / kMacTile, nq, 1);
-    static bool attr_done[2][9][8] = {};
     auto go = [&](auto kern, int stages, int tpb) -> cudaError_t {
       const size_t sm = sizeof(MacStage) * stages;
-      if (!attr_done[tpb == 128][stages][g_mac_minb & 7]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e) return e;
-        attr_done[tpb == 128][stages][g_mac_minb & 7] = true;
-      }
+      cudaError_t e = ensure_smem((const void*)kern, sm);
+      if (e) return e;
       kern<<<g, tpb, sm, st>>>(M, ng, nt, nq, logN, accumulate, mc);
       return cudaGetLastError();
     };
@@ -1950,13 +1964,9 @@ cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN
     return go(k_mac_multi_tma<4>, 4, 256);
   }
   if (g_mac_async && (1u << logN) % kMacTile == 0) {
-    static bool attr = false;
     const size_t sm = sizeof(MacStage) * kMacStages;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k_mac_multi_async, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e) return e;
-      attr = true;
-    }
+    cudaError_t e = ensure_smem((const void*)k_mac_multi_async, sm);
+    if (e) return e;
     dim3 g((1u << logN) / kMacTile, nq, 1);
     k_mac_multi_async<<<g, 256, sm, st>>>(M, ng, nt, nq, logN, accumulate, mc);
     return cudaGetLastError();
@@ -2109,22 +2119,20 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
                             Basis basis, u32 alpha, u32 ndig, u32 logN, u64 g, const ModConsts* mc,
                             cudaStream_t st, u32 nb, size_t x_bst, const u64* c0, size_t c0_bst, const u64* pR,
                             u32 key_lq, u32 fast_from) {
-  // TMA staging pays once a key tile feeds >= 3 entries; small batches keep
-  // the register-pipelined kernel (measured: tools/ks_bench.py)
+  // batches of g_ks_tma_min (2) or more entries take the TMA-staged inner
+  // product, single entries the register-pipelined kernel (measured with
+  // tools/ks_bench.py and interleaved ResNet20 A/B runs)
   if (g_ks_tma && g_ks_tma3 && nb >= (u32)g_ks_tma_min && (1u << logN) % kMacTile == 0) {
     // rows [0, ff) and [nq, n_ext): generic; [ff, nq): 96-bit carry chains
     const u32 nbb = nb ? nb : 1, nq = basis.nq, nl = basis.nlimbs();
     const u32 ff = fast_from < 1 ? 1 : (fast_from > nq ? nq : fast_from);
-    static bool attr3[2][5] = {};
     const int stages = g_ks3_stages >= 2 && g_ks3_stages <= 4 ? g_ks3_stages : 3;
     auto go3 = [&](auto kern, int fast, u32 r0, u32 rows) -> cudaError_t {
+      (void)fast;
       if (rows == 0) return cudaSuccess;
       const size_t sm = sizeof(KsStage) * stages;
-      if (!attr3[fast][stages]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e) return e;
-        attr3[fast][stages] = true;
-      }
+      cudaError_t e = ensure_smem((const void*)kern, sm);
+      if (e) return e;
       dim3 grid((1u << logN) / kMacTile, rows, (nbb + kKsEntries - 1) / kKsEntries);
       kern<<<grid, 128 + 32, sm, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nbb, x_bst,
                                       c0, c0_bst, pR, key_lq, r0);
@@ -2144,15 +2152,11 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
   if (g_ks_tma && nb >= (u32)g_ks_tma_min && (1u << logN) % kMacTile == 0) {
     const u32 nbb = nb ? nb : 1;
     dim3 grid((1u << logN) / kMacTile, basis.nlimbs(), (nbb + kKsEntries - 1) / kKsEntries);
-    static bool attr_done[2][9] = {};
     const int tpb = g_ks_tpb == 128 ? 128 : 256;
     auto go = [&](auto kern, int stages) -> cudaError_t {
       const size_t sm = sizeof(KsStage) * stages;
-      if (!attr_done[tpb == 128][stages]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e) return e;
-        attr_done[tpb == 128][stages] = true;
-      }
+      cudaError_t e = ensure_smem((const void*)kern, sm);
+      if (e) return e;
       kern<<<grid, tpb, sm, st>>>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nbb, x_bst, c0,
                                   c0_bst, pR, key_lq);
       return cudaGetLastError();

@@ -1168,7 +1168,7 @@ static int mac_terms_impl(hcnn_ctx* c, uint64_t* out, const uint64_t* const* cts
 }
 
 static int masks_packable(const hcnn_ctx* c, u32 nq) {
-  if (nq > 64) return 0;
+  if (nq > 63) return 0;  // packed_hb / packed_hi_off shift 1ull << nq
   for (u32 r = 1; r < nq; ++r)
     if (c->mods[r] >> 48) return 0;
   return 1;

@@ -276,7 +276,7 @@ class DeviceContext:
         return (8 + 4 * level + sum(2 if q >> 40 else 1 for q in self.q_list[1:level + 1])) * self.n
 
     def masks_packable(self, level: int) -> bool:
-        return level < 64 and all(q < (1 << 48) for q in self.q_list[1:level + 1])
+        return level < 63 and all(q < (1 << 48) for q in self.q_list[1:level + 1])  # nq <= 63 (hcnn_pack_masks)
 
     def pack_masks(self, rows: torch.Tensor, level: int) -> torch.Tensor:
         """Montgomery rows [k, l+1, N] -> uint8 [k, packed_mask_bytes(l)] (lossless 40/48-bit planes)."""

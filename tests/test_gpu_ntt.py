@@ -112,12 +112,14 @@ def test_ntt_from_signed_fused(logn, mont):
 
 def test_roofline_instrumentation():
     """bench.py's integer roofline: the butterfly-rate probes run and order
-    as measured (FP64 quotient > integer fast > full width), and the limb
-    counters classify one forward + one inverse transform by modulus width."""
+    as measured (pure FP64 network > FP64 quotient > integer fast > full
+    width), and the limb counters classify one forward + one inverse
+    transform by modulus width."""
     from paper_2310_16530_b200 import _native
     from paper_2310_16530_b200.engine import context_for, to_device_u64
-    fp, fast, full = (_native.ntt_butterfly_peak(k) for k in (2, 1, 0))
-    assert fp > 0 and fast > 0 and full > 0
+    f64, fp, fast, full = (_native.ntt_butterfly_peak(k) for k in (4, 2, 1, 0))
+    assert f64 > 0 and fp > 0 and fast > 0 and full > 0
+    assert f64 > fp  # the network the class-2 (q < 2^41) limbs now run
     assert fast > full  # the unreduced network issues fewer instructions
     n = 1 << 16
     qs = _mods(n)  # 59-bit (full), 40-bit (FP64 class), 45-bit (integer fast class)

@@ -298,7 +298,7 @@ _KNOB_VARIANTS = [
 def test_launch_shape_variants_bit_identical(small, cts):
     """Every launch shape of k_mac_multi_tma(2/3) / k_ks_inner_tma(2) gives the
     residues of the shipped shape: plane MACs over mixed packed / unpacked /
-    absent masks, and batched (>= 3 entries: TMA path) hoisted rotations."""
+    absent masks, and batched (>= 2 entries: TMA path) hoisted rotations."""
     import torch
     from paper_2310_16530_b200 import _native, ckks
     params, ks = small

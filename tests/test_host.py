@@ -277,3 +277,57 @@ def test_conv_rotation_step_counts():
     assert len(ba) == 8 + 2
     fixed = packing.conv_rotation_steps(packing.ConvLayerSpec(w, 1, A, A), shape, 256, fixed=True)
     assert len(fixed) == 9 * 4 - 1
+
+
+_SHIM_SCRIPT = r"""
+import os, sys, traceback
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from hcnn import ckks as rc, packing as rp, graph as rg        # the unmodified reference
+from paper_2310_16530_b200 import ckks as gc, ring as gr, refshim
+from paper_2310_16530_b200.errors import NativeError
+orig_hmult, orig_ct = rc.hmult, rp.Ciphertext
+refshim.enable(rc, rp, rg)
+assert rc.hmult is gc.hmult and rc.rotate is gc.rotate and rc.encode is gc.encode
+assert rp.Ciphertext is gc.Ciphertext and rg.Ciphertext is gc.Ciphertext
+assert rp.to_mont_rows is gr.to_mont_rows and rp._zero_ct is refshim._zero_ct
+params = rc.CkksParams.build("shim", 256, 50, 40, 4, 50, 2)
+assert type(params) is gc.CkksParams
+class KS:                                  # only .params is read before the first device call
+    pass
+ks = KS(); ks.params = params
+fmt = rp.PackingFormat("A", 4, 1, 4)
+try:
+    rp.encrypt_tensor(np.zeros((4, 2, 2)), fmt, ks, np.random.default_rng(0), 2)
+    raise SystemExit("expected NativeError: no CUDA device")
+except NativeError:
+    frames = [f.filename for f in traceback.extract_tb(sys.exc_info()[2])]
+    assert any(f.endswith("hcnn/packing.py") for f in frames), frames          # the reference's layer code ...
+    assert any("paper_2310_16530_b200" in f for f in frames), frames           # ... called into the engine
+refshim.disable()
+assert rc.hmult is orig_hmult and rp.Ciphertext is orig_ct
+print("shim ok")
+"""
+
+
+def test_reference_side_shim_routes_reference_layers_into_the_engine(tmp_path):
+    """refshim.enable patches the reference's hcnn.ckks / packing / graph
+    (including the name-bound hooks), so the reference's own
+    packing code calls this engine -- here, without a GPU, its loud
+    NativeError proves the routing.  Runs only where /root/reference exists
+    (the build container); the GPU box has no reference to patch."""
+    import os
+    import subprocess
+    import sys
+    src = Path("/root/reference/pkg/src")
+    if not (src / "hcnn" / "packing.py").exists():
+        pytest.skip("reference package not present")
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("routing check relies on the no-device NativeError")
+    env = dict(os.environ, NUMBA_CACHE_DIR=str(tmp_path / "numba"), HCNN_TEST_MODE="1",
+               PYTHONPATH=str(ROOT) + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run([sys.executable, "-c", _SHIM_SCRIPT, str(src)], cwd=tmp_path, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "shim ok" in r.stdout
