@@ -349,13 +349,13 @@ def run_resnet20(args, cl):
     # eager runs first (mask build, measured residency fill, lazy tables;
     # then one event-profiled image for the kernel table / roofline / launch
     # count), then capture -- so the capture pool reuses the eager memory
-    warm = workloads.warm_up(s, imgs[0], cache)
+    warm = workloads.warm_up(s, imgs, cache)
     k0 = _native.kernel_launches()
     _native.profile_read(reset=True)
     _native.ntt_limb_counts(reset=True)
     _native.ks_counters(reset=True)
     _native.profile_enable(True)
-    graph.execute(s.graph, s.plan, imgs[-1], s.ks, "encrypted", cache=cache)
+    graph.execute_many(s.graph, s.plan, imgs, s.ks, cache=cache)
     torch.cuda.synchronize()
     _native.profile_enable(False)
     prof = _native.profile_read(reset=True)
@@ -365,13 +365,14 @@ def run_resnet20(args, cl):
     roofline, kernels = roofline_from_profile(prof)
     roofline = int_roofline(roofline, prof, limbs, s.params.n)
     ks_roof = keyswitch_roofline(prof, ksc, s.params.n)
-    runner = graph.CapturedInference(s.graph, s.plan, s.ks, imgs[0], cache, warmup=False)
+    # all B images of a step in one captured graph (graph.execute_many:
+    # their refresh points bootstrap as one batch)
+    runner = graph.CapturedInference(s.graph, s.plan, s.ks, imgs[0], cache, warmup=False, images=B)
     per_layer = _layer_rows(runner.report.per_layer)
     tally = runner.report.totals().as_dict()
 
     def step():
-        for im in imgs:
-            runner.run(im)
+        runner.run_many(imgs)
 
     for _ in range(args.warmup):
         step()
@@ -385,22 +386,24 @@ def run_resnet20(args, cl):
 
     # e2e: every step's encrypted inputs from pinned host memory, encrypted logits back
     host_in = [[ct.data.to("cpu").pin_memory() for ct in im.cts] for im in imgs]
-    out_ct = runner.out
-    host_out = [torch.empty(out_ct.data.shape, dtype=torch.int64).pin_memory() for _ in imgs]
+    host_out = [torch.empty(o.data.shape, dtype=torch.int64).pin_memory() for o in runner.outs]
     h2d = sum(t.numel() * 8 for src in host_in for t in src)
 
     def e2e_step():
-        for src, hout in zip(host_in, host_out):
-            for dst, h in zip(runner.inp.cts, src):
+        for src, inp in zip(host_in, runner.inps):
+            for dst, h in zip(inp.cts, src):
                 dst.data.copy_(h, non_blocking=True)
-            runner.cuda_graph.replay()
-            hout.copy_(out_ct.data, non_blocking=True)
+        runner.cuda_graph.replay()
+        for o, hout in zip(runner.outs, host_out):
+            hout.copy_(o.data, non_blocking=True)
 
     for _ in range(2):
         e2e_step()
     ms_e2e = timed_steps(cl, e2e_step, args.steps)
+    torch.cuda.synchronize()
     e2e = {"value": B * cl.world / (ms_e2e / args.steps / 1e3), "unit": "images/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": sum(h.numel() * 8 for h in host_out)}
+    out_ct = runner.out
 
     # correctness of the measured path: decrypt each of this rank's replayed
     # logits (the last e2e step's host copies) against the float mirror
@@ -432,7 +435,7 @@ def run_resnet20(args, cl):
             "data": "synthetic",
             "config": resnet20_config(s.params, s.graph, s.plan, s.cfg.depth(), s.boot.output_level, cl.world, B),
             "e2e": e2e, "roofline": roofline, "keyswitch": ks_roof, "cpu_baseline": cpu, "clocks": clocks,
-            "gpu_launches": launches * B, "gpu_launches_per_image": launches, "cuda_graph": True,
+            "gpu_launches": launches, "gpu_launches_per_image": launches / B, "cuda_graph": True,
             "resident_mask_gb": round(packing.resident_bytes() / 2 ** 30, 1),
             "tally_per_image": tally, "kernels": kernels,
             "per_rank": [{"rank": p["rank"], "ms": round(p["ms"], 3), "images_per_s": round(p["value_rank"], 4)}

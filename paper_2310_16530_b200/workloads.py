@@ -67,13 +67,6 @@ def cfg2_params() -> ckks.CkksParams:
                                  CFG2["log_p"], CFG2["n_special"])
 
 
-# per-image op tally of resnet20_setup()'s encrypted inference
-# (graph.CostReport.totals(); profiles/r01_resnet20_graph.json) -- lets the
-# host-only reference arm extrapolate without running the GPU executor
-RESNET20_TALLY = {"rotations": 1964, "hmults": 172, "pmults": 44464, "hadds": 44856, "rescales": 793,
-                  "refreshes": 32}
-
-
 def resnet20_plan_only(app_levels: int | None = None, seed: int = 3):
     """Host-only part of resnet20_setup (params, graph, plan; no keys/GPU)."""
     cfg = resnet20_boot_config()
@@ -87,13 +80,16 @@ def resnet20_plan_only(app_levels: int | None = None, seed: int = 3):
     return params, g, plan
 
 
-def warm_up(s: ResNet20Setup, ct: packing.PackedTensor, cache: dict) -> dict:
+def warm_up(s: ResNet20Setup, ct, cache: dict) -> dict:
     """First two eager inferences of a workload, sizing mask residency from
     measurement instead of a guess: run 1 builds every mask (compact, none
     resident) and measures the largest transient working set of any layer
     W (peak minus the layer's starting footprint); run 2 keeps masks
     resident while 1.5 W + 3 GiB stays free -- room for the CUDA-graph
-    capture (graph.CapturedInference) and the live activations."""
+    capture (graph.CapturedInference) and the live activations.  `ct` may
+    be a list of images: both runs then go through graph.execute_many, so
+    W includes the batched bootstraps of all of them."""
+    cts = list(ct) if isinstance(ct, (list, tuple)) else [ct]
     import time
     import torch
     packing.set_residency(False)
@@ -112,7 +108,7 @@ def warm_up(s: ResNet20Setup, ct: packing.PackedTensor, cache: dict) -> dict:
             work[0] = max(work[0], torch.cuda.max_memory_allocated() - max(marks["start"], end))
 
     t0 = time.time()
-    graph.execute(s.graph, s.plan, ct, s.ks, "encrypted", cache=cache, layer_hook=hook)
+    graph.execute_many(s.graph, s.plan, cts, s.ks, cache=cache, layer_hook=hook)
     torch.cuda.synchronize()
     t_build = time.time() - t0
     after = torch.cuda.memory_allocated()
@@ -120,7 +116,7 @@ def warm_up(s: ResNet20Setup, ct: packing.PackedTensor, cache: dict) -> dict:
     torch.cuda.empty_cache()
     packing.set_residency(True, reserve)
     t0 = time.time()
-    graph.execute(s.graph, s.plan, ct, s.ks, "encrypted", cache=cache)
+    graph.execute_many(s.graph, s.plan, cts, s.ks, cache=cache)
     torch.cuda.synchronize()
     return {"first_image_s": round(t_build, 2), "residency_fill_s": round(time.time() - t0, 2),
             "layer_working_set_gb": round(work[0] / 2 ** 30, 2),

@@ -68,3 +68,29 @@ def test_tiny_cnn_desk_b_bit_exact(golden_hashes):
     ref, _ = graph.execute(g, plan, x, mode="plaintext-ref")
     assert np.max(np.abs(logits - ref)) < 1e-2
     assert int(np.argmax(logits)) == int(np.argmax(ref))
+
+
+def test_execute_many_matches_single_images(golden_hashes):
+    """graph.execute_many (B images in lockstep, bench.py --images-per-gpu)
+    gives each image exactly its single-image residues and op tally on a
+    graph without refresh points (the acceptance basic block, desk-A)."""
+    import torch
+    from paper_2310_16530_b200 import ckks, graph, packing
+    gold = golden_hashes["layers"]["block"]
+    params = ckks.desk_a()
+    fx = graph.gen_fixture("basic-block-stack(1)", 21, params)
+    g = graph.build_graph("basic-block-stack(1)", fx, multiplex=8)
+    steps = sorted(graph.required_rotation_steps(g, params.slots))
+    ks = ckks.keygen(params, np.random.default_rng(gold["key_seed"]), rotations=steps)
+    plan = graph.plan_levels(g, params.max_level)
+    assert not plan.refresh_points
+    rng = np.random.default_rng(5)
+    xs = [packing.encrypt_tensor(rng.uniform(-1, 1, (8, 8, 8)), g.input_format, ks, rng, plan.entry_levels[0])
+          for _ in range(3)]
+    cache: dict = {}
+    many = graph.execute_many(g, plan, xs, ks, cache=cache)
+    for x, (out, rep) in zip(xs, many):
+        one, rep1 = graph.execute(g, plan, x, ks, "encrypted", cache=cache)
+        assert rep.totals().as_dict() == rep1.totals().as_dict()
+        assert all(torch.equal(a.data, b.data) for a, b in zip(out.cts, one.cts))
+    assert h(_cts(many[0][0].cts)) != h(_cts(many[1][0].cts))
