@@ -13,6 +13,29 @@
 
 namespace hcnn {
 
+// Per-device side stream + fork/join events for kernels that run next to
+// another launch of the same call (created once per device, never freed).
+static cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join) {
+  static std::mutex mu;
+  static cudaStream_t ss[64] = {};
+  static cudaEvent_t ef[64] = {}, ej[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ss[dev]) {
+    e = cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking);
+    if (!e) e = cudaEventCreateWithFlags(&ef[dev], cudaEventDisableTiming);
+    if (!e) e = cudaEventCreateWithFlags(&ej[dev], cudaEventDisableTiming);
+    if (e) return e;
+  }
+  *s = ss[dev];
+  *fork = ef[dev];
+  *join = ej[dev];
+  return cudaSuccess;
+}
+
 // Dynamic shared memory above 48 KB needs a per-kernel opt-in, and the
 // attribute is per device: cache (kernel, device, bytes) under a mutex so
 // contexts on several devices / threads each get it.
@@ -1909,6 +1932,7 @@ int g_ks3_stages = 3;  // its ring depth (2, 3, 4)
 int g_mac_tma = 3;    // 1: bulk-copy (TMA) staged k_mac_multi_tma(2), 3: warp-specialised k_mac_multi_tma3
 int g_mac3_stages = 4;  // k_mac_multi_tma3 ring depth (2, 3, 4, 6); tools/mac_probe.py: 4 = 3 < 2, 6
 int g_mac3_tpb = 128;   // k_mac_multi_tma3 threads per CTA (128 or 256)
+int g_mac3_fork = 1;    // run the generic (limb 0) rows on a forked side stream
 int g_mac_minb = 1;  // minimum resident CTAs per SM (register cap) of k_mac_multi_tma: 1, 4, 5, 6
 int g_mac_tpb = 128;  // threads per plane-MAC CTA: 128 (k_mac_multi_tma2, two coefficients per thread) or 256
 int g_tma_stages = 3;  // ring depth of the TMA-staged plane MAC (128 threads: 2, 3, 4; 256: 4, 6, 8; the 256-thread key-switch kernel takes max(4, this))
@@ -1922,22 +1946,47 @@ cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN
   if (g_mac_tma == 3 && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
     // rows [0, fast_from): generic 128-bit MACs; [fast_from, nq): 96-bit carry chains
     const int stages = g_mac3_stages, tpb = g_mac3_tpb;
-    auto go3 = [&](auto kern, int fast, u32 r0, u32 rows, int kst, int ktpb) -> cudaError_t {
+    auto go3 = [&](auto kern, int fast, u32 r0, u32 rows, int kst, int ktpb, cudaStream_t ls) -> cudaError_t {
       (void)fast;
       if (rows == 0) return cudaSuccess;
       const size_t sm = sizeof(MacStage) * kst;
       cudaError_t e = ensure_smem((const void*)kern, sm);
       if (e) return e;
-      kern<<<dim3((1u << logN) / kMacTile, rows, 1), ktpb + 32, sm, st>>>(M, ng, nt, nq, logN, r0, accumulate, mc);
+      kern<<<dim3((1u << logN) / kMacTile, rows, 1), ktpb + 32, sm, ls>>>(M, ng, nt, nq, logN, r0, accumulate, mc);
       return cudaGetLastError();
     };
     const u32 ff = M.fast_from < 1 ? 1 : (M.fast_from > nq ? nq : M.fast_from);
-    cudaError_t e = go3(k_mac_multi_tma3<3, 128, false>, 0, 0, ff, 3, 128);
-    if (e) return e;
-#define MAC3(ST, TPB) if (stages == ST && tpb == TPB) return go3(k_mac_multi_tma3<ST, TPB, true>, 1, ff, nq - ff, ST, TPB)
-    MAC3(2, 128); MAC3(4, 128); MAC3(6, 128); MAC3(2, 256); MAC3(3, 256); MAC3(4, 256); MAC3(6, 256);
+    // the generic rows (limb 0: 256 CTAs, latency-bound) run on a side
+    // stream forked from st, concurrently with the FAST rows, and join back
+    // before the call returns (also inside a CUDA-graph capture: a fork /
+    // join branch of the captured graph)
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    const bool par = g_mac3_fork && ff < nq && side_stream(&side, &fork, &join) == cudaSuccess;
+    cudaStream_t gst = st;
+    if (par) {
+      cudaError_t e = cudaEventRecord(fork, st);
+      if (!e) e = cudaStreamWaitEvent(side, fork, 0);
+      if (e) return e;
+      gst = side;
+    }
+    {
+      cudaError_t e = go3(k_mac_multi_tma3<3, 128, false>, 0, 0, ff, 3, 128, gst);
+      if (e) return e;
+    }
+    cudaError_t e = cudaSuccess;
+    bool done = false;
+#define MAC3(ST, TPB) \
+    if (!done && stages == ST && tpb == TPB) { e = go3(k_mac_multi_tma3<ST, TPB, true>, 1, ff, nq - ff, ST, TPB, st); done = true; }
+    MAC3(2, 128) MAC3(4, 128) MAC3(6, 128) MAC3(2, 256) MAC3(3, 256) MAC3(4, 256) MAC3(6, 256)
 #undef MAC3
-    return go3(k_mac_multi_tma3<3, 128, true>, 1, ff, nq - ff, 3, 128);
+    if (!done) e = go3(k_mac_multi_tma3<3, 128, true>, 1, ff, nq - ff, 3, 128, st);
+    if (par) {
+      cudaError_t e2 = cudaEventRecord(join, side);
+      if (!e2) e2 = cudaStreamWaitEvent(st, join, 0);
+      if (!e) e = e2;
+    }
+    return e;
   }
   if (g_mac_tma && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
     dim3 g((1u << logN) / kMacTile, nq, 1);

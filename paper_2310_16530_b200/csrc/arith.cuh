@@ -39,6 +39,7 @@ extern int g_ks_tma3;
 extern int g_ks3_stages;
 extern int g_mac3_stages;
 extern int g_mac3_tpb;
+extern int g_mac3_fork;
 extern int g_mac_tpb;
 extern int g_mac_minb;
 extern int g_ks_tpb;

@@ -1295,6 +1295,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ks3_stages") g_ks3_stages = (int)value;
   else if (k == "mac3_stages") g_mac3_stages = (int)value;
   else if (k == "mac3_tpb") g_mac3_tpb = (int)value;
+  else if (k == "mac3_fork") g_mac3_fork = (int)value;
   else if (k == "tma_stages") g_tma_stages = (int)value;
   else if (k == "ks_tpb") g_ks_tpb = value == 128 ? 128 : 256;
   else if (k == "ks_stages") g_ks_stages = (int)value;

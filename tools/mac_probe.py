@@ -14,7 +14,7 @@ import torch
 from paper_2310_16530_b200 import bootstrap as bt
 
 
-def main(level: int = 10, T: int = 36, G: int = 4, settings=("mac_tma=1",)):
+def main(level: int = 10, T: int = 36, G: int = 4, settings=("mac_tma=3",)):
     from paper_2310_16530_b200 import _native
     cfg = bt.BootConfig()
     params = bt.boot_params("resnet20-16", 1 << 16, 14, cfg)
@@ -65,5 +65,5 @@ def main(level: int = 10, T: int = 36, G: int = 4, settings=("mac_tma=1",)):
 
 if __name__ == "__main__":
     nums = [int(a) for a in sys.argv[1:] if "=" not in a]
-    sets = [a for a in sys.argv[1:] if "=" in a] or ["mac_tma=1"]
+    sets = [a for a in sys.argv[1:] if "=" in a] or ["mac_tma=3"]
     main(*nums, settings=sets)
