@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "arith.cuh"
+#include "tma.cuh"
 
 namespace hcnn {
 
@@ -36,22 +37,6 @@ static cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* 
   return cudaSuccess;
 }
 
-// Dynamic shared memory above 48 KB needs a per-kernel opt-in, and the
-// attribute is per device: cache (kernel, device, bytes) under a mutex so
-// contexts on several devices / threads each get it.
-static cudaError_t ensure_smem(const void* fn, size_t bytes) {
-  static std::mutex mu;
-  static std::set<std::tuple<const void*, int, size_t>> done;
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e) return e;
-  std::lock_guard<std::mutex> lk(mu);
-  auto key = std::make_tuple(fn, dev, bytes);
-  if (done.count(key)) return cudaSuccess;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (!e) done.insert(key);
-  return e;
-}
 
 static inline dim3 row_grid(u32 work_per_row, u32 rows, u32 threads) {
   u32 x = (work_per_row + threads - 1) / threads;
@@ -1198,29 +1183,6 @@ __global__ void __launch_bounds__(256) k_mac_multi_async(MacMulti M, int ng, int
 // stage's mbarrier phase and run the 8 lazy MACs per term.  Branches on
 // mask presence / packing read one flag byte per term staged in smem.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "MBAR_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
 __device__ __forceinline__ void mac_stage_bulk(MacStage& S, u64* bar, const MacMulti& M, int t, u32 fl, u32 r,
                                                u32 nq, u32 N, u32 k0) {
   const size_t off = (size_t)r * N + k0, pst = (size_t)nq * N;
@@ -1419,9 +1381,6 @@ __global__ void __launch_bounds__(TPB, MINB > 1 ? MINB : 0) k_mac_multi_tma2(Mac
 // product's ~11, no lazy folds (T < 2^90 < q 2^64 for <= 48 terms), one
 // REDC at the end: the same canonical sum * R^-1 mod q as mac128.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_arrive(u64* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void mac96(u64& lh, u64& mid, u32 a0, u32 a1, u32 m0, u32 m1) {
   asm("{\n\t.reg .u32 lo, hi, ml, mh;\n\t"
       "mov.b64 {lo, hi}, %0;\n\t"

@@ -1283,6 +1283,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_occupancy") g_ntt_tuning.occupancy = (int)value;
   else if (k == "ntt_split") g_ntt_tuning.split = (int)value;
   else if (k == "ntt_f64_minb") g_ntt_tuning.f64_minb = (int)value;
+  else if (k == "ntt_pipe") g_ntt_tuning.pipe = (int)value;
   else if (k == "ks_batch") g_ks_batch = (int)value;
   else if (k == "ks_pipe") g_ks_pipe = (int)value;
   else if (k == "ks_tma") g_ks_tma = (int)value;

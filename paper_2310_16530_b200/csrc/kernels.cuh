@@ -36,6 +36,7 @@ struct NttTuning {
   int occupancy = 0;  // 1: register-capped kernels (more resident warps)
   int split = 2;      // 1: separate launches per modulus class, 2: forward transforms only
   int f64_minb = 1;   // FP64 chunk passes: min CTAs per SM hint (1, 5 or 6)
+  int pipe = 1;       // FP64 forward chunk pass pipelined over polys (ntt2_fwd_chunks_f64p)
 };
 extern NttTuning g_ntt_tuning;
 

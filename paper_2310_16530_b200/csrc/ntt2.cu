@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace hcnn {
 
@@ -693,6 +694,88 @@ __global__ void __launch_bounds__(128, MINB) ntt2_fwd_chunks_f64(LimbMap map, co
   for (int k = 0; k < 16; ++k) a[j + 16 * k] = tl[17 * k + j];
 }
 
+// Forward chunk pass of the FP64 network, pipelined over polys: a CTA owns
+// chunk group blockIdx.x (8 chunks = 2048 contiguous coefficients) of one
+// limb for a range of polys.  The chunk twiddles are loaded once per CTA,
+// and each poly's 16 KB block is bulk-copied (cp.async.bulk + mbarrier)
+// into a double-buffered shared ring while the previous poly computes, so
+// the load latency that stalls the one-shot kernel (long_scoreboard ~50 %
+// of samples, r02_ncu_summary.md) overlaps the butterflies.
+constexpr u32 kChunkBlock = kChunksPerCta * 256;  // coefficients per CTA block
+template <bool HINT>
+__global__ void __launch_bounds__(128) ntt2_fwd_chunks_f64p(LimbMap map, const ModConsts* __restrict__ mc,
+                                                            const ulonglong2* __restrict__ ctw, u32 logN, u32 zper,
+                                                            u32 nz) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  u64* buf = reinterpret_cast<u64*>(smem_raw);  // [2][kChunkBlock]
+  u64* tile = buf + 2 * kChunkBlock;             // [kChunksPerCta][16 * 17]
+  __shared__ ulonglong2 twa[kChunksPerCta][16];
+  __shared__ __align__(8) u64 full[2];
+  const u32 r = blockIdx.y + map.r0;
+  const u32 z_lo = map.z0 + blockIdx.z * zper;
+  const u32 z_hi = z_lo + zper < map.z0 + nz ? z_lo + zper : map.z0 + nz;
+  const u32 N = 1u << logN, N1 = N >> 8;
+  const u32 mod = map.basis.mod_of(r + map.first_limb);
+  const double q = (double)mc[mod].q, qinv = 1.0 / q;
+  const int tid = threadIdx.x, cc = tid >> 4, j = tid & 15;
+  const u32 g0 = blockIdx.x * kChunksPerCta, g = g0 + cc;
+  const ulonglong2* T = ctw + ((size_t)mod * N1 + g) * 256;
+  u64* tl = tile + cc * (16 * 17);
+  const u64 pol = HINT ? keep_policy() : 0;
+  if (j < 15) twa[cc][j] = ld_tw<HINT>(&T[j], pol);
+  ulonglong2 tb[15];
+#pragma unroll
+  for (int d = 0; d < 4; ++d)
+#pragma unroll
+    for (int b = 0; b < (1 << d); ++b) tb[(1 << d) - 1 + b] = ld_tw<HINT>(&T[(16 << d) - 1 + (j << d) + b], pol);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto blk = [&](u32 z) { return map.base + (size_t)z * map.poly_stride + (size_t)r * N + (size_t)g0 * 256; };
+  auto next = [&](u32 z) {
+    while (z < z_hi && limb_skipped2(map, r, z)) ++z;
+    return z;
+  };
+  u32 z = next(z_lo);
+  if (tid == 0 && z < z_hi) {
+    mbar_expect_tx(&full[0], kChunkBlock * 8);
+    bulk_g2s(buf, blk(z), kChunkBlock * 8, &full[0]);
+  }
+  auto twA = [&](int d, int b) { return twa[cc][(1 << d) - 1 + b]; };
+  auto twB = [&](int d, int b) { return tb[(1 << d) - 1 + b]; };
+  for (u32 it = 0; z < z_hi; ++it) {
+    const u32 zn = next(z + 1), cur = it & 1u;
+    if (tid == 0 && zn < z_hi) {  // buffer cur^1 was released by the previous iteration's barrier
+      mbar_expect_tx(&full[cur ^ 1u], kChunkBlock * 8);
+      bulk_g2s(buf + (cur ^ 1u) * kChunkBlock, blk(zn), kChunkBlock * 8, &full[cur ^ 1u]);
+    }
+    mbar_wait(&full[cur], (it >> 1) & 1u);
+    const u64* B = buf + cur * kChunkBlock + cc * 256;
+    double x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = bits_d(B[j + 16 * k]);
+    ct16_f64<0>(x, q, twA);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tl[17 * k + j] = d_bits(x[k]);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = bits_d(tl[17 * j + k]);
+    ct16_f64<0>(x, q, twB);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tl[17 * j + k] = d2u(fcanon(x[k], q, qinv));  // |x| < 13q -> [0, q)
+    __syncwarp();
+    u64* a = blk(z) + (size_t)cc * 256;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[j + 16 * k] = tl[17 * k + j];
+    __syncthreads();  // buf[cur] and the transpose tiles are free
+    z = zn;
+  }
+}
+
 template <bool HINT, int MINB>
 __global__ void __launch_bounds__(128, MINB) ntt2_inv_chunks_f64(LimbMap map, const ModConsts* __restrict__ mc,
                                                              const ulonglong2* __restrict__ ctw, u32 logN) {
@@ -987,6 +1070,20 @@ static cudaError_t launch_pair_f64(const NttTables& T, const LimbMap& map, u32 n
     }
   };
   const int mb = g_ntt_tuning.f64_minb;
+  if (!inverse && g_ntt_tuning.pipe) {
+    if (!cols_launch(false)) return cudaErrorInvalidValue;
+    // polys per CTA: enough CTAs for ~2 waves of 4 per SM, the rest pipelined
+    const u32 want = 2u * 148u * 4u, per_z = gk.x * ny;
+    u32 zsplit = (want + per_z - 1) / per_z;
+    zsplit = zsplit < 1 ? 1 : (zsplit > nz ? nz : zsplit);
+    const u32 zper = (nz + zsplit - 1) / zsplit;
+    zsplit = (nz + zper - 1) / zper;
+    const size_t sm = (2 * kChunkBlock + kChunksPerCta * 16 * 17) * 8;
+    cudaError_t e = ensure_smem((const void*)ntt2_fwd_chunks_f64p<H>, sm);
+    if (e) return e;
+    ntt2_fwd_chunks_f64p<H><<<dim3(gk.x, ny, zsplit), 128, sm, st>>>(map, T.mc, T.ctw, logN, zper, nz);
+    return cudaGetLastError();
+  }
   if (!inverse) {
     if (!cols_launch(false)) return cudaErrorInvalidValue;
     if (mb == 5) ntt2_fwd_chunks_f64<H, 5><<<gk, 128, 0, st>>>(map, T.mc, T.ctw, logN);
