@@ -680,6 +680,42 @@ __global__ void __launch_bounds__(256) k_moddown_combine_steps(ComboSteps S, con
   }
 }
 
+// k_moddown_combine for rows r0.. of the lift from an NttCombine
+// descriptor (the rows whose lift NTT ran on the integer network)
+__global__ void __launch_bounds__(256) k_combine_rows(NttCombine C, const u64* __restrict__ lift, u32 nq, u32 r0,
+                                                     u32 logN, const ModConsts* __restrict__ mc) {
+  const u32 N = 1u << logN, r = blockIdx.y + r0, z = blockIdx.z, p = z & 1, sb = z >> 1, s = sb / C.nb,
+            b = sb % C.nb;
+  const u64 q = mc[r].q;
+  const u64 w = C.pinv[r], wp = C.pinv_sh[r];
+  const u64 g_add = C.g[s];
+  const u64* A = C.acc + (size_t)z * C.acc_pst + (size_t)r * N;
+  const u64* L = lift + ((size_t)z * nq + r) * N;
+  const u64* ADD = C.add[p] ? C.add[p] + (size_t)b * C.add_bst + (size_t)r * N : nullptr;
+  u64* O = C.out[s] + (size_t)b * C.out_bst + (size_t)p * C.out_pst + (size_t)r * N;
+  for (u32 k2 = blockIdx.x * blockDim.x + threadIdx.x; k2 < N / 2; k2 += gridDim.x * blockDim.x) {
+    const u32 k = 2 * k2;
+    const ulonglong2 av = *reinterpret_cast<const ulonglong2*>(A + k);
+    const ulonglong2 lv = *reinterpret_cast<const ulonglong2*>(L + k);
+    u64 v0 = shoup_mul(sub_mod(av.x, lv.x, q), w, wp, q);
+    u64 v1 = shoup_mul(sub_mod(av.y, lv.y, q), w, wp, q);
+    if (ADD) {
+      v0 = add_mod(v0, ADD[g_add == 1 ? k : galois_src(k, g_add, logN)], q);
+      v1 = add_mod(v1, ADD[g_add == 1 ? k + 1 : galois_src(k + 1, g_add, logN)], q);
+    }
+    *reinterpret_cast<ulonglong2*>(O + k) = make_ulonglong2(v0, v1);
+  }
+}
+
+cudaError_t launch_combine_rows(const NttCombine& C, const u64* lift, u32 nq, u32 r0, u32 nrows, u32 npolys,
+                                u32 logN, const ModConsts* mc, cudaStream_t st) {
+  if (nrows == 0 || npolys == 0) return cudaSuccess;
+  dim3 g = row_grid((1u << logN) / 2, nrows, 256);
+  g.z = npolys;
+  k_combine_rows<<<g, 256, 0, st>>>(C, lift, nq, r0, logN, mc);
+  return cudaGetLastError();
+}
+
 // acc_{b,p}[r] += P * d_{b,p}[r] mod q_r on the Q limbs of nb extended-basis
 // accumulators ([nb][2][n_ext]); d is [nb][2][nq] (the tensor product's d0,
 // d1), pR = P R mod q_r (Montgomery form, so one REDC gives P d).  Fused
@@ -1885,7 +1921,7 @@ __global__ void __launch_bounds__(TPB + 32) k_ks_inner_tma3(u64* __restrict__ ac
 
 // 0: off -- measured slower than k_ks_inner_tma2 (tools/ks_bench.py: 3.7 vs 4.3 TB/s
 // at level 14 nb 4, 4.0 vs 4.6 at level 30 nb 8; three row launches, 3 CTAs/SM)
-int g_ks_tma3 = 0;     // 1: k_ks_inner_tma3 (warp-specialised) for TMA-routed batches
+int g_ks_tma3 = 0;     // 1: k_ks_inner_tma3 (warp-specialised, 96-bit rows split out), 2: one generic launch
 int g_ks3_stages = 3;  // its ring depth (2, 3, 4)
 
 int g_mac_tma = 3;    // 1: bulk-copy (TMA) staged k_mac_multi_tma(2), 3: warp-specialised k_mac_multi_tma3
@@ -2148,6 +2184,7 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
     };
     cudaError_t e;
 #define KS3(ST)                                                                          \
+    if (stages == ST && g_ks_tma3 == 2) return go3(k_ks_inner_tma3<ST, 128, false>, 0, 0, nl); \
     if (stages == ST) {                                                                  \
       e = go3(k_ks_inner_tma3<ST, 128, false>, 0, 0, ff);                                \
       if (!e) e = go3(k_ks_inner_tma3<ST, 128, true>, 1, ff, nq - ff);                   \

@@ -859,10 +859,31 @@ static int ks_moddown(hcnn_ctx* c, u32 level, u64* acc, u64* lift, u64* out0, u6
   l.base = lift;
   l.poly_stride = nq * N;
   l.basis = c->basis(nq, 0);
+  // the combine rides on the lift NTT's store when the outputs are laid out
+  // [c0 | c1] (out1 = out0 + nq N, add1 = add0 + nq N or absent)
+  NttCombine cb{};
+  const bool fuse = g_ntt_tuning.md_fuse && g_ntt_tuning.group_limbs == 0 && out1 == out0 + (size_t)nq * N &&
+                    (!add1 || (add0 && add1 == add0 + (size_t)nq * N));
+  if (fuse) {
+    cb.acc = acc;
+    cb.acc_pst = (size_t)n_ext * N;
+    cb.pinv = c->d_pinv;
+    cb.pinv_sh = c->d_pinv_sh;
+    cb.nb = nb;
+    cb.out_bst = out_bst;
+    cb.out_pst = (size_t)nq * N;
+    cb.add_bst = add_bst;
+    cb.add[0] = add0;
+    cb.add[1] = add1;
+    cb.out[0] = out0;
+    cb.g[0] = g_add;
+    l.cb = &cb;
+  }
   PK("ntt_fwd_moddown", 16.0 * 2 * nb * nq * N, ntt_nk(c), st, launch_ntt(c->tables(), l, nq, 2 * nb, false, st));
-  PK("moddown_combine", 8.0 * 2 * nb * (3 * nq + (add0 ? nq : 0)) * N, 1, st,
-     launch_moddown_combine(out0, out1, acc, lift, add0, add1, g_add, nq, n_ext, c->logN, c->d_pinv,
-                            c->d_pinv_sh, c->d_mc, st, nb, out_bst, add_bst));
+  if (!fuse)
+    PK("moddown_combine", 8.0 * 2 * nb * (3 * nq + (add0 ? nq : 0)) * N, 1, st,
+       launch_moddown_combine(out0, out1, acc, lift, add0, add1, g_add, nq, n_ext, c->logN, c->d_pinv,
+                              c->d_pinv_sh, c->d_mc, st, nb, out_bst, add_bst));
   return HCNN_OK;
 }
 
@@ -990,11 +1011,31 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
     l.base = w.lift;
     l.poly_stride = nq * N;
     l.basis = c->basis(nq, 0);
+    NttCombine cb{};
+    const bool fuse = g_ntt_tuning.md_fuse && g_ntt_tuning.group_limbs == 0 && nr <= (u32)kCombineMax;
+    if (fuse) {
+      cb.acc = w.acc;
+      cb.acc_pst = (size_t)n_ext * N;
+      cb.pinv = c->d_pinv;
+      cb.pinv_sh = c->d_pinv_sh;
+      cb.nb = nb;
+      cb.out_bst = ct;
+      cb.out_pst = (size_t)nq * N;
+      cb.add_bst = ct;
+      cb.add[0] = cts;
+      cb.add[1] = nullptr;
+      for (u32 j = 0; j < nr; ++j) {
+        cb.out[j] = S.out[j];
+        cb.g[j] = S.g[j];
+      }
+      l.cb = &cb;
+    }
     PK("ntt_fwd_moddown", 16.0 * np * nq * N, ntt_nk(c), STREAM(s),
        launch_ntt(c->tables(), l, nq, np, false, STREAM(s)));
-    PK("moddown_combine", 8.0 * np * 4 * nq * N, 1, STREAM(s),
-       launch_moddown_combine_steps(S, nr, w.acc, w.lift, cts, nb, nq, n_ext, c->logN, c->d_pinv, c->d_pinv_sh,
-                                    c->d_mc, ct, ct, STREAM(s)));
+    if (!fuse)
+      PK("moddown_combine", 8.0 * np * 4 * nq * N, 1, STREAM(s),
+         launch_moddown_combine_steps(S, nr, w.acc, w.lift, cts, nb, nq, n_ext, c->logN, c->d_pinv, c->d_pinv_sh,
+                                      c->d_mc, ct, ct, STREAM(s)));
   }
   return HCNN_OK;
 }
@@ -1284,6 +1325,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_split") g_ntt_tuning.split = (int)value;
   else if (k == "ntt_f64_minb") g_ntt_tuning.f64_minb = (int)value;
   else if (k == "ntt_pipe") g_ntt_tuning.pipe = (int)value;
+  else if (k == "md_fuse") g_ntt_tuning.md_fuse = (int)value;
   else if (k == "ks_batch") g_ks_batch = (int)value;
   else if (k == "ks_pipe") g_ks_pipe = (int)value;
   else if (k == "ks_tma") g_ks_tma = (int)value;

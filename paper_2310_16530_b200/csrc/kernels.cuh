@@ -26,7 +26,31 @@ struct LimbMap {
   // sin_center != 0: the row holds residues mod sin_center (a rescale's top
   // limb after its iNTT), read as the centred lift t > q/2 ? t - q : t
   u64 sin_center;
+  // forward NTT only, host pointer (null: plain NTT): the transform is the
+  // ModDown lift and its store is fused with the combine (NttCombine)
+  const struct NttCombine* cb;
 };
+
+// ModDown combine fused into the lift's forward NTT (ckks.py:548-602): for
+// poly z = 2 (s nb + b) + p of the lift, out = (acc_Q - lift) P^-1 (+ add),
+// exactly k_moddown_combine(_steps)'s arithmetic.  out[s] + b out_bst +
+// p out_pst + r N; add[p] + b add_bst + r N gathered through Galois g[s].
+constexpr int kCombineMax = 32;
+struct NttCombine {
+  const u64* acc;
+  size_t acc_pst;  // poly stride of acc (n_ext N)
+  const u64* pinv;
+  const u64* pinv_sh;
+  u32 nb;
+  size_t out_bst, out_pst, add_bst;
+  const u64* add[2];
+  u64* out[kCombineMax];
+  u64 g[kCombineMax];
+};
+// the combine for rows [r0, r0 + nrows) of an npolys-poly lift (the rows the
+// NTT did not fuse)
+cudaError_t launch_combine_rows(const NttCombine& C, const u64* lift, u32 nq, u32 r0, u32 nrows, u32 npolys,
+                                u32 logN, const ModConsts* mc, cudaStream_t st);
 
 // tuning knobs (hcnn_set_option): NTT sub-batch size in limbs (0 = one
 // launch pair for the whole batch) and L2 cache-policy hints
@@ -37,6 +61,10 @@ struct NttTuning {
   int split = 2;      // 1: separate launches per modulus class, 2: forward transforms only
   int f64_minb = 1;   // FP64 chunk passes: min CTAs per SM hint (1, 5 or 6)
   int pipe = 1;       // FP64 forward chunk pass pipelined over polys (ntt2_fwd_chunks_f64p)
+  // ModDown combine fused into the lift NTT's FP64 chunk pass: off -- measured
+  // slower (tools/ks_bench.py: hoisted rotations at level 14, 2.21 -> 2.86 ms;
+  // the epilogue's acc / c0 loads are not prefetched and stall every poly)
+  int md_fuse = 0;
 };
 extern NttTuning g_ntt_tuning;
 

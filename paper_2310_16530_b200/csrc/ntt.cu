@@ -252,6 +252,14 @@ cudaError_t launch_ntt(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 n
                        cudaStream_t st) {
   if (nlimbs == 0 || npolys == 0) return cudaSuccess;
   if (T.ctw) return launch_ntt2(T, map, nlimbs, npolys, inverse, st);
+  if (map.cb) {  // small rings: plain NTT, then the ModDown combine kernel
+    LimbMap m = map;
+    m.cb = nullptr;
+    cudaError_t e = launch_ntt(T, m, nlimbs, npolys, inverse, st);
+    if (e) return e;
+    return launch_combine_rows(*map.cb, map.base, map.basis.nq, map.r0 + map.first_limb, nlimbs, npolys, T.logN,
+                               T.mc, st);
+  }
   u32 logN = T.logN, logN1;
   ntt_split(logN, &logN1);
   const u32 N = 1u << logN;

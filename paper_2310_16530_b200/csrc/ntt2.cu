@@ -702,10 +702,10 @@ __global__ void __launch_bounds__(128, MINB) ntt2_fwd_chunks_f64(LimbMap map, co
 // the load latency that stalls the one-shot kernel (long_scoreboard ~50 %
 // of samples, r02_ncu_summary.md) overlaps the butterflies.
 constexpr u32 kChunkBlock = kChunksPerCta * 256;  // coefficients per CTA block
-template <bool HINT>
+template <bool HINT, bool CB>
 __global__ void __launch_bounds__(128) ntt2_fwd_chunks_f64p(LimbMap map, const ModConsts* __restrict__ mc,
                                                             const ulonglong2* __restrict__ ctw, u32 logN, u32 zper,
-                                                            u32 nz) {
+                                                            u32 nz, NttCombine cbv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   u64* buf = reinterpret_cast<u64*>(smem_raw);  // [2][kChunkBlock]
   u64* tile = buf + 2 * kChunkBlock;             // [kChunksPerCta][16 * 17]
@@ -768,9 +768,26 @@ __global__ void __launch_bounds__(128) ntt2_fwd_chunks_f64p(LimbMap map, const M
 #pragma unroll
     for (int k = 0; k < 16; ++k) tl[17 * j + k] = d2u(fcanon(x[k], q, qinv));  // |x| < 13q -> [0, q)
     __syncwarp();
-    u64* a = blk(z) + (size_t)cc * 256;
+    if constexpr (CB) {
+      // fused ModDown combine: out = (acc_Q - lift) P^-1 (+ add), k_moddown_combine's arithmetic
+      const u32 p = z & 1u, sb = z >> 1, s = sb / cbv.nb, b = sb % cbv.nb;
+      const u64 qi = mc[mod].q, w = cbv.pinv[r], wp = cbv.pinv_sh[r], ga = cbv.g[s];
+      const size_t k0 = (size_t)g * 256;
+      const u64* A = cbv.acc + (size_t)z * cbv.acc_pst + (size_t)r * N + k0;
+      const u64* ADD = cbv.add[p] ? cbv.add[p] + (size_t)b * cbv.add_bst + (size_t)r * N : nullptr;
+      u64* O = cbv.out[s] + (size_t)b * cbv.out_bst + (size_t)p * cbv.out_pst + (size_t)r * N + k0;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) a[j + 16 * k] = tl[17 * k + j];
+      for (int k = 0; k < 16; ++k) {
+        const u32 e = j + 16 * k;
+        u64 v = shoup_mul(sub_mod(A[e], tl[17 * k + j], qi), w, wp, qi);
+        if (ADD) v = add_mod(v, ADD[ga == 1 ? (u32)k0 + e : galois_src((u32)k0 + e, ga, logN)], qi);
+        O[e] = v;
+      }
+    } else {
+      u64* a = blk(z) + (size_t)cc * 256;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) a[j + 16 * k] = tl[17 * k + j];
+    }
     __syncthreads();  // buf[cur] and the transpose tiles are free
     z = zn;
   }
@@ -1079,9 +1096,16 @@ static cudaError_t launch_pair_f64(const NttTables& T, const LimbMap& map, u32 n
     const u32 zper = (nz + zsplit - 1) / zsplit;
     zsplit = (nz + zper - 1) / zper;
     const size_t sm = (2 * kChunkBlock + kChunksPerCta * 16 * 17) * 8;
-    cudaError_t e = ensure_smem((const void*)ntt2_fwd_chunks_f64p<H>, sm);
-    if (e) return e;
-    ntt2_fwd_chunks_f64p<H><<<dim3(gk.x, ny, zsplit), 128, sm, st>>>(map, T.mc, T.ctw, logN, zper, nz);
+    if (map.cb) {
+      cudaError_t e = ensure_smem((const void*)ntt2_fwd_chunks_f64p<H, true>, sm);
+      if (e) return e;
+      ntt2_fwd_chunks_f64p<H, true><<<dim3(gk.x, ny, zsplit), 128, sm, st>>>(map, T.mc, T.ctw, logN, zper, nz, *map.cb);
+    } else {
+      cudaError_t e = ensure_smem((const void*)ntt2_fwd_chunks_f64p<H, false>, sm);
+      if (e) return e;
+      ntt2_fwd_chunks_f64p<H, false><<<dim3(gk.x, ny, zsplit), 128, sm, st>>>(map, T.mc, T.ctw, logN, zper, nz,
+                                                                             NttCombine{});
+    }
     return cudaGetLastError();
   }
   if (!inverse) {
@@ -1154,7 +1178,16 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
     return occ ? launch_pair<true, 1, 2>(T, m, ny, nz, inverse, st) : launch_pair<true, 0, 2>(T, m, ny, nz, inverse, st);
   };
   auto pair = [&](const LimbMap& m, u32 ny, u32 nz) -> cudaError_t {
-    if (!split || !T.small) return one(m, ny, nz, 2);
+    if (!split || !T.small) {
+      LimbMap mm = m;
+      mm.cb = nullptr;
+      cudaError_t err = one(mm, ny, nz, 2);
+      if (!err && m.cb) {
+        err = launch_combine_rows(*m.cb, m.base, m.basis.nq, m.r0 + m.first_limb, ny, nz, T.logN, T.mc, st);
+        g_ntt_extra_launches += 1;
+      }
+      return err;
+    }
     u32 r = 0;
     // launch class of a limb: the FP64 network (class 2) always alone; the
     // integer classes merge into one run-time-dispatch inverse unless split == 1
@@ -1172,7 +1205,16 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
       // class 2: the FP64 network both ways; other classes keep one
       // run-time-dispatch inverse launch unless split == 1
       const int mode = f == 2 ? 3 : f < 0 ? 2 : f;
+      // the fused ModDown combine runs inside the FP64 pipelined chunk pass;
+      // integer-network rows get a plain NTT and the combine kernel after it
+      const bool fuse_here = mm.cb && mode == 3 && !inverse && g_ntt_tuning.pipe;
+      const NttCombine* cb = mm.cb;
+      if (!fuse_here) mm.cb = nullptr;
       cudaError_t err = one(mm, e - r, nz, mode);
+      if (!err && cb && !fuse_here) {
+        err = launch_combine_rows(*cb, m.base, m.basis.nq, mm.r0 + m.first_limb, e - r, nz, T.logN, T.mc, st);
+        g_ntt_extra_launches += 1;
+      }
       if (r > 0) g_ntt_extra_launches += 2;  // launch accounting counts one pair per call
       if (err) return err;
       r = e;

@@ -164,7 +164,8 @@ def _bench16_cts(params, ks):
 
 
 def test_deska_launch_shapes_batched_galois(golden_hashes):
-    """The launch-shape knobs of the TMA key-switch inner product at desk-A
+    """The launch-shape knobs of the key switch at desk-A (TMA inner product
+    shapes, the fused ModDown combine, the pipelined FP64 chunk pass)
     (N=2^13: 32 tiles per limb, so the per-CTA Galois source block and the
     s_in remap for batch entries >= 1 are exercised) with non-trivial
     Galois elements: every variant gives the shipped residues, and entry 0
@@ -182,8 +183,9 @@ def test_deska_launch_shapes_batched_galois(golden_hashes):
     ct2 = ckks.encrypt(ckks.encode(v2, params, L), ks, np.random.default_rng(78))
     batch = ckks.stack([ct1, ct2, ct1, ct2, ct2])
     steps = [1, 8, 64, 2048]
-    defaults = {"ks_tpb": 128, "ks_stages": 3, "ks_tma_min": 2}
-    variants = [{"ks_tpb": 256}, {"ks_stages": 4}, {"ks_tpb": 256, "ks_stages": 4}, {"ks_tma_min": 1}]
+    defaults = {"ks_tpb": 128, "ks_stages": 3, "ks_tma_min": 2, "md_fuse": 0, "ntt_pipe": 1, "ks_tma3": 0}
+    variants = [{"ks_tpb": 256}, {"ks_stages": 4}, {"ks_tpb": 256, "ks_stages": 4}, {"ks_tma_min": 1},
+                {"md_fuse": 1}, {"ntt_pipe": 0}, {"md_fuse": 1, "ks_tma_min": 1}, {"ks_tma3": 1}, {"ks_tma3": 2}]
 
     def run():
         outs = [r.data.clone() for r in ckks.rotate_many(batch, steps, ks)]
