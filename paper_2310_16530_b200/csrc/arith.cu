@@ -16,15 +16,18 @@ namespace hcnn {
 
 // Per-device side stream + fork/join events for kernels that run next to
 // another launch of the same call (created once per device, never freed).
-static cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join) {
-  static std::mutex mu;
+// The caller holds *mu across record-fork / wait / launch / record-join /
+// wait so host threads sharing a device cannot interleave their forks.
+static cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join, std::mutex** mu) {
+  static std::mutex init_mu;
+  static std::mutex use_mu[64];
   static cudaStream_t ss[64] = {};
   static cudaEvent_t ef[64] = {}, ej[64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e) return e;
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  std::lock_guard<std::mutex> lk(mu);
+  std::lock_guard<std::mutex> lk(init_mu);
   if (!ss[dev]) {
     e = cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking);
     if (!e) e = cudaEventCreateWithFlags(&ef[dev], cudaEventDisableTiming);
@@ -34,6 +37,7 @@ static cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* 
   *s = ss[dev];
   *fork = ef[dev];
   *join = ej[dev];
+  *mu = &use_mu[dev];
   return cudaSuccess;
 }
 
@@ -1957,7 +1961,10 @@ cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN
     // join branch of the captured graph)
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
-    const bool par = g_mac3_fork && ff < nq && side_stream(&side, &fork, &join) == cudaSuccess;
+    std::mutex* fmu = nullptr;
+    const bool par = g_mac3_fork && ff < nq && side_stream(&side, &fork, &join, &fmu) == cudaSuccess;
+    std::unique_lock<std::mutex> flk;
+    if (par) flk = std::unique_lock<std::mutex>(*fmu);
     cudaStream_t gst = st;
     if (par) {
       cudaError_t e = cudaEventRecord(fork, st);
