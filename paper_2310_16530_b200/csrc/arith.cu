@@ -42,6 +42,38 @@ static cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* 
 }
 
 
+// 96-bit carry-chain MAC for operands below 2^42 (a = a1 2^32 + a0, m = m1 2^32 + m0,
+// a1, m1 < 2^10): a m = a0 m0 + (a0 m1 + a1 m0) 2^32 + a1 m1 2^64 accumulated as
+// T = lh + mid 2^32 -- 5 IMADs per product instead of the 128-bit product's ~11
+__device__ __forceinline__ void mac96(u64& lh, u64& mid, u32 a0, u32 a1, u32 m0, u32 m1) {
+  asm("{\n\t.reg .u32 lo, hi, ml, mh;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "mov.b64 {ml, mh}, %1;\n\t"
+      "mad.lo.cc.u32 lo, %2, %4, lo;\n\t"
+      "madc.hi.cc.u32 hi, %2, %4, hi;\n\t"
+      "madc.lo.u32 mh, %3, %5, mh;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t"
+      "mov.b64 %1, {ml, mh};\n\t"
+      "mad.wide.u32 %1, %2, %5, %1;\n\t"
+      "mad.wide.u32 %1, %3, %4, %1;\n\t"
+      "}"
+      : "+l"(lh), "+l"(mid)
+      : "r"(a0), "r"(a1), "r"(m0), "r"(m1));
+}
+// T = lh + mid 2^32 (< 2^90) -> T R^-1 mod q
+__device__ __forceinline__ u64 redc96(u64 lh, u64 mid, u64 q, u64 ninv) {
+  const u64 L2 = lh + (mid << 32);
+  const u64 H = (mid >> 32) + (L2 < lh ? 1ull : 0ull);
+  return redc128(H, L2, q, ninv);
+}
+
+// FBC: the 96-bit path for conversions whose sources and target are all below 2^42
+__constant__ bool g_fbc_fast_dev = true;
+cudaError_t set_fbc_fast(int on) {
+  const bool v = on != 0;
+  return cudaMemcpyToSymbol(g_fbc_fast_dev, &v, sizeof(v));
+}
+
 static inline dim3 row_grid(u32 work_per_row, u32 rows, u32 threads) {
   u32 x = (work_per_row + threads - 1) / threads;
   if (x == 0) x = 1;
@@ -362,12 +394,14 @@ __global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, 
   for (u32 e = threadIdx.x; e < nt * NS; e += blockDim.x) s_tm[e] = T.tmat[(size_t)t0 * NS + e];
   for (u32 e = threadIdx.x; e < nt * NM; e += blockDim.x) s_corr[e] = T.corr[(size_t)t0 * NM + e];
   u64 qi[NS], hq[NS], ip[NS], ips[NS];
+  bool src_small = g_fbc_fast_dev;
 #pragma unroll
   for (int i = 0; i < NS; ++i) {
     qi[i] = mc[T.src_mod[i]].q;
     hq[i] = qi[i] >> 1;
     ip[i] = T.inv_punc[i];
     ips[i] = T.inv_punc_sh[i];
+    src_small = src_small && qi[i] < (1ull << 42);
   }
   __syncthreads();
   const u64* src = in + (size_t)b * in_bst + (size_t)z * in_pst;
@@ -389,15 +423,30 @@ __global__ void __launch_bounds__(256) k_fbc_t(const FbcDev* __restrict__ tabs, 
 #pragma unroll 2
     for (u32 t = 0; t < nt; ++t) {
       const u64 qt = s_q[t], ni = s_ninv[t];
-      u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+      u64 v0, v1;
+      if (src_small && qt < (1ull << 42)) {
+        // every operand below 2^42: 96-bit carry-chain sums (5 IMADs per
+        // product, T < 2^87 < q 2^64), the same canonical sum R^-1 mod q
+        u64 L0 = 0, M0 = 0, L1 = 0, M1 = 0;
 #pragma unroll
-      for (int i = 0; i < NS; ++i) {  // NS <= 6 < kLazyTerms
-        const u64 b = s_tm[t * NS + i];
-        mac128_lazy(h0, l0, y0[i], b);
-        mac128_lazy(h1, l1, y1[i], b);
+        for (int i = 0; i < NS; ++i) {
+          const u64 b = s_tm[t * NS + i];
+          mac96(L0, M0, (u32)y0[i], (u32)(y0[i] >> 32), (u32)b, (u32)(b >> 32));
+          mac96(L1, M1, (u32)y1[i], (u32)(y1[i] >> 32), (u32)b, (u32)(b >> 32));
+        }
+        v0 = sub_mod(redc96(L0, M0, qt, ni), s_corr[t * NM + m0], qt);
+        v1 = sub_mod(redc96(L1, M1, qt, ni), s_corr[t * NM + m1], qt);
+      } else {
+        u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {  // NS <= 6 < kLazyTerms
+          const u64 b = s_tm[t * NS + i];
+          mac128_lazy(h0, l0, y0[i], b);
+          mac128_lazy(h1, l1, y1[i], b);
+        }
+        v0 = sub_mod(redc128(h0, l0, qt, ni), s_corr[t * NM + m0], qt);
+        v1 = sub_mod(redc128(h1, l1, qt, ni), s_corr[t * NM + m1], qt);
       }
-      const u64 v0 = sub_mod(redc128(h0, l0, qt, ni), s_corr[t * NM + m0], qt);
-      const u64 v1 = sub_mod(redc128(h1, l1, qt, ni), s_corr[t * NM + m1], qt);
       *reinterpret_cast<ulonglong2*>(dst + s_pos[t] + k) = make_ulonglong2(v0, v1);
     }
   }
@@ -1421,28 +1470,6 @@ __global__ void __launch_bounds__(TPB, MINB > 1 ? MINB : 0) k_mac_multi_tma2(Mac
 // product's ~11, no lazy folds (T < 2^90 < q 2^64 for <= 48 terms), one
 // REDC at the end: the same canonical sum * R^-1 mod q as mac128.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void mac96(u64& lh, u64& mid, u32 a0, u32 a1, u32 m0, u32 m1) {
-  asm("{\n\t.reg .u32 lo, hi, ml, mh;\n\t"
-      "mov.b64 {lo, hi}, %0;\n\t"
-      "mov.b64 {ml, mh}, %1;\n\t"
-      "mad.lo.cc.u32 lo, %2, %4, lo;\n\t"
-      "madc.hi.cc.u32 hi, %2, %4, hi;\n\t"
-      "madc.lo.u32 mh, %3, %5, mh;\n\t"
-      "mov.b64 %0, {lo, hi};\n\t"
-      "mov.b64 %1, {ml, mh};\n\t"
-      "mad.wide.u32 %1, %2, %5, %1;\n\t"
-      "mad.wide.u32 %1, %3, %4, %1;\n\t"
-      "}"
-      : "+l"(lh), "+l"(mid)
-      : "r"(a0), "r"(a1), "r"(m0), "r"(m1));
-}
-// T = lh + mid 2^32 (< 2^90) -> T R^-1 mod q
-__device__ __forceinline__ u64 redc96(u64 lh, u64 mid, u64 q, u64 ninv) {
-  const u64 L2 = lh + (mid << 32);
-  const u64 H = (mid >> 32) + (L2 < lh ? 1ull : 0ull);
-  return redc128(H, L2, q, ninv);
-}
-
 template <int ST, int TPB, bool FAST>
 __global__ void __launch_bounds__(TPB + 32) k_mac_multi_tma3(MacMulti M, int ng, int nt, u32 nq, u32 logN, u32 r0,
                                                              int accumulate, const ModConsts* __restrict__ mc) {

@@ -35,6 +35,7 @@ extern int g_mac_batch;
 extern int g_mac_lanes;
 extern int g_mac_async;
 extern int g_mac_tma;
+cudaError_t set_fbc_fast(int on);  // 96-bit FBC sums for all-small conversions (default on)
 extern int g_ks_tma3;
 extern int g_ks3_stages;
 extern int g_mac3_stages;
