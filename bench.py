@@ -349,13 +349,20 @@ def run_resnet20(args, cl):
     # eager runs first (mask build, measured residency fill, lazy tables;
     # then one event-profiled image for the kernel table / roofline / launch
     # count), then capture -- so the capture pool reuses the eager memory
-    warm = workloads.warm_up(s, imgs, cache)
+    # --batch-mode stack (default): the B images of a step are stacked into
+    # [B, 2, l+1, N] ciphertexts and the executor runs ONCE for all of them
+    # (graph.stack_images: every kernel covers the B images, bootstraps
+    # included; each image's residues equal its single-image run);
+    # lockstep: graph.execute_many (per-image layers, shared bootstraps)
+    stacked = B > 1 and args.batch_mode == "stack"
+    units = [graph.stack_images(imgs)] if stacked else imgs
+    warm = workloads.warm_up(s, units, cache)
     k0 = _native.kernel_launches()
     _native.profile_read(reset=True)
     _native.ntt_limb_counts(reset=True)
     _native.ks_counters(reset=True)
     _native.profile_enable(True)
-    graph.execute_many(s.graph, s.plan, imgs, s.ks, cache=cache)
+    graph.execute_many(s.graph, s.plan, units, s.ks, cache=cache)
     torch.cuda.synchronize()
     _native.profile_enable(False)
     prof = _native.profile_read(reset=True)
@@ -365,14 +372,13 @@ def run_resnet20(args, cl):
     roofline, kernels = roofline_from_profile(prof)
     roofline = int_roofline(roofline, prof, limbs, s.params.n)
     ks_roof = keyswitch_roofline(prof, ksc, s.params.n)
-    # all B images of a step in one captured graph (graph.execute_many:
-    # their refresh points bootstrap as one batch)
-    runner = graph.CapturedInference(s.graph, s.plan, s.ks, imgs[0], cache, warmup=False, images=B)
+    # all B images of a step in one captured graph
+    runner = graph.CapturedInference(s.graph, s.plan, s.ks, units[0], cache, warmup=False, images=len(units))
     per_layer = _layer_rows(runner.report.per_layer)
     tally = runner.report.totals().as_dict()
 
     def step():
-        runner.run_many(imgs)
+        runner.run_many(units)
 
     for _ in range(args.warmup):
         step()
@@ -385,7 +391,7 @@ def run_resnet20(args, cl):
     value = B * cl.world / (ms_step / 1e3)
 
     # e2e: every step's encrypted inputs from pinned host memory, encrypted logits back
-    host_in = [[ct.data.to("cpu").pin_memory() for ct in im.cts] for im in imgs]
+    host_in = [[ct.data.to("cpu").pin_memory() for ct in im.cts] for im in units]
     host_out = [torch.empty(o.data.shape, dtype=torch.int64).pin_memory() for o in runner.outs]
     h2d = sum(t.numel() * 8 for src in host_in for t in src)
 
@@ -404,11 +410,13 @@ def run_resnet20(args, cl):
     e2e = {"value": B * cl.world / (ms_e2e / args.steps / 1e3), "unit": "images/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": sum(h.numel() * 8 for h in host_out)}
     out_ct = runner.out
+    # one host logits tensor per image (the last e2e step's copies)
+    per_image_out = [h[b] for h in host_out for b in range(h.shape[0])] if stacked else host_out
 
     # correctness of the measured path: decrypt each of this rank's replayed
-    # logits (the last e2e step's host copies) against the float mirror
+    # logits against the float mirror
     checks = []
-    for i, x, hout in zip(mine, raw, host_out):
+    for i, x, hout in zip(mine, raw, per_image_out):
         ct = ckks.Ciphertext(hout.to(s.params.ctx.torch_device), out_ct.scale, out_ct.n, s.params)
         lg = packing.read_logits(ct, s.graph.n_classes, s.graph.formats[-1], s.ks)
         pl, _ = graph.execute(s.graph, s.plan, x, mode="plaintext-ref")
@@ -443,7 +451,7 @@ def run_resnet20(args, cl):
             "logits_check": {"images": len(flat), "max_rel_err_vs_plaintext": max(c["rel_err"] for c in flat),
                              "max_abs_err_vs_plaintext": max(c["max_abs_err"] for c in flat),
                              "argmax_agree": all(c["argmax_agree"] for c in flat)},
-            "setup": warm,
+            "setup": warm, "batch_mode": (args.batch_mode if B > 1 else None),
             "vs_baseline_note": "paper A100 1402 ms / our s per image (PAPER.md:189)",
         }
         print(json.dumps(line), flush=True)
@@ -665,6 +673,8 @@ def main():
     ap.add_argument("--batch", type=int, default=8, help="cfg2: ciphertext pairs per step")
     ap.add_argument("--boot-batch", type=int, default=1, help="boot16: ciphertexts bootstrapped per step")
     ap.add_argument("--images-per-gpu", type=int, default=1, help="resnet20: images per GPU per step")
+    ap.add_argument("--batch-mode", default="stack", choices=["stack", "lockstep"],
+                    help="resnet20, B > 1: stacked image batches (one executor pass) or execute_many")
     ap.add_argument("--workload", default="resnet20", choices=["resnet20", "cfg2", "boot16", "selftest"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -255,6 +255,19 @@ class DeviceContext:
         """outs[g] (+)= sum_t cts[t] (.) masks[g][t] (None: no term), one ciphertext read per 4 outputs.
         A mask may be an int64 [l+1, N] Montgomery row tensor or a uint8 packed mask (pack_masks)."""
         G, T = len(masks), len(cts)
+        if T and cts[0].dim() == 4:
+            # image batches [B, 2, l+1, N] sharing the masks (ckks.image_batched):
+            # one launch set per image
+            B = int(cts[0].shape[0])
+            for c in cts:
+                if not c.is_contiguous() or c.shape != (B, 2, level + 1, self.n):
+                    raise BasisError("mac_terms_multi image batches must be contiguous [B, 2, l+1, N]")
+            if outs is None:
+                outs = [self.empty(B, 2, level + 1, self.n) for _ in range(G)]
+            for b in range(B):
+                self.mac_terms_multi([c[b] for c in cts], masks, level, outs=[o[b] for o in outs],
+                                     accumulate=accumulate)
+            return list(outs)
         for c in cts:
             if not c.is_contiguous() or c.shape != (2, level + 1, self.n):
                 raise BasisError("mac_terms_multi ciphertexts must be contiguous [2, l+1, N]")

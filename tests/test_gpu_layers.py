@@ -94,3 +94,28 @@ def test_execute_many_matches_single_images(golden_hashes):
         assert rep.totals().as_dict() == rep1.totals().as_dict()
         assert all(torch.equal(a.data, b.data) for a, b in zip(out.cts, one.cts))
     assert h(_cts(many[0][0].cts)) != h(_cts(many[1][0].cts))
+
+
+def test_stacked_images_match_single_images(golden_hashes):
+    """graph.stack_images: ciphertexts holding B images ([B, 2, l+1, N]) run
+    through the executor once (bench.py --images-per-gpu B, batch-mode
+    stack); every image's residues and tally equal its single-image run."""
+    import torch
+    from paper_2310_16530_b200 import ckks, graph, packing
+    gold = golden_hashes["layers"]["block"]
+    params = ckks.desk_a()
+    fx = graph.gen_fixture("basic-block-stack(1)", 21, params)
+    g = graph.build_graph("basic-block-stack(1)", fx, multiplex=8)
+    steps = sorted(graph.required_rotation_steps(g, params.slots))
+    ks = ckks.keygen(params, np.random.default_rng(gold["key_seed"]), rotations=steps)
+    plan = graph.plan_levels(g, params.max_level)
+    rng = np.random.default_rng(6)
+    xs = [packing.encrypt_tensor(rng.uniform(-1, 1, (8, 8, 8)), g.input_format, ks, rng, plan.entry_levels[0])
+          for _ in range(3)]
+    cache: dict = {}
+    out, rep = graph.execute(g, plan, graph.stack_images(xs), ks, "encrypted", cache=cache)
+    assert ckks.image_batch() == 1  # the image-batch context is scoped to the call
+    for x, o in zip(xs, graph.unstack_images(out)):
+        one, rep1 = graph.execute(g, plan, x, ks, "encrypted", cache=cache)
+        assert rep.totals().as_dict() == rep1.totals().as_dict()
+        assert all(torch.equal(a.data, b.data) for a, b in zip(o.cts, one.cts))

@@ -72,6 +72,13 @@ def r20_bench():
         out, rep = graph.execute(s.graph, s.plan, im, s.ks, "encrypted", cache=cache)
         eager.append((out.data.clone(), out.scale, out.level))
     tally = rep.totals().as_dict()
+    # two images stacked into [2, 2, l+1, N] ciphertexts through one executor
+    # pass (bench.py --images-per-gpu 2): bootstraps included, each image
+    # must equal its single-image run
+    sout, srep = graph.execute(s.graph, s.plan, graph.stack_images(imgs[:2]), s.ks, "encrypted", cache=cache)
+    stacked = [(o.data.clone(), o.scale, o.level) for o in graph.unstack_images(sout)]
+    stacked_tally = srep.totals().as_dict()
+    del sout
     runner = graph.CapturedInference(s.graph, s.plan, s.ks, imgs[0], cache, warmup=False)
     replay = []
     for im in imgs:
@@ -82,6 +89,7 @@ def r20_bench():
                                   s.graph.formats[-1], s.ks) for d, sc, _ in replay]
     plain = [graph.execute(s.graph, s.plan, x, mode="plaintext-ref")[0] for x in raw]
     res = {"eager": eager, "replay": replay, "logits": logits, "plain": plain, "tally": tally,
+           "stacked": stacked, "stacked_tally": stacked_tally,
            "runner_tally": runner.report.totals().as_dict(),
            "per_layer": [{"name": r["name"], "kind": r["kind"], "tally": r["tally"], "entry_level": r["entry_level"]}
                          for r in runner.report.per_layer]}
@@ -96,6 +104,17 @@ def test_replay_equals_eager(r20_bench):
     for (de, se, le), (dr, sr, lr) in zip(r20_bench["eager"], r20_bench["replay"]):
         assert le == lr and se == sr
         assert torch.equal(de, dr), "CUDA-graph replay differs from eager execution"
+
+
+def test_stacked_images_equal_single_runs(r20_bench):
+    """ResNet20 at N=2^16 with real bootstrapping, two images stacked into
+    [2, 2, l+1, N] ciphertexts: each image's encrypted logits are bit-identical
+    to its single-image run (bootstrapping is entry-wise in a batch)."""
+    import torch
+    assert r20_bench["stacked_tally"] == r20_bench["tally"]
+    for (ds, ss, ls), (de, se, le) in zip(r20_bench["stacked"], r20_bench["eager"][:2]):
+        assert ls == le and ss == se
+        assert torch.equal(ds, de)
 
 
 def test_committed_tally_matches_executor(r20_bench):
