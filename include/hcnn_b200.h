@@ -153,6 +153,14 @@ int hcnn_mac_terms_multi(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* c
 int hcnn_mac_terms_multi_packed(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* const* cts,
                                 const uint64_t* const* masks_mont, const unsigned char* packed, uint32_t n_out,
                                 uint32_t n_terms, uint32_t level, int accumulate, void* stream);
+/* hcnn_mac_terms_multi_packed over image batches (no reference counterpart:
+ * the reference runs one image at a time): cts[t] and outs[g] each hold
+ * n_images (1 or 2) ciphertexts 2 (level+1) N words apart that share every
+ * mask; each mask tile is read once for both images.  Per image the residues
+ * equal hcnn_mac_terms_multi_packed's. */
+int hcnn_mac_terms_multi_images(hcnn_ctx* ctx, uint64_t* const* outs, const uint64_t* const* cts,
+                                const uint64_t* const* masks, const unsigned char* packed, uint32_t n_out,
+                                uint32_t n_terms, uint32_t level, uint32_t n_images, int accumulate, void* stream);
 /* Resident mask compaction: n_masks Montgomery rows [n][level+1][N] ->
  * (8 + 4 level + sum_r hb_r) N bytes each: limb 0 as u64, limbs 1.. as u32
  * low-word planes, then one high plane per limb, u8 when q_r < 2^40 and u16

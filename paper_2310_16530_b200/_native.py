@@ -72,6 +72,8 @@ SIGNATURES = {
                                     _U32, _INT, _VP]),
     "hcnn_mac_terms_multi_packed": (_INT, [_VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), ctypes.POINTER(_VP),
                                            ctypes.POINTER(ctypes.c_ubyte), _U32, _U32, _U32, _INT, _VP]),
+    "hcnn_mac_terms_multi_images": (_INT, [_VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), ctypes.POINTER(_VP),
+                                           ctypes.POINTER(ctypes.c_ubyte), _U32, _U32, _U32, _U32, _INT, _VP]),
     "hcnn_pack_masks": (_INT, [_VP, _VP, _VP, _U32, _U32, _VP]),
     "hcnn_unpack_mask": (_INT, [_VP, _VP, _VP, _U32, _VP]),
     "hcnn_mac_terms_batch": (_INT, [_VP, _VP, ctypes.POINTER(_VP), ctypes.POINTER(_VP), _U32, _U32, _U32, _INT,

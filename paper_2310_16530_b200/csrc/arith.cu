@@ -1579,6 +1579,136 @@ __global__ void __launch_bounds__(TPB + 32) k_mac_multi_tma3(MacMulti M, int ng,
 }
 
 // ---------------------------------------------------------------------------
+// k_mac_multi_img2: k_mac_multi_tma3 over two images that share every mask
+// (image-batched execution, graph.stack_images): per term the producer warp
+// bulk-copies both images' ciphertext tiles and each output's mask tile
+// ONCE; 256 consumer threads (one coefficient each) accumulate the two
+// images' sums with 96-bit carry chains.  Rows with q < 2^42 only (the
+// generic limb-0 rows run as two single-image launches).
+// ---------------------------------------------------------------------------
+struct MacStage2 {
+  u64 ct[2][2][kMacTile];        // [image][poly][coefficient]
+  u64 mask[kMultiG][kMacTile];
+};
+
+__device__ __forceinline__ void mac_stage_bulk2(MacStage2& S, u64* bar, const MacMulti& M, int t, u32 fl, u32 r,
+                                                u32 nq, u32 N, u32 k0) {
+  const size_t off = (size_t)r * N + k0, pst = (size_t)nq * N;
+  u32 bytes = 4 * kMacTile * 8;
+  const u32 pk = kMacTile * (4 + packed_hb(r, M.wide));
+  for (int g = 0; g < kMultiG; ++g)
+    if (fl >> g & 1u) bytes += (fl >> (4 + g) & 1u) ? pk : kMacTile * 8;
+  mbar_expect_tx(bar, bytes);
+  for (int b = 0; b < 2; ++b) {
+    const u64* c = M.ct[t] + (size_t)b * M.img_stride;
+    bulk_g2s(S.ct[b][0], c + off, kMacTile * 8, bar);
+    bulk_g2s(S.ct[b][1], c + pst + off, kMacTile * 8, bar);
+  }
+  for (int g = 0; g < kMultiG; ++g) {
+    if (!(fl >> g & 1u)) continue;
+    const u64* mp = M.mask[g][t];
+    if (fl >> (4 + g) & 1u) {
+      const char* bb = reinterpret_cast<const char*>(mp);
+      char* dst = reinterpret_cast<char*>(S.mask[g]);
+      const unsigned hb = packed_hb(r, M.wide);
+      bulk_g2s(dst, bb + 8 * (size_t)N + 4 * ((size_t)(r - 1) * N + k0), kMacTile * 4, bar);
+      bulk_g2s(dst + kMacTile * 4, bb + packed_hi_off(r, nq, N, M.wide) + (size_t)hb * k0, kMacTile * hb, bar);
+    } else {
+      bulk_g2s(S.mask[g], M.packed[g][t] ? mp + k0 : mp + off, kMacTile * 8, bar);
+    }
+  }
+}
+
+template <int ST>
+__global__ void __launch_bounds__(kMacTile + 32, 2) k_mac_multi_img2(MacMulti M, int ng, int nt, u32 nq, u32 logN,
+                                                                  u32 r0, int accumulate,
+                                                                  const ModConsts* __restrict__ mc) {
+  constexpr int NW = kMacTile / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MacStage2* S = reinterpret_cast<MacStage2*>(smem_raw);
+  __shared__ __align__(8) u64 full[ST];
+  __shared__ __align__(8) u64 empty[ST];
+  __shared__ unsigned char flags[kMultiT];
+  const u32 N = 1u << logN, r = blockIdx.y + r0, k0 = blockIdx.x * kMacTile, tid = threadIdx.x;
+  const u64 q = mc[r].q, ninv = mc[r].ninv;
+  const unsigned hb = packed_hb(r, M.wide);
+  for (u32 i = tid; i < (u32)nt; i += kMacTile + 32) {
+    u32 fl = 0;
+    for (int g = 0; g < ng; ++g)
+      if (M.mask[g][i]) fl |= (1u << g) | (M.packed[g][i] ? (16u << g) : 0u);
+    flags[i] = (unsigned char)fl;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= (u32)kMacTile) {  // producer warp
+    if (tid == (u32)kMacTile) {
+      for (int t = 0; t < nt; ++t) {
+        const int slot = t % ST;
+        if (t >= ST) mbar_wait(&empty[slot], (u32)(t / ST - 1) & 1u);
+        mac_stage_bulk2(S[slot], &full[slot], M, t, flags[t], r, nq, N, k0);
+      }
+    }
+    return;
+  }
+  u64 AL[kMultiG][2][2], AH[kMultiG][2][2];  // [output][image][poly]
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) AL[g][b][0] = AL[g][b][1] = AH[g][b][0] = AH[g][b][1] = 0;
+  for (int t = 0; t < nt; ++t) {
+    const int slot = t % ST;
+    const u32 fl = flags[t];
+    mbar_wait(&full[slot], (u32)(t / ST) & 1u);
+    const MacStage2& C = S[slot];
+    u64 x[2][2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      x[b][0] = C.ct[b][0][tid];
+      x[b][1] = C.ct[b][1][tid];
+    }
+#pragma unroll
+    for (int g = 0; g < kMultiG; ++g) {
+      if (!(fl >> g & 1u)) continue;
+      u32 m0, m1;
+      if (fl >> (4 + g) & 1u) {
+        m0 = reinterpret_cast<const unsigned*>(C.mask[g])[tid];
+        m1 = (u32)packed_hi(reinterpret_cast<const unsigned char*>(C.mask[g]) + kMacTile * 4, tid, hb);
+      } else {
+        const u64 m = C.mask[g][tid];
+        m0 = (u32)m;
+        m1 = (u32)(m >> 32);
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int p = 0; p < 2; ++p) mac96(AL[g][b][p], AH[g][b][p], (u32)x[b][p], (u32)(x[b][p] >> 32), m0, m1);
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
+  }
+  const size_t pst = (size_t)nq * N, off = (size_t)r * N + k0 + tid;
+#pragma unroll
+  for (int g = 0; g < kMultiG; ++g) {
+    if (g >= ng) break;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        u64* d = M.out[g] + (size_t)b * M.img_stride + p * pst + off;
+        u64 y = redc96(AL[g][b][p], AH[g][b][p], q, ninv);
+        if (accumulate) y = add_mod(y, *d, q);
+        *d = y;
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Key-switch inner product with TMA-staged operands.  A CTA owns one
 // 256-coefficient tile of one output limb r for up to kKsEntries batch
 // entries; per digit j one elected thread bulk-copies the two key rows'
@@ -1969,6 +2099,36 @@ int g_mac_lanes = 1;  // 1: k_mac_multi_lanes, 0: register-blocked k_mac_multi
 cudaError_t launch_mac_multi(const MacMulti& M, int ng, int nt, u32 nq, u32 logN, int accumulate,
                              const ModConsts* mc, cudaStream_t st) {
   if (ng < 1 || ng > kMultiG) return cudaErrorInvalidValue;
+  if (M.nimg == 2) {
+    // two images sharing the masks: FAST rows in one k_mac_multi_img2 launch,
+    // the generic rows (limb 0) as one single-image launch per image
+    if ((1u << logN) % kMacTile || nt > kMultiT) return cudaErrorInvalidValue;
+    const u32 ff = M.fast_from < 1 ? 1 : (M.fast_from > nq ? nq : M.fast_from);
+    for (int b = 0; b < 2; ++b) {
+      MacMulti M1 = M;
+      M1.nimg = 1;
+      M1.fast_from = nq;  // every row generic in this helper call: only rows < ff are launched below
+      for (int t = 0; t < nt; ++t) M1.ct[t] = M.ct[t] + (size_t)b * M.img_stride;
+      for (int g = 0; g < kMultiG; ++g) M1.out[g] = M.out[g] ? M.out[g] + (size_t)b * M.img_stride : nullptr;
+      const size_t sm = sizeof(MacStage) * 3;
+      cudaError_t e = ensure_smem((const void*)k_mac_multi_tma3<3, 128, false>, sm);
+      if (e) return e;
+      k_mac_multi_tma3<3, 128, false><<<dim3((1u << logN) / kMacTile, ff, 1), 160, sm, st>>>(M1, ng, nt, nq, logN, 0,
+                                                                                           accumulate, mc);
+      e = cudaGetLastError();
+      if (e) return e;
+    }
+    if (ff < nq) {
+      constexpr int ST = 3;
+      const size_t sm = sizeof(MacStage2) * ST;
+      cudaError_t e = ensure_smem((const void*)k_mac_multi_img2<ST>, sm);
+      if (e) return e;
+      k_mac_multi_img2<ST><<<dim3((1u << logN) / kMacTile, nq - ff, 1), kMacTile + 32, sm, st>>>(
+          M, ng, nt, nq, logN, ff, accumulate, mc);
+      return cudaGetLastError();
+    }
+    return cudaSuccess;
+  }
   if (g_mac_tma == 3 && (1u << logN) % kMacTile == 0 && nt <= kMultiT) {
     // rows [0, fast_from): generic 128-bit MACs; [fast_from, nq): 96-bit carry chains
     const int stages = g_mac3_stages, tpb = g_mac3_tpb;

@@ -116,6 +116,8 @@ struct MacMulti {
   u64* out[kMultiG];
   unsigned char packed[kMultiG][kMultiT];  // 1: mask in the packed layout (launch_pack_masks)
   unsigned fast_from;  // limbs r >= fast_from (>= 1) have q < 2^42: 96-bit carry-chain MACs (k_mac_multi_tma3)
+  unsigned nimg;       // image batches: ct[t] / out[g] hold nimg images img_stride apart (1: single)
+  size_t img_stride;
   unsigned long long wide;                 // packed layout: bit r set = limb r needs a 16-bit high plane
 };
 // Packed resident masks: limb 0 as u64 [N]; limbs 1..nq-1 as u32 low words

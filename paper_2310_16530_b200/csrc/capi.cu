@@ -1241,20 +1241,31 @@ int hcnn_mac_terms_multi(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* con
 int hcnn_mac_terms_multi_packed(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* const* cts,
                                 const uint64_t* const* masks, const unsigned char* packed, uint32_t n_out,
                                 uint32_t n_terms, uint32_t level, int accumulate, void* s) {
+  return hcnn_mac_terms_multi_images(c, outs, cts, masks, packed, n_out, n_terms, level, 1, accumulate, s);
+}
+
+int hcnn_mac_terms_multi_images(hcnn_ctx* c, uint64_t* const* outs, const uint64_t* const* cts,
+                                const uint64_t* const* masks, const unsigned char* packed, uint32_t n_out,
+                                uint32_t n_terms, uint32_t level, uint32_t n_images, int accumulate, void* s) {
   if (!c) return fail(HCNN_E_PARAMETER, "null context");
   if (level >= c->Lq) return fail(HCNN_E_LEVEL, "level outside chain");
+  if (n_images != 1 && n_images != 2) return fail(HCNN_E_PARAMETER, "n_images must be 1 or 2");
+  if (n_images == 2 && c->n % 256) return fail(HCNN_E_PARAMETER, "two-image MAC needs N % 256 == 0");
   const u32 nq = level + 1;
   for (u32 g0 = 0; g0 < n_out; g0 += kMultiG) {
     const u32 ng = std::min<u32>(kMultiG, n_out - g0);
     if (n_terms == 0) {
       if (!accumulate)
-        for (u32 g = 0; g < ng; ++g) CK(cudaMemsetAsync(outs[g0 + g], 0, 2ull * nq * c->n * 8, STREAM(s)));
+        for (u32 g = 0; g < ng; ++g)
+          CK(cudaMemsetAsync(outs[g0 + g], 0, 2ull * n_images * nq * c->n * 8, STREAM(s)));
       continue;
     }
     for (u32 t0 = 0; t0 < n_terms; t0 += kMultiT) {
       const u32 nt = std::min<u32>(kMultiT, n_terms - t0);
       MacMulti M;
       M.wide = c->wide;
+      M.nimg = n_images;
+      M.img_stride = 2ull * nq * c->n;
       M.fast_from = nq;
       while (M.fast_from > 1 && c->mods[M.fast_from - 1] < (1ull << 42)) --M.fast_from;
       for (u32 t = 0; t < nt; ++t) M.ct[t] = cts[t0 + t];
@@ -1270,7 +1281,8 @@ int hcnn_mac_terms_multi_packed(hcnn_ctx* c, uint64_t* const* outs, const uint64
           used += M.mask[g][t] ? (M.packed[g][t] ? pf : 1.0) : 0.0;
         }
       }
-      PK("mac_multi", 8.0 * (2.0 * nt + used + 2.0 * ng * (accumulate || t0 ? 2 : 1)) * nq * c->n, 1, STREAM(s),
+      PK("mac_multi", 8.0 * (2.0 * nt * n_images + used + 2.0 * ng * n_images * (accumulate || t0 ? 2 : 1)) * nq * c->n,
+         n_images == 2 ? 3 : 1, STREAM(s),
          launch_mac_multi(M, (int)ng, (int)nt, nq, c->logN, accumulate || t0 > 0, c->d_mc, STREAM(s)));
     }
   }

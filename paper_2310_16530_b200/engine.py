@@ -264,25 +264,36 @@ class DeviceContext:
                     raise BasisError("mac_terms_multi image batches must be contiguous [B, 2, l+1, N]")
             if outs is None:
                 outs = [self.empty(B, 2, level + 1, self.n) for _ in range(G)]
-            for b in range(B):
-                self.mac_terms_multi([c[b] for c in cts], masks, level, outs=[o[b] for o in outs],
-                                     accumulate=accumulate)
+            b = 0
+            while b < B:
+                if b + 1 < B and self.n % 256 == 0:  # two images per launch: each mask tile read once for both
+                    self._mac_multi_call([c[b] for c in cts], masks, level, [o[b] for o in outs], accumulate, 2)
+                    b += 2
+                else:
+                    self._mac_multi_call([c[b] for c in cts], masks, level, [o[b] for o in outs], accumulate, 1)
+                    b += 1
             return list(outs)
         for c in cts:
             if not c.is_contiguous() or c.shape != (2, level + 1, self.n):
                 raise BasisError("mac_terms_multi ciphertexts must be contiguous [2, l+1, N]")
         if outs is None:
             outs = [self.empty(2, level + 1, self.n) for _ in range(G)]
+        self._mac_multi_call(cts, masks, level, outs, accumulate, 1)
+        return list(outs)
+
+    def _mac_multi_call(self, cts, masks, level, outs, accumulate, n_images):
+        """hcnn_mac_terms_multi_images; with n_images = 2, cts[t] / outs[g] are
+        the first of two images stored back to back."""
+        G, T = len(masks), len(cts)
         P = ctypes.c_void_p
         flat = [m for row in masks for m in row]
         ptrs = [(m.data_ptr() if m is not None else None) for m in flat]
         packed = [1 if (m is not None and m.dtype == torch.uint8) else 0 for m in flat]
         pk = (ctypes.c_ubyte * max(len(packed), 1))(*packed) if any(packed) else None
-        self._chk(self.lib.hcnn_mac_terms_multi_packed(self.handle, (P * max(G, 1))(*[o.data_ptr() for o in outs]),
+        self._chk(self.lib.hcnn_mac_terms_multi_images(self.handle, (P * max(G, 1))(*[o.data_ptr() for o in outs]),
                                                        (P * max(T, 1))(*[c.data_ptr() for c in cts]),
-                                                       (P * max(G * T, 1))(*ptrs), pk, G, T, level,
+                                                       (P * max(G * T, 1))(*ptrs), pk, G, T, level, n_images,
                                                        1 if accumulate else 0, _stream()))
-        return list(outs)
 
     def packed_mask_bytes(self, level: int) -> int:
         """limb 0 as u64, limbs 1..level as u32 low words + a u8 (q < 2^40) or u16 high plane"""

@@ -26,7 +26,9 @@ def main(level: int = 10, T: int = 36, G: int = 4, settings=("mac_tma=3",)):
         return torch.from_numpy(np.stack([np.stack([rng.integers(0, q, params.n, dtype=np.uint64) for q in qs])
                                           for _ in range(k)]).view(np.int64)).to(ctx.torch_device)
 
-    cts = [rows(2) for _ in range(T)]
+    images = int(os.environ.get("MAC_PROBE_IMAGES", "1"))
+    cts = [rows(2) for _ in range(T)] if images == 1 else \
+        [torch.stack([rows(2) for _ in range(images)]).contiguous() for _ in range(T)]
     packed = os.environ.get("MAC_PROBE_UNPACKED") is None
     masks = [[ctx.pack_masks(rows(1), level)[0] if packed else rows(1)[0] for _ in range(T)] for _ in range(G)]
     ref = None
@@ -57,8 +59,8 @@ def main(level: int = 10, T: int = 36, G: int = 4, settings=("mac_tma=3",)):
         ms = sorted(runs)[len(runs) // 2]
         lb = params.n * 8
         mb = ctx.packed_mask_bytes(level) if packed else (level + 1) * lb
-        alg = (2 * T * (level + 1) * lb + G * T * mb + 2 * G * (level + 1) * lb)
-        print(f"{st} mac_multi T={T} G={G} level={level}: {ms:.4f} ms, {alg / ms / 1e6:.1f} GB/s algorithmic (median of {len(runs)}, "
+        alg = (2 * T * images * (level + 1) * lb + G * T * mb + 2 * G * images * (level + 1) * lb)
+        print(f"{st} images={images} mac_multi T={T} G={G} level={level}: {ms:.4f} ms, {alg / ms / 1e6:.1f} GB/s algorithmic (median of {len(runs)}, "
               f"min {min(runs):.4f}), bit_identical={same}", flush=True)
         assert same
 
