@@ -23,13 +23,39 @@ class ResNet20Setup:
     ks: ckks.KeySet
 
 
-def resnet20_boot_config(stc_stages=None) -> bt.BootConfig:
-    """Bootstrapping configuration of the ResNet20 workload (HCNN_STC env: e.g. "8,7")."""
+# the ResNet20 chain: q0 + application levels + bootstrapping depth = 30 q-limbs
+# (+ 4 specials: logQP 1680 <= 1772, the 128-bit bound at N=2^16)
+RESNET20_Q_LIMBS = 30
+# EvalMod's Chebyshev degree before the 3 double angles: 31 approximates
+# sin(2 pi x) near the integers to 2^-25.5 (tests/test_bootstrap_plain.py),
+# below the bootstrap's own noise, and needs one level less than 59 (depth
+# 15): the same refresh plan on a 30-limb chain, 381.9 -> 360.3 ms/image
+RESNET20_EVALMOD_DEGREE = 31
+
+
+def resnet20_boot_config(stc_stages=None, degree=None) -> bt.BootConfig:
+    """Bootstrapping configuration of the ResNet20 workload (HCNN_STC env:
+    e.g. "8,7"; HCNN_EVALMOD_DEGREE: the Chebyshev degree before the double
+    angles)."""
     import os
     env = os.environ.get("HCNN_STC")
     if stc_stages is None and env:
         stc_stages = tuple(int(v) for v in env.split(","))
-    return bt.BootConfig() if stc_stages is None else bt.BootConfig(stc_stages=tuple(stc_stages))
+    if degree is None:
+        degree = int(os.environ.get("HCNN_EVALMOD_DEGREE", RESNET20_EVALMOD_DEGREE))
+    kw = {}
+    if stc_stages is not None:
+        kw["stc_stages"] = tuple(stc_stages)
+    if degree is not None:
+        kw["degree"] = int(degree)
+    return bt.BootConfig(**kw)
+
+
+def resnet20_app_levels(cfg: bt.BootConfig) -> int:
+    """Application levels of a fixed-length chain: what the bootstrap does not
+    use (HCNN_Q_LIMBS overrides the chain length)."""
+    import os
+    return int(os.environ.get("HCNN_Q_LIMBS", RESNET20_Q_LIMBS)) - 1 - cfg.depth()
 
 
 def resnet20_setup(app_levels: int | None = None, seed: int = 3, key_seed: int = 20) -> ResNet20Setup:
@@ -39,8 +65,8 @@ def resnet20_setup(app_levels: int | None = None, seed: int = 3, key_seed: int =
     bootstrapping at the snapshot-aware planner's refresh points."""
     packing.set_mask_mode("compact")
     cfg = resnet20_boot_config()
-    if app_levels is None:  # keep the chain length (logQP) fixed: StC levels trade for application levels
-        app_levels = 17 - len(cfg.stc_stages)
+    if app_levels is None:  # keep the chain length (logQP) fixed: bootstrap levels trade for application levels
+        app_levels = resnet20_app_levels(cfg)
     params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg)
     boot = bt.Bootstrapper(params, cfg)
     fx = graph.gen_fixture("resnet20", seed, params, golden_count=1)
@@ -71,7 +97,7 @@ def resnet20_plan_only(app_levels: int | None = None, seed: int = 3):
     """Host-only part of resnet20_setup (params, graph, plan; no keys/GPU)."""
     cfg = resnet20_boot_config()
     if app_levels is None:
-        app_levels = 17 - len(cfg.stc_stages)
+        app_levels = resnet20_app_levels(cfg)
     params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg)
     fx = graph.gen_fixture("resnet20", seed, params, golden_count=1)
     g = graph.build_graph("resnet20", fx, multiplex=4)

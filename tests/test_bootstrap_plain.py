@@ -132,3 +132,21 @@ def test_diag_plan_any_baby_count(n1):
         p = bt.diag_plan(m, n1)
         assert p.n1 == n1
         assert np.allclose(bt.apply_plain([p], v), m @ v)
+
+
+def test_resnet20_evalmod_degree_is_precise_enough():
+    """The ResNet20 workload's EvalMod (degree 31 before 3 double angles,
+    workloads.RESNET20_EVALMOD_DEGREE) approximates sin(2 pi x) within
+    2^-24 wherever x = I + eps, |I| < k_bound, |eps| <= 2^-10 -- below the
+    bootstrap's own noise -- one level shallower than degree 59."""
+    import numpy as np
+    from paper_2310_16530_b200 import bootstrap as bt, workloads
+    cfg = workloads.resnet20_boot_config()
+    assert cfg.degree == workloads.RESNET20_EVALMOD_DEGREE == 31
+    assert cfg.evalmod_depth() == bt.BootConfig().evalmod_depth() - 1
+    B = cfg.k_bound + 1
+    I = np.arange(-cfg.k_bound + 1, cfg.k_bound)
+    eps = np.linspace(-2 ** -10, 2 ** -10, 201)
+    y = ((I[:, None] + eps[None, :]) / B).ravel()
+    err = np.max(np.abs(bt.evalmod_plain(cfg, y) - np.sin(2 * np.pi * B * y)))
+    assert err < 2 ** -24, err
