@@ -24,7 +24,7 @@ class ResNet20Setup:
 
 
 # the ResNet20 chain: q0 + application levels + bootstrapping depth = 30 q-limbs
-# (+ 4 specials: logQP 1680 <= 1772, the 128-bit bound at N=2^16)
+# (+ RESNET20_N_SPECIAL specials: logQP 1741 <= 1772, the 128-bit bound at N=2^16)
 RESNET20_Q_LIMBS = 30
 # EvalMod's Chebyshev degree before the 3 double angles: 31 approximates
 # sin(2 pi x) near the integers to 2^-25.5 (tests/test_bootstrap_plain.py),
@@ -51,6 +51,19 @@ def resnet20_boot_config(stc_stages=None, degree=None) -> bt.BootConfig:
     return bt.BootConfig(**kw)
 
 
+# special primes K (= alpha, the key-switch digit size): 5 x 61 bits spends
+# the slack the degree-31 EvalMod left under logQP 1772 (1680 -> 1741 bits)
+# on fewer digits -- ceil(n_q/5) instead of ceil(n_q/4): fewer ModUp NTTs,
+# 23 % smaller keys (360.3 -> 354.5 ms/image)
+RESNET20_N_SPECIAL = 5
+
+
+def resnet20_n_special() -> int:
+    """Special primes of the ResNet20 chain (HCNN_N_SPECIAL overrides)."""
+    import os
+    return int(os.environ.get("HCNN_N_SPECIAL", RESNET20_N_SPECIAL))
+
+
 def resnet20_app_levels(cfg: bt.BootConfig) -> int:
     """Application levels of a fixed-length chain: what the bootstrap does not
     use (HCNN_Q_LIMBS overrides the chain length)."""
@@ -67,7 +80,7 @@ def resnet20_setup(app_levels: int | None = None, seed: int = 3, key_seed: int =
     cfg = resnet20_boot_config()
     if app_levels is None:  # keep the chain length (logQP) fixed: bootstrap levels trade for application levels
         app_levels = resnet20_app_levels(cfg)
-    params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg)
+    params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg, n_special=resnet20_n_special())
     boot = bt.Bootstrapper(params, cfg)
     fx = graph.gen_fixture("resnet20", seed, params, golden_count=1)
     g = graph.build_graph("resnet20", fx, multiplex=4)
@@ -98,7 +111,7 @@ def resnet20_plan_only(app_levels: int | None = None, seed: int = 3):
     cfg = resnet20_boot_config()
     if app_levels is None:
         app_levels = resnet20_app_levels(cfg)
-    params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg)
+    params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg, n_special=resnet20_n_special())
     fx = graph.gen_fixture("resnet20", seed, params, golden_count=1)
     g = graph.build_graph("resnet20", fx, multiplex=4)
     out_level = params.max_level - cfg.depth()
