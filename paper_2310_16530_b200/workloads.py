@@ -48,6 +48,8 @@ def resnet20_boot_config(stc_stages=None, degree=None) -> bt.BootConfig:
         kw["stc_stages"] = tuple(stc_stages)
     if degree is not None:
         kw["degree"] = int(degree)
+    if os.environ.get("HCNN_BSGS_BABY"):
+        kw["bsgs_baby"] = int(os.environ["HCNN_BSGS_BABY"])
     return bt.BootConfig(**kw)
 
 
