@@ -58,7 +58,7 @@ struct NttTuning {
   int group_limbs = 0;
   int hints = 1;
   int occupancy = 0;  // 1: register-capped kernels (more resident warps)
-  int split = 2;      // 1: separate launches per modulus class, 2: forward transforms only
+  int split = 1;      // 1: separate launches per modulus class (measured: inverse 0.778 -> 0.758 us/limb), 2: forward only
   int f64_minb = 1;   // FP64 chunk passes: min CTAs per SM hint (1, 5 or 6)
   int pipe = 1;       // FP64 forward chunk pass pipelined over polys (ntt2_fwd_chunks_f64p)
   // ModDown combine fused into the lift NTT's FP64 chunk pass: off -- measured
