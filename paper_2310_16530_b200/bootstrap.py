@@ -47,10 +47,14 @@ from .errors import KeyError_, LevelError, ParameterError
 
 
 def boot_params(name: str, n: int, app_levels: int, cfg: "BootConfig | None" = None, q0_bits: int = 60,
-                app_bits: int = 40, big_bits: int = 58, n_special: int = 4, special_bits: int = 61) -> CkksParams:
+                app_bits: int = 40, big_bits: int = 58, n_special: int = 4,
+                special_bits: "int | tuple[int, ...]" = 61) -> CkksParams:
     """A bootstrappable chain: q0, `app_levels` + StC levels of app_bits,
     then EvalMod + CtS levels of big_bits (top of the chain), Delta = 2^app_bits.
-    Large top primes keep the CtS/EvalMod plaintext products precise."""
+    Large top primes keep the CtS/EvalMod plaintext products precise.
+    `special_bits` may list one size per special prime (n_special is then
+    its length): P must exceed the largest key-switch digit product, so one
+    wide special next to narrow ones covers a digit holding q0."""
     from .ring import Modulus, find_ntt_primes
     cfg = cfg or BootConfig()
     n_small = app_levels + len(cfg.stc_stages)
@@ -58,7 +62,10 @@ def boot_params(name: str, n: int, app_levels: int, cfg: "BootConfig | None" = N
     q0 = find_ntt_primes(n, q0_bits, 1)
     small = find_ntt_primes(n, app_bits, n_small, avoid=q0, alternate=True)
     big = find_ntt_primes(n, big_bits, n_big, avoid=q0 + small, alternate=True)
-    ps = find_ntt_primes(n, special_bits, n_special, avoid=q0 + small + big)
+    sizes = [special_bits] * n_special if isinstance(special_bits, int) else list(special_bits)
+    ps: list[int] = []
+    for b in sorted(set(sizes), key=sizes.index):
+        ps += find_ntt_primes(n, b, sizes.count(b), avoid=q0 + small + big + ps, alternate=b <= 41)
     return CkksParams(name=name, n=n, q_mods=tuple(Modulus.make(q) for q in q0 + small + big),
                       p_mods=tuple(Modulus.make(p) for p in ps), delta=float(2 ** app_bits))
 

@@ -24,13 +24,16 @@ class ResNet20Setup:
 
 
 # the ResNet20 chain: q0 + application levels + bootstrapping depth = 30 q-limbs
-# (+ RESNET20_N_SPECIAL specials: logQP 1741 <= 1772, the 128-bit bound at N=2^16)
+# (+ RESNET20_N_SPECIAL specials: logQP 1759 <= 1772, the 128-bit bound at N=2^16).
+# 30 keeps the 6-bootstrap refresh plan of 31 (refresh points 7/17/27/37) with
+# every op one limb narrower (29 re-plans to 7 bootstraps: 601 ms/image)
 RESNET20_Q_LIMBS = 30
-# EvalMod's Chebyshev degree before the 3 double angles: 31 approximates
-# sin(2 pi x) near the integers to 2^-25.5 (tests/test_bootstrap_plain.py),
-# below the bootstrap's own noise, and needs one level less than 59 (depth
-# 15): the same refresh plan on a 30-limb chain, 381.9 -> 360.3 ms/image
-RESNET20_EVALMOD_DEGREE = 31
+# EvalMod's Chebyshev degree before the 3 double angles.  The bootstrap
+# multiplies the sin approximation error by ~sqrt(N) q0 / (2 pi Delta_1) =
+# 2^8 * 2^12 / 2 pi ~ 2^17.3 (every slot sums N coefficients), so 59 (2^-43)
+# keeps bootstraps at the noise floor (19.6 bits, boot16) while 31 (2^-25.5,
+# one level less) measured 8 bits (tools/boot_precision.py) -- rejected
+RESNET20_EVALMOD_DEGREE = 59
 
 
 def resnet20_boot_config(stc_stages=None, degree=None) -> bt.BootConfig:
@@ -54,9 +57,9 @@ def resnet20_boot_config(stc_stages=None, degree=None) -> bt.BootConfig:
 
 
 # special primes K (= alpha, the key-switch digit size): 5 x 61 bits spends
-# the slack the degree-31 EvalMod left under logQP 1772 (1680 -> 1741 bits)
-# on fewer digits -- ceil(n_q/5) instead of ceil(n_q/4): fewer ModUp NTTs,
-# 23 % smaller keys (360.3 -> 354.5 ms/image)
+# the slack of the 30-limb chain under logQP 1772 on fewer digits --
+# ceil(n_q/5) instead of ceil(n_q/4): fewer ModUp NTTs, 23 % smaller keys
+# (360.3 -> 354.5 ms/image on the same chain)
 RESNET20_N_SPECIAL = 5
 
 
@@ -64,6 +67,31 @@ def resnet20_n_special() -> int:
     """Special primes of the ResNet20 chain (HCNN_N_SPECIAL overrides)."""
     import os
     return int(os.environ.get("HCNN_N_SPECIAL", RESNET20_N_SPECIAL))
+
+
+# bits of the CtS / EvalMod primes at the top of the chain (HCNN_BIG_BITS overrides)
+RESNET20_BIG_BITS = 58
+
+
+def resnet20_big_bits() -> int:
+    import os
+    return int(os.environ.get("HCNN_BIG_BITS", RESNET20_BIG_BITS))
+
+
+def resnet20_special_bits():
+    """Bits of each special prime (HCNN_SPECIAL_BITS, e.g. "61,40,40,40,40";
+    default: RESNET20_N_SPECIAL primes of 61 bits)."""
+    import os
+    env = os.environ.get("HCNN_SPECIAL_BITS")
+    if env:
+        return tuple(int(v) for v in env.split(","))
+    return (61,) * resnet20_n_special()
+
+
+def resnet20_params(name: str, app_levels: int, cfg: bt.BootConfig) -> ckks.CkksParams:
+    sb = resnet20_special_bits()
+    return bt.boot_params(name, 1 << 16, app_levels, cfg, n_special=len(sb), special_bits=sb,
+                          big_bits=resnet20_big_bits())
 
 
 def resnet20_app_levels(cfg: bt.BootConfig) -> int:
@@ -82,7 +110,7 @@ def resnet20_setup(app_levels: int | None = None, seed: int = 3, key_seed: int =
     cfg = resnet20_boot_config()
     if app_levels is None:  # keep the chain length (logQP) fixed: bootstrap levels trade for application levels
         app_levels = resnet20_app_levels(cfg)
-    params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg, n_special=resnet20_n_special())
+    params = resnet20_params("resnet20-16", app_levels, cfg)
     boot = bt.Bootstrapper(params, cfg)
     fx = graph.gen_fixture("resnet20", seed, params, golden_count=1)
     g = graph.build_graph("resnet20", fx, multiplex=4)
@@ -113,7 +141,7 @@ def resnet20_plan_only(app_levels: int | None = None, seed: int = 3):
     cfg = resnet20_boot_config()
     if app_levels is None:
         app_levels = resnet20_app_levels(cfg)
-    params = bt.boot_params("resnet20-16", 1 << 16, app_levels, cfg, n_special=resnet20_n_special())
+    params = resnet20_params("resnet20-16", app_levels, cfg)
     fx = graph.gen_fixture("resnet20", seed, params, golden_count=1)
     g = graph.build_graph("resnet20", fx, multiplex=4)
     out_level = params.max_level - cfg.depth()

@@ -134,19 +134,27 @@ def test_diag_plan_any_baby_count(n1):
         assert np.allclose(bt.apply_plain([p], v), m @ v)
 
 
-def test_resnet20_evalmod_degree_is_precise_enough():
-    """The ResNet20 workload's EvalMod (degree 31 before 3 double angles,
-    workloads.RESNET20_EVALMOD_DEGREE) approximates sin(2 pi x) within
-    2^-24 wherever x = I + eps, |I| < k_bound, |eps| <= 2^-10 -- below the
-    bootstrap's own noise -- one level shallower than degree 59."""
-    import numpy as np
-    from paper_2310_16530_b200 import bootstrap as bt, workloads
-    cfg = workloads.resnet20_boot_config()
-    assert cfg.degree == workloads.RESNET20_EVALMOD_DEGREE == 31
-    assert cfg.evalmod_depth() == bt.BootConfig().evalmod_depth() - 1
+def _evalmod_error(cfg):
     B = cfg.k_bound + 1
     I = np.arange(-cfg.k_bound + 1, cfg.k_bound)
     eps = np.linspace(-2 ** -10, 2 ** -10, 201)
     y = ((I[:, None] + eps[None, :]) / B).ravel()
-    err = np.max(np.abs(bt.evalmod_plain(cfg, y) - np.sin(2 * np.pi * B * y)))
-    assert err < 2 ** -24, err
+    return np.max(np.abs(bt.evalmod_plain(cfg, y) - np.sin(2 * np.pi * B * y)))
+
+
+def test_resnet20_evalmod_degree_is_precise_enough():
+    """The ResNet20 workload's EvalMod (workloads.RESNET20_EVALMOD_DEGREE
+    before 3 double angles) must approximate sin(2 pi x) near the integers
+    (x = I + eps, |I| < k_bound, |eps| <= 2^-10) so well that the bootstrap's
+    ~2^17.3 amplification (sqrt(N) coefficients per slot x q0 / (2 pi
+    Delta_1), message ratio 2^12, N = 2^16) keeps slots within 2^-19:
+    degree 59 does (2^-43); degree 31, one level shallower, does not (2^-25.5
+    -> the 8-bit bootstraps tools/boot_precision.py measured)."""
+    from paper_2310_16530_b200 import workloads
+    cfg = workloads.resnet20_boot_config()
+    assert cfg.degree == workloads.RESNET20_EVALMOD_DEGREE == 59
+    amp = 2 ** 8 * 2 ** cfg.message_ratio_bits / (2 * np.pi)
+    assert _evalmod_error(cfg) * amp < 2 ** -19
+    shallow = bt.BootConfig(degree=31)
+    assert shallow.evalmod_depth() == cfg.evalmod_depth() - 1
+    assert _evalmod_error(shallow) * amp > 2 ** -10
