@@ -474,19 +474,32 @@ def run_cfg2(args, cl):
     pairs = [(ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, L), ks, rng),
               ckks.encrypt(ckks.encode(rng.uniform(-1, 1, params.slots), params, L), ks, rng)) for _ in range(B)]
 
-    def step():
+    # batched (default): the B pairs stacked once into [B, 2, L+1, N] ciphertexts,
+    # one hmult / rescale / rotate call each over the whole batch
+    # (hcnn_hmult_batch, hcnn_rotate_hoisted_batch: keys read once per batch);
+    # sequential: the reference's one-ciphertext-per-call loop, timed alongside
+    sa, sb = ckks.stack([a for a, _ in pairs]), ckks.stack([b for _, b in pairs])
+
+    def seq_step():
         for a, b in pairs:
             ckks.rescale(ckks.hmult(a, b, ks), params)
             ckks.rotate(a, 1, ks)
 
+    def batch_step():
+        ckks.rescale(ckks.hmult(sa, sb, ks), params)
+        ckks.rotate(sa, 1, ks)
+
+    step = seq_step if args.batch_mode == "lockstep" or B == 1 else batch_step
     for _ in range(args.warmup):
-        step()
+        seq_step()
+        batch_step()
     sampler = ClockSampler(cl.local)
     sampler.start()
     sampler.wait_first()
     k0 = _native.kernel_launches()
     ms = timed_steps(cl, step, args.steps)
     launches = _native.kernel_launches() - k0
+    seq_ms = timed_steps(cl, seq_step, args.steps)
     clocks = sampler.stop()
     value = cl.world * B * args.steps / (ms / 1e3)
     _native.profile_read(reset=True)
@@ -508,7 +521,10 @@ def run_cfg2(args, cl):
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic",
             "config": {"workload": "ckks-bench16-hmult-rescale-hrot", "batch_per_step": B, "ring_n": params.n,
-                       "q_limbs": L + 1, "special_limbs": 4, "dnum": params.dnum, "level": L},
+                       "q_limbs": L + 1, "special_limbs": 4, "dnum": params.dnum, "level": L,
+                       "calls": "sequential" if step is seq_step else "batched"},
+            "sequential": {"ms_per_step": seq_ms / args.steps, "value": cl.world * B * args.steps / (seq_ms / 1e3),
+                           "note": "one hmult / rescale / rotate call per ciphertext (the reference's loop)"},
             "roofline": roofline, "keyswitch": ks_roof, "clocks": clocks, "gpu_launches": launches // args.steps,
             "kernels": kernels}), flush=True)
 
@@ -674,7 +690,8 @@ def main():
     ap.add_argument("--boot-batch", type=int, default=1, help="boot16: ciphertexts bootstrapped per step")
     ap.add_argument("--images-per-gpu", type=int, default=1, help="resnet20: images per GPU per step")
     ap.add_argument("--batch-mode", default="stack", choices=["stack", "lockstep"],
-                    help="resnet20, B > 1: stacked image batches (one executor pass) or execute_many")
+                    help="resnet20, B > 1: stacked image batches (one executor pass) or execute_many; "
+                         "cfg2: stack = one batched call per op, lockstep = one call per ciphertext")
     ap.add_argument("--workload", default="resnet20", choices=["resnet20", "cfg2", "boot16", "selftest"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

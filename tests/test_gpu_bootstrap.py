@@ -238,3 +238,23 @@ def test_boot16_full_slot_precision():
     torch.cuda.synchronize()
     assert torch.equal(ckks.unstack(out)[0].data, single.data)
     assert torch.equal(ckks.unstack(out)[1].data, batch[1].data)
+
+
+def test_resnet20_chain_bootstrap_precision():
+    """The ResNet20 workload's own chain (workloads.resnet20_params: 30
+    q-limbs, 5 specials, EvalMod degree RESNET20_EVALMOD_DEGREE) bootstraps
+    full-slot U(-1,1) inputs to >= 19 bits -- the precision the bench's
+    inference runs at (degree 31 measured 8 bits: tools/boot_precision.py)."""
+    from paper_2310_16530_b200 import bootstrap as bt, ckks, workloads
+    cfg = workloads.resnet20_boot_config()
+    params = workloads.resnet20_params("resnet20-16", workloads.resnet20_app_levels(cfg), cfg)
+    assert params.max_level + 1 == workloads.RESNET20_Q_LIMBS and len(params.p_mods) == workloads.RESNET20_N_SPECIAL
+    b = bt.Bootstrapper(params, cfg)
+    ks = b.keygen(np.random.default_rng(20), rotations=[])
+    rng = np.random.default_rng(5)
+    v = rng.uniform(-1, 1, params.slots)
+    out = b.bootstrap(ckks.encrypt(ckks.encode(v, params, 0), ks, rng), ks)
+    assert out.level == b.output_level
+    err = float(np.max(np.abs(ckks.decode(ckks.decrypt(out, ks), params, imag_tol=None) - v)))
+    print("resnet20-chain bootstrap bits", -np.log2(err))
+    assert -np.log2(err) >= 19.0
