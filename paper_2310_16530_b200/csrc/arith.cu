@@ -18,7 +18,7 @@ namespace hcnn {
 // another launch of the same call (created once per device, never freed).
 // The caller holds *mu across record-fork / wait / launch / record-join /
 // wait so host threads sharing a device cannot interleave their forks.
-static cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join, std::mutex** mu) {
+cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join, std::mutex** mu) {
   static std::mutex init_mu;
   static std::mutex use_mu[64];
   static cudaStream_t ss[64] = {};

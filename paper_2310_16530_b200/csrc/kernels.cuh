@@ -1,6 +1,7 @@
 // Kernel-level interfaces shared between the .cu translation units.
 #pragma once
 #include <atomic>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -65,8 +66,16 @@ struct NttTuning {
   // slower (tools/ks_bench.py: hoisted rotations at level 14, 2.21 -> 2.86 ms;
   // the epilogue's acc / c0 loads are not prefetched and stall every poly)
   int md_fuse = 0;
+  // integer-network class runs of a mixed launch (q0, the wide bootstrapping
+  // primes, the specials) on a side stream forked from the caller's, next
+  // to the FP64-network run (a fork / join branch inside a graph capture)
+  int fork = 1;
 };
 extern NttTuning g_ntt_tuning;
+
+// per-device side stream + fork / join events (arith.cu); the caller holds
+// *mu from the fork record to the join wait
+cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join, std::mutex** mu);
 
 struct NttTables {
   u32 logN;

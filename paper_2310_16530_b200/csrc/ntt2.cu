@@ -1166,22 +1166,22 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
   // chunk twiddles are stored as doubles
   const bool split = g_ntt_tuning.split == 1 || (g_ntt_tuning.split == 2 && !inverse) ||
                      (kNttFp && T.small != nullptr);
-  auto one = [&](const LimbMap& m, u32 ny, u32 nz, int mode) -> cudaError_t {
-    if (mode == 0) return g_ntt_tuning.occupancy == 2 ? launch_pair<true, 2, 0>(T, m, ny, nz, inverse, st)
-                          : occ ? launch_pair<true, 1, 0>(T, m, ny, nz, inverse, st)
-                                : launch_pair<true, 0, 0>(T, m, ny, nz, inverse, st);
-    if (mode == 1) return occ ? launch_pair<true, 1, 1>(T, m, ny, nz, inverse, st)
-                              : launch_pair<true, 0, 1>(T, m, ny, nz, inverse, st);
+  auto one = [&](const LimbMap& m, u32 ny, u32 nz, int mode, cudaStream_t s) -> cudaError_t {
+    if (mode == 0) return g_ntt_tuning.occupancy == 2 ? launch_pair<true, 2, 0>(T, m, ny, nz, inverse, s)
+                          : occ ? launch_pair<true, 1, 0>(T, m, ny, nz, inverse, s)
+                                : launch_pair<true, 0, 0>(T, m, ny, nz, inverse, s);
+    if (mode == 1) return occ ? launch_pair<true, 1, 1>(T, m, ny, nz, inverse, s)
+                              : launch_pair<true, 0, 1>(T, m, ny, nz, inverse, s);
     // occupancy 2: chunk pass capped at 128 registers (4 CTAs of 128 threads per SM), cols unchanged
-    if (mode == 3) return g_ntt_tuning.occupancy == 2 ? launch_pair<true, 2, 3>(T, m, ny, nz, inverse, st)
-                                                      : launch_pair<true, 0, 3>(T, m, ny, nz, inverse, st);
-    return occ ? launch_pair<true, 1, 2>(T, m, ny, nz, inverse, st) : launch_pair<true, 0, 2>(T, m, ny, nz, inverse, st);
+    if (mode == 3) return g_ntt_tuning.occupancy == 2 ? launch_pair<true, 2, 3>(T, m, ny, nz, inverse, s)
+                                                      : launch_pair<true, 0, 3>(T, m, ny, nz, inverse, s);
+    return occ ? launch_pair<true, 1, 2>(T, m, ny, nz, inverse, s) : launch_pair<true, 0, 2>(T, m, ny, nz, inverse, s);
   };
   auto pair = [&](const LimbMap& m, u32 ny, u32 nz) -> cudaError_t {
     if (!split || !T.small) {
       LimbMap mm = m;
       mm.cb = nullptr;
-      cudaError_t err = one(mm, ny, nz, 2);
+      cudaError_t err = one(mm, ny, nz, 2, st);
       if (!err && m.cb) {
         err = launch_combine_rows(*m.cb, m.base, m.basis.nq, m.r0 + m.first_limb, ny, nz, T.logN, T.mc, st);
         g_ntt_extra_launches += 1;
@@ -1196,7 +1196,26 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
       if (f == 2 && kNttFp) return 2;
       return inverse && g_ntt_tuning.split != 1 ? -1 : f;
     };
-    while (r < ny) {
+    // a mix of FP64-network and integer-network runs: the integer runs (q0's
+    // single limb, the specials: small, latency-bound launches) go to the
+    // side stream, forked before the first launch and joined after the last,
+    // so they overlap the FP64 run instead of serialising behind it
+    bool has_fp = false, has_int = false;
+    for (u32 rr = 0; rr < ny; ++rr) (cls(rr) == 2 ? has_fp : has_int) = true;
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    std::mutex* fmu = nullptr;
+    const bool par = g_ntt_tuning.fork && has_fp && has_int &&
+                     side_stream(&side, &fork, &join, &fmu) == cudaSuccess;
+    std::unique_lock<std::mutex> flk;
+    if (par) {
+      flk = std::unique_lock<std::mutex>(*fmu);
+      cudaError_t e0 = cudaEventRecord(fork, st);
+      if (!e0) e0 = cudaStreamWaitEvent(side, fork, 0);
+      if (e0) return e0;
+    }
+    cudaError_t err = cudaSuccess;
+    while (r < ny && !err) {
       const int f = cls(r);
       u32 e = r + 1;
       while (e < ny && cls(e) == f) ++e;
@@ -1205,21 +1224,26 @@ cudaError_t launch_ntt2(const NttTables& T, const LimbMap& map, u32 nlimbs, u32 
       // class 2: the FP64 network both ways; other classes keep one
       // run-time-dispatch inverse launch unless split == 1
       const int mode = f == 2 ? 3 : f < 0 ? 2 : f;
+      const cudaStream_t rs = par && mode != 3 ? side : st;
       // the fused ModDown combine runs inside the FP64 pipelined chunk pass;
       // integer-network rows get a plain NTT and the combine kernel after it
       const bool fuse_here = mm.cb && mode == 3 && !inverse && g_ntt_tuning.pipe;
       const NttCombine* cb = mm.cb;
       if (!fuse_here) mm.cb = nullptr;
-      cudaError_t err = one(mm, e - r, nz, mode);
+      err = one(mm, e - r, nz, mode, rs);
       if (!err && cb && !fuse_here) {
-        err = launch_combine_rows(*cb, m.base, m.basis.nq, mm.r0 + m.first_limb, e - r, nz, T.logN, T.mc, st);
+        err = launch_combine_rows(*cb, m.base, m.basis.nq, mm.r0 + m.first_limb, e - r, nz, T.logN, T.mc, rs);
         g_ntt_extra_launches += 1;
       }
       if (r > 0) g_ntt_extra_launches += 2;  // launch accounting counts one pair per call
-      if (err) return err;
       r = e;
     }
-    return cudaSuccess;
+    if (par) {  // join even after an error: the capture must not end with an open fork
+      cudaError_t e2 = cudaEventRecord(join, side);
+      if (!e2) e2 = cudaStreamWaitEvent(st, join, 0);
+      if (!err) err = e2;
+    }
+    return err;
   };
   (void)hint;
   count_limbs(T, map, nlimbs, npolys, inverse);
