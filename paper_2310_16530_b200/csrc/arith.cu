@@ -18,6 +18,8 @@ namespace hcnn {
 // another launch of the same call (created once per device, never freed).
 // The caller holds *mu across record-fork / wait / launch / record-join /
 // wait so host threads sharing a device cannot interleave their forks.
+int g_fbc_fork = 1;  // ModUp: the partial last digit's FBC on the side stream
+
 cudaError_t side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join, std::mutex** mu) {
   static std::mutex init_mu;
   static std::mutex use_mu[64];
@@ -2339,17 +2341,35 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
                                                                 n_ext, logN);
     return cudaGetLastError();
   }
-  // full digits share one launch; a partial last digit gets its own
+  // full digits share one launch; a partial last digit gets its own, on the
+  // side stream next to it (independent outputs; joined before returning)
   u32 nfull = ndig;
   if (htabs[ndig - 1].ns != alpha) nfull = ndig - 1;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  std::mutex* fmu = nullptr;
+  const bool par = g_fbc_fork && nfull && nfull < ndig && side_stream(&side, &fork, &join, &fmu) == cudaSuccess;
+  std::unique_lock<std::mutex> flk;
+  cudaStream_t pst = st;
+  if (par) {
+    flk = std::unique_lock<std::mutex>(*fmu);
+    cudaError_t e0 = cudaEventRecord(fork, st);
+    if (!e0) e0 = cudaStreamWaitEvent(side, fork, 0);
+    if (e0) return e0;
+    pst = side;
+  }
   cudaError_t e = cudaSuccess;
-  if (nfull)
-    e = dispatch_fbc_t((int)alpha, tabs, 1, mc, xc, (size_t)alpha * (1u << logN), raised,
-                       (size_t)n_ext * (1u << logN), logN, nfull, 0, htabs[0].nt, 0, st, nb, xc_bst, r_bst);
-  if (e) return e;
   if (nfull < ndig)
     e = dispatch_fbc_t((int)htabs[ndig - 1].ns, tabs, 1, mc, xc, (size_t)alpha * (1u << logN), raised,
-                       (size_t)n_ext * (1u << logN), logN, 1, nfull, htabs[ndig - 1].nt, 0, st, nb, xc_bst, r_bst);
+                       (size_t)n_ext * (1u << logN), logN, 1, nfull, htabs[ndig - 1].nt, 0, pst, nb, xc_bst, r_bst);
+  if (!e && nfull)
+    e = dispatch_fbc_t((int)alpha, tabs, 1, mc, xc, (size_t)alpha * (1u << logN), raised,
+                       (size_t)n_ext * (1u << logN), logN, nfull, 0, htabs[0].nt, 0, st, nb, xc_bst, r_bst);
+  if (par) {
+    cudaError_t e2 = cudaEventRecord(join, side);
+    if (!e2) e2 = cudaStreamWaitEvent(st, join, 0);
+    if (!e) e = e2;
+  }
   return e;
 }
 

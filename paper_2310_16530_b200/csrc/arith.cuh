@@ -28,6 +28,7 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
 // acc [nb][2][n_ext]; x_eval entries x_bst apart; one key load feeds up to
 // g_ks_batch (1, 2 or 4) entries (hcnn_set_option "ks_batch")
 extern int g_ks_batch;
+extern int g_fbc_fork;
 extern int g_ks_pipe;
 extern int g_ks_tma;
 extern int g_ks_tma_min;

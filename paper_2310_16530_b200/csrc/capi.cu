@@ -1338,6 +1338,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_f64_minb") g_ntt_tuning.f64_minb = (int)value;
   else if (k == "ntt_pipe") g_ntt_tuning.pipe = (int)value;
   else if (k == "ntt_fork") g_ntt_tuning.fork = (int)value;
+  else if (k == "fbc_fork") g_fbc_fork = (int)value;
   else if (k == "md_fuse") g_ntt_tuning.md_fuse = (int)value;
   else if (k == "fbc_fast") CK(set_fbc_fast((int)value));
   else if (k == "ks_batch") g_ks_batch = (int)value;
