@@ -68,7 +68,8 @@ int hcnn_ntt_forward(hcnn_ctx* ctx, uint64_t* data, uint32_t nq, uint32_t np, ui
 /* ntt_inverse ring.py:328-336 (kernels.intt_inplace kernels.py:255-281) */
 int hcnn_ntt_inverse(hcnn_ctx* ctx, uint64_t* data, uint32_t nq, uint32_t np, uint32_t npolys, void* stream);
 /* poly_add / poly_sub / poly_neg ring.py:264-284 (kernels.addmod/submod/negmod kernels.py:208-230).
- * b_broadcast != 0: b is a single poly applied to every poly of a. */
+ * b_broadcast == 1: b is a single poly applied to every poly of a; == 2 (add / sub): a holds
+ * ciphertexts (c0, c1 pairs), b is applied to every c0 and every c1 is copied (padd, ckks.py:477-479). */
 int hcnn_poly_add(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,
                   uint32_t npolys, int b_broadcast, void* stream);
 int hcnn_poly_sub(hcnn_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t nq, uint32_t np,

@@ -110,6 +110,12 @@ __global__ void k_ew_binary(int op, u64* __restrict__ out, const u64* __restrict
   const ulonglong2* A = reinterpret_cast<const ulonglong2*>(a + off);
   const ulonglong2* B = reinterpret_cast<const ulonglong2*>(b + boff);
   ulonglong2* O = reinterpret_cast<ulonglong2*>(out + off);
+  // b_bcast == 2 (ciphertext + plaintext): b goes into the even polys (c0 of
+  // every ciphertext), the odd ones (c1) are copied -- one pass, no clone
+  if (b_bcast == 2 && (rc.z & 1u)) {
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < N / 2; i += gridDim.x * blockDim.x) O[i] = A[i];
+    return;
+  }
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < N / 2; i += gridDim.x * blockDim.x) {
     ulonglong2 x = A[i], y = B[i], o;
     switch (op) {

@@ -116,10 +116,17 @@ class DeviceContext:
         return t
 
     def binop(self, op: str, a: torch.Tensor, b: torch.Tensor, nq: int, np_: int = 0,
-              out: torch.Tensor | None = None) -> torch.Tensor:
+              out: torch.Tensor | None = None, plain_c0: bool = False) -> torch.Tensor:
+        """plain_c0: a holds ciphertexts ([.., 2, limbs, N]), b one plaintext
+        poly added to every c0; every c1 is copied (hcnn_poly_add b_broadcast 2)."""
         npolys = self._npolys(a, nq, np_, self.n)
         nb = self._npolys(b, nq, np_, self.n)
-        bcast = 1 if (nb == 1 and npolys > 1) else 0
+        if plain_c0:
+            if nb != 1 or npolys % 2 or op not in ("add", "sub"):
+                raise BasisError("plain_c0: one plaintext poly against whole ciphertexts")
+            bcast = 2
+        else:
+            bcast = 1 if (nb == 1 and npolys > 1) else 0
         if not bcast and nb != npolys:
             raise BasisError("operand batch sizes differ")
         if out is None:
