@@ -331,3 +331,37 @@ def test_reference_side_shim_routes_reference_layers_into_the_engine(tmp_path):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "shim ok" in r.stdout
+
+
+def test_stack_views_and_image_batches():
+    """ckks.stack / unstack and graph.stack_images / unstack_images are pure
+    tensor bookkeeping (host-checkable): consecutive slices of one buffer
+    stack without a copy (the conv planes' MAC buffer, packing._mac_multi),
+    other members are copied; under ckks.image_batched(B) members are
+    [B, 2, l+1, N] image batches that stack along the image axis and unstack
+    into B-image chunks; stack_images / unstack_images round-trip."""
+    import torch
+    from paper_2310_16530_b200 import ckks, graph, packing
+    buf = torch.arange(3 * 2 * 4 * 8, dtype=torch.int64).reshape(3, 2, 4, 8)
+    cts = [ckks.Ciphertext(buf[i], 2.0, 8, None) for i in range(3)]
+    s = ckks.stack(cts)
+    assert s.batch == 3 and s.data.data_ptr() == buf.data_ptr()        # a view, no copy
+    apart = [ckks.Ciphertext(buf[i].clone(), 2.0, 8, None) for i in (2, 0)]
+    s2 = ckks.stack(apart)
+    assert s2.data.data_ptr() != buf.data_ptr() and torch.equal(s2.data[0], buf[2])
+    assert [torch.equal(u.data, buf[i]) for i, u in enumerate(ckks.unstack(s))] == [True] * 3
+    with pytest.raises(Exception):
+        ckks.stack([cts[0], ckks.Ciphertext(buf[1], 3.0, 8, None)])   # scales differ
+    with ckks.image_batched(2):
+        x = [ckks.Ciphertext(torch.full((2, 2, 4, 8), i, dtype=torch.int64), 2.0, 8, None) for i in range(3)]
+        st = ckks.stack(x)
+        assert st.data.shape == (6, 2, 4, 8)
+        un = ckks.unstack(st)
+        assert [u.data.shape for u in un] == [(2, 2, 4, 8)] * 3 and int(un[2].data[1, 1, 3, 7]) == 2
+    imgs = [packing.PackedTensor(cts=[ckks.Ciphertext(torch.full((2, 4, 8), 10 * b + i, dtype=torch.int64),
+                                                      2.0, 8, None) for i in range(2)], fmt="F", shape=(1, 2, 2))
+            for b in range(3)]
+    both = graph.stack_images(imgs)
+    assert [c.data.shape for c in both.cts] == [(3, 2, 4, 8)] * 2
+    back = graph.unstack_images(both)
+    assert all(torch.equal(back[b].cts[i].data, imgs[b].cts[i].data) for b in range(3) for i in range(2))
