@@ -194,12 +194,14 @@ def int_roofline(roof: dict, prof: dict, limbs: dict, n: int) -> dict:
     hbm = {k: roof[k] for k in ("achieved", "peak", "unit", "frac", "peak_source", "algorithmic_bytes_per_launch")}
     # DRAM traffic per launch from the committed ncu --set full capture, scaled per limb
     traffic = roof.get("traffic")
-    tf = ROOT / "profiles" / "r01_ncu_ntt_traffic.json"
-    if traffic is None and fam == "ntt_fwd" and tf.exists():
-        per_limb = json.loads(tf.read_text())["dram_bytes_per_limb"]
+    tf = ROOT / "profiles" / "r02_ncu_ntt_traffic.json"
+    if traffic is None and tf.exists():
+        cls = json.loads(tf.read_text())["per_class"]
         launches = sum(v["launches"] for k, v in prof.items() if _kernel_family(k) == fam)
-        traffic = round(per_limb * (fast + full) / max(launches, 1))
-        hbm["traffic_source"] = ("profiles/r01_ncu_ntt_traffic.json (ncu, cold L2) x mean limbs per launch "
+        traffic = round((cls[f"{d}_f64"]["dram_bytes_per_limb"] * fast + cls[f"{d}_int"]["dram_bytes_per_limb"] * full)
+                        / max(launches, 1))
+        hbm["traffic_source"] = ("profiles/r02_ncu_ntt_traffic.json (ncu --cache-control none, steady state, "
+                                 "per-class DRAM bytes per limb) x this run's limbs per launch "
                                  "(one launch = the cols + chunks pass pair)")
     out = {"kernel": fam, "bound": "int", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
            "unit": "Gbutterfly/s", "frac": round(ideal_s / (ms / 1e3), 4), "traffic": traffic,
