@@ -1837,18 +1837,20 @@ __global__ void __launch_bounds__(256) k_ks_inner_tma(u64* __restrict__ acc, con
 }
 
 // k_ks_inner_tma with TPB threads per CTA and kMacTile / TPB output
-// coefficients per thread (independent MAC chains per thread).
+// coefficients per thread (independent MAC chains per thread).  The body
+// serves one rotation's output tile `tile` of limb row blockIdx.y.
 template <int ST, int TPB>
-__global__ void __launch_bounds__(TPB) k_ks_inner_tma2(u64* __restrict__ acc, const u64* __restrict__ x_eval,
-                                                      const u64* __restrict__ raised, const u64* __restrict__ key_b,
-                                                      const u64* __restrict__ key_a, Basis basis, u32 alpha,
-                                                      u32 ndig, u32 logN, u64 g, const ModConsts* __restrict__ mc,
-                                                      u32 nb, size_t x_bst, const u64* __restrict__ c0,
-                                                      size_t c0_bst, const u64* __restrict__ pR, u32 key_lq) {
+__device__ __forceinline__ void ks_inner_tma2_body(u64* __restrict__ acc, const u64* __restrict__ x_eval,
+                                                   const u64* __restrict__ raised, const u64* __restrict__ key_b,
+                                                   const u64* __restrict__ key_a, const Basis& basis, u32 alpha,
+                                                   u32 ndig, u32 logN, u64 g, const ModConsts* __restrict__ mc,
+                                                   u32 nb, size_t x_bst, const u64* __restrict__ c0,
+                                                   size_t c0_bst, const u64* __restrict__ pR, u32 key_lq,
+                                                   u32 tile) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KsStage* S = reinterpret_cast<KsStage*>(smem_raw);
   __shared__ __align__(8) u64 full[ST];
-  const u32 N = 1u << logN, r = blockIdx.y, tile = blockIdx.x, tid = threadIdx.x;
+  const u32 N = 1u << logN, r = blockIdx.y, tid = threadIdx.x;
   const u32 b0 = blockIdx.z * kKsEntries;
   const u32 ne = nb - b0 < (u32)kKsEntries ? nb - b0 : (u32)kKsEntries;
   const u32 n_ext = basis.nlimbs();
@@ -1948,6 +1950,36 @@ __global__ void __launch_bounds__(TPB) k_ks_inner_tma2(u64* __restrict__ acc, co
       A[((size_t)n_ext + r) * N + kc] = redc128(ah[e][c], al[e][c], q, ninv);
     }
   }
+}
+
+template <int ST, int TPB>
+__global__ void __launch_bounds__(TPB) k_ks_inner_tma2(u64* __restrict__ acc, const u64* __restrict__ x_eval,
+                                                      const u64* __restrict__ raised, const u64* __restrict__ key_b,
+                                                      const u64* __restrict__ key_a, Basis basis, u32 alpha,
+                                                      u32 ndig, u32 logN, u64 g, const ModConsts* __restrict__ mc,
+                                                      u32 nb, size_t x_bst, const u64* __restrict__ c0,
+                                                      size_t c0_bst, const u64* __restrict__ pR, u32 key_lq) {
+  ks_inner_tma2_body<ST, TPB>(acc, x_eval, raised, key_b, key_a, basis, alpha, ndig, logN, g, mc, nb, x_bst, c0,
+                              c0_bst, pR, key_lq, blockIdx.x);
+}
+
+// Every rotation of a hoisted group in one launch: blockIdx.x = tile * n +
+// rotation, so the CTAs resident at any time cover a few limb rows for all
+// rotations and the raised digits of those rows (shared by every rotation,
+// each read through its own Galois block remap) come from L2 after the
+// first rotation touches them -- one HBM pass over the raised digits per
+// group instead of one per rotation.  Same arithmetic per output as
+// k_ks_inner_tma2 (bit-identical).
+template <int ST, int TPB>
+__global__ void __launch_bounds__(TPB) k_ks_inner_tma2_rots(const __grid_constant__ KsRots R, u32 nrot,
+                                                           const u64* __restrict__ x_eval,
+                                                           const u64* __restrict__ raised, Basis basis, u32 alpha,
+                                                           u32 ndig, u32 logN, const ModConsts* __restrict__ mc,
+                                                           u32 nb, size_t x_bst, const u64* __restrict__ c0,
+                                                           size_t c0_bst, const u64* __restrict__ pR) {
+  const u32 rot = blockIdx.x % nrot, tile = blockIdx.x / nrot;
+  ks_inner_tma2_body<ST, TPB>(R.acc[rot], x_eval, raised, R.kb[rot], R.ka[rot], basis, alpha, ndig, logN, R.g[rot],
+                              mc, nb, x_bst, c0, c0_bst, pR, R.klq[rot], tile);
 }
 
 // k_ks_inner_tma3: k_ks_inner_tma2 with a dedicated producer warp and a
@@ -2456,6 +2488,32 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
                                            x_bst, c0, c0_bst, pR, key_lq);
   }
   return cudaGetLastError();
+}
+
+
+int g_ks_rots = 1;         // hoisted groups: every rotation's inner product in one launch (k_ks_inner_tma2_rots)
+int g_ks_rots_min_nb = 1;  // ... for batches of at least this many entries
+
+bool ks_rots_ok(u32 nb, u32 nrot, u32 logN) {
+  return g_ks_rots && g_ks_tma && !g_ks_tma3 && g_ks_tpb == 128 && nrot >= 2 && nb >= (u32)g_ks_rots_min_nb &&
+         (1u << logN) % kMacTile == 0;
+}
+
+cudaError_t launch_ks_inner_rots(const KsRots& R, u32 nrot, const u64* x_eval, const u64* raised, Basis basis,
+                                 u32 alpha, u32 ndig, u32 logN, const ModConsts* mc, cudaStream_t st, u32 nb,
+                                 size_t x_bst, const u64* c0, size_t c0_bst, const u64* pR) {
+  if (nrot == 0) return cudaSuccess;
+  if (nrot > (u32)kKsRotMax) return cudaErrorInvalidValue;
+  const u32 nbb = nb ? nb : 1;
+  dim3 grid((1u << logN) / kMacTile * nrot, basis.nlimbs(), (nbb + kKsEntries - 1) / kKsEntries);
+  auto go = [&](auto kern, int stages) -> cudaError_t {
+    const size_t sm = sizeof(KsStage) * stages;
+    cudaError_t e = ensure_smem((const void*)kern, sm);
+    if (e) return e;
+    kern<<<grid, 128, sm, st>>>(R, nrot, x_eval, raised, basis, alpha, ndig, logN, mc, nbb, x_bst, c0, c0_bst, pR);
+    return cudaGetLastError();
+  };
+  return g_ks_stages == 4 ? go(k_ks_inner_tma2_rots<4, 128>, 4) : go(k_ks_inner_tma2_rots<3, 128>, 3);
 }
 
 cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,

@@ -54,6 +54,23 @@ cudaError_t launch_ks_inner(u64* acc, const u64* x_eval, const u64* raised, cons
                             cudaStream_t st, u32 nb = 1, size_t x_bst = 0, const u64* c0 = nullptr,
                             size_t c0_bst = 0, const u64* pR = nullptr, u32 key_lq = 0,
                             u32 fast_from = 0xffffffffu);  // Q rows >= fast_from: q < 2^42 (96-bit MACs)
+// every rotation of a hoisted group in one inner-product launch (same
+// arguments as launch_ks_inner, per-rotation acc / keys / Galois / key_lq)
+constexpr int kKsRotMax = 16;
+struct KsRots {
+  u64* acc[kKsRotMax];
+  const u64* kb[kKsRotMax];
+  const u64* ka[kKsRotMax];
+  u64 g[kKsRotMax];
+  u32 klq[kKsRotMax];
+};
+extern int g_ks_rots;
+extern int g_ks_rots_min_nb;
+bool ks_rots_ok(u32 nb, u32 nrot, u32 logN);
+cudaError_t launch_ks_inner_rots(const KsRots& R, u32 nrot, const u64* x_eval, const u64* raised, Basis basis,
+                                 u32 alpha, u32 ndig, u32 logN, const ModConsts* mc, cudaStream_t st, u32 nb,
+                                 size_t x_bst, const u64* c0 = nullptr, size_t c0_bst = 0,
+                                 const u64* pR = nullptr);
 // acc [nb][2][n_ext], lift [nb][2][nq]; outputs / addends of entry b at +b*out_bst / +b*add_bst
 cudaError_t launch_moddown_combine(u64* out0, u64* out1, const u64* acc, const u64* lift, const u64* add0,
                                    const u64* add1, u64 g_add, u32 nq, u32 n_ext, u32 logN, const u64* pinv,

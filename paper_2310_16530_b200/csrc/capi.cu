@@ -983,6 +983,10 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
   for (u32 i0 = 0; i0 < n_rot; i0 += chunk) {
     const u32 nr = n_rot - i0 < chunk ? n_rot - i0 : chunk;
     ComboSteps S;
+    // the chunk's inner products: one launch for all its rotations when
+    // ks_rots_ok (raised digits read from HBM once per chunk), else one each
+    const bool rots = nr <= (u32)kKsRotMax && ks_rots_ok(nb, nr, c->logN);
+    KsRots R{};
     for (u32 j = 0; j < nr; ++j) {
       const u32 i = i0 + j;
       const u64 g = galois[i] % (2ull * c->n);
@@ -990,10 +994,22 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
       S.g[j] = g;
       ks_acc(0, nb);
       ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * nq) * N);
+      if (rots) {
+        R.acc[j] = w.acc + j * a_step;
+        R.kb[j] = kbs[i];
+        R.ka[j] = kas[i];
+        R.g[j] = g;
+        R.klq[j] = key_lqs ? key_lqs[i] : 0;
+        continue;
+      }
       PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
          launch_ks_inner(w.acc + j * a_step, c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd,
                          c->logN, g, c->d_mc, STREAM(s), nb, ct, nullptr, 0, nullptr, key_lqs ? key_lqs[i] : 0, ks_fast_from(c, nq)));
     }
+    if (rots)
+      PK("ks_inner", 8.0 * nr * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
+         launch_ks_inner_rots(R, nr, c1, w.raised, c->basis(nq, c->K), c->alpha, nd, c->logN, c->d_mc, STREAM(s),
+                              nb, ct));
     const u32 np = 2 * nb * nr;
     LimbMap m{};
     m.base = w.acc + nq * N;
@@ -1056,13 +1072,32 @@ int hcnn_rotate_hoisted_ext_batch(hcnn_ctx* c, uint64_t* const* outs, const uint
   const u64* c1 = cts + nq * N;
   rc = ks_modup(c, level, c1, w, STREAM(s), nb, ct);
   if (rc) return rc;
-  for (u32 i = 0; i < n_rot; ++i) {
-    const u64 g = galois[i] % (2ull * c->n);
-    ks_acc(0, nb);
-    ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * n_ext + nb * nq) * N);
-    PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext + nb * nq) * N, 1, STREAM(s),
-       launch_ks_inner(outs[i], c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd, c->logN, g,
-                       c->d_mc, STREAM(s), nb, ct, cts, ct, c->d_pR, key_lqs ? key_lqs[i] : 0, ks_fast_from(c, nq)));
+  // groups of up to kKsRotMax rotations in one launch when ks_rots_ok
+  for (u32 i0 = 0; i0 < n_rot; i0 += (u32)kKsRotMax) {
+    const u32 nr = n_rot - i0 < (u32)kKsRotMax ? n_rot - i0 : (u32)kKsRotMax;
+    const bool rots = ks_rots_ok(nb, nr, c->logN);
+    KsRots R{};
+    for (u32 j = 0; j < nr; ++j) {
+      const u32 i = i0 + j;
+      const u64 g = galois[i] % (2ull * c->n);
+      ks_acc(0, nb);
+      ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * n_ext + nb * nq) * N);
+      if (rots) {
+        R.acc[j] = outs[i];
+        R.kb[j] = kbs[i];
+        R.ka[j] = kas[i];
+        R.g[j] = g;
+        R.klq[j] = key_lqs ? key_lqs[i] : 0;
+        continue;
+      }
+      PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext + nb * nq) * N, 1, STREAM(s),
+         launch_ks_inner(outs[i], c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd, c->logN, g,
+                         c->d_mc, STREAM(s), nb, ct, cts, ct, c->d_pR, key_lqs ? key_lqs[i] : 0, ks_fast_from(c, nq)));
+    }
+    if (rots)
+      PK("ks_inner", 8.0 * nr * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext + nb * nq) * N, 1, STREAM(s),
+         launch_ks_inner_rots(R, nr, c1, w.raised, c->basis(nq, c->K), c->alpha, nd, c->logN, c->d_mc, STREAM(s),
+                              nb, ct, cts, ct, c->d_pR));
   }
   return HCNN_OK;
 }
@@ -1339,6 +1374,8 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ntt_pipe") g_ntt_tuning.pipe = (int)value;
   else if (k == "ntt_fork") g_ntt_tuning.fork = (int)value;
   else if (k == "fbc_fork") g_fbc_fork = (int)value;
+  else if (k == "ks_rots") g_ks_rots = (int)value;
+  else if (k == "ks_rots_min_nb") g_ks_rots_min_nb = (int)value;
   else if (k == "md_fuse") g_ntt_tuning.md_fuse = (int)value;
   else if (k == "fbc_fast") CK(set_fbc_fast((int)value));
   else if (k == "ks_batch") g_ks_batch = (int)value;
