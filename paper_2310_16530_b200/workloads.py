@@ -53,6 +53,8 @@ def resnet20_boot_config(stc_stages=None, degree=None) -> bt.BootConfig:
         kw["degree"] = int(degree)
     if os.environ.get("HCNN_BSGS_BABY"):
         kw["bsgs_baby"] = int(os.environ["HCNN_BSGS_BABY"])
+    if os.environ.get("HCNN_DOUBLE_ANGLE"):
+        kw["double_angle"] = int(os.environ["HCNN_DOUBLE_ANGLE"])
     return bt.BootConfig(**kw)
 
 

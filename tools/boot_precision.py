@@ -22,9 +22,10 @@ def main():
               "mixsp": dict(big_bits=58, special_bits=(61, 40, 40, 40), n_special=4)}
     degree = int(sys.argv[1]) if len(sys.argv) > 1 else 59
     pick = sys.argv[2].split(",") if len(sys.argv) > 2 else list(chains)
+    r = int(sys.argv[3]) if len(sys.argv) > 3 else 3
     for name in pick:
         kw = chains[name]
-        cfg = bt.BootConfig(degree=degree)
+        cfg = bt.BootConfig(degree=degree, double_angle=r)
         params = bt.boot_params("boot16", 1 << 16, 8, cfg, **kw)
         b = bt.Bootstrapper(params, cfg)
         ks = b.keygen(np.random.default_rng(16), rotations=[1])
@@ -46,7 +47,7 @@ def main():
         for _ in range(5):
             b.bootstrap(ct, ks)
         torch.cuda.synchronize()
-        print(json.dumps({"chain": name, "degree": degree, **{k: str(v) for k, v in kw.items()}, "bits": bits,
+        print(json.dumps({"chain": name, "degree": degree, "double_angle": r, **{k: str(v) for k, v in kw.items()}, "bits": bits,
                           "ms_eager": round((time.perf_counter() - t) / 5 * 1e3, 2)}), flush=True)
         del b, ks
         torch.cuda.empty_cache()
