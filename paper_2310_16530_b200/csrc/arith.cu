@@ -71,6 +71,12 @@ __device__ __forceinline__ u64 redc96(u64 lh, u64 mid, u64 q, u64 ninv) {
 
 // FBC: the 96-bit path for conversions whose sources and target are all below 2^42
 __constant__ bool g_fbc_fast_dev = true;
+// key-switch inner product (k_ks_inner_tma2 / _rots): 96-bit rows for q < 2^42
+__constant__ bool g_ks96_dev = true;
+cudaError_t set_ks96(int on) {
+  const bool v = on != 0;
+  return cudaMemcpyToSymbol(g_ks96_dev, &v, sizeof(v));
+}
 cudaError_t set_fbc_fast(int on) {
   const bool v = on != 0;
   return cudaMemcpyToSymbol(g_fbc_fast_dev, &v, sizeof(v));
@@ -1856,6 +1862,10 @@ __device__ __forceinline__ void ks_inner_tma2_body(u64* __restrict__ acc, const 
   const u32 n_ext = basis.nlimbs();
   const u32 mod = basis.mod_of(r);
   const u64 q = mc[mod].q, ninv = mc[mod].ninv, one_sh = mc[mod].one_sh;
+  // rows whose modulus is below 2^42 (the 40-bit primes): residues and key
+  // words fit 42 bits, so each product accumulates through a 96-bit carry
+  // chain (5 IMADs instead of ~11, no lazy folds; T < 2^90) -- CTA-uniform
+  const bool f96 = g_ks96_dev && q < (1ull << 42);
   const u32 klq = key_lq ? key_lq : basis.Lq;
   const size_t key_dst = (size_t)(klq + basis.np) * N;
   const u32 kmod = mod < basis.Lq ? mod : klq + (mod - basis.Lq);
@@ -1915,8 +1925,13 @@ __device__ __forceinline__ void ks_inner_tma2_body(u64* __restrict__ acc, const 
         for (int e = 0; e < kKsEntries; ++e) {
           if ((u32)e >= ne) break;
           const u64 x = T.x[e][s_in[c]];
-          mac128_lazy(bh[e][c], bl[e][c], x, kb);
-          mac128_lazy(ah[e][c], al[e][c], x, ka);
+          if (f96) {
+            mac96(bh[e][c], bl[e][c], (u32)x, (u32)(x >> 32), (u32)kb, (u32)(kb >> 32));
+            mac96(ah[e][c], al[e][c], (u32)x, (u32)(x >> 32), (u32)ka, (u32)(ka >> 32));
+          } else {
+            mac128_lazy(bh[e][c], bl[e][c], x, kb);
+            mac128_lazy(ah[e][c], al[e][c], x, ka);
+          }
         }
       }
     } else {
@@ -1926,10 +1941,12 @@ __device__ __forceinline__ void ks_inner_tma2_body(u64* __restrict__ acc, const 
 #pragma unroll
         for (int e = 0; e < kKsEntries; ++e) {
           if ((u32)e >= ne) break;
-          mac128_lazy(bh[e][c], bl[e][c], T.x[e][s_in[c]], w);
+          const u64 x = T.x[e][s_in[c]];
+          if (f96) mac96(bh[e][c], bl[e][c], (u32)x, (u32)(x >> 32), (u32)w, (u32)(w >> 32));
+          else mac128_lazy(bh[e][c], bl[e][c], x, w);
         }
     }
-    if ((j + 1) % kLazyTerms == 0 || j + 1 == nst) {
+    if (!f96 && ((j + 1) % kLazyTerms == 0 || j + 1 == nst)) {
 #pragma unroll
       for (int e = 0; e < kKsEntries; ++e)
 #pragma unroll
@@ -1946,8 +1963,8 @@ __device__ __forceinline__ void ks_inner_tma2_body(u64* __restrict__ acc, const 
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const u32 kc = k + c * TPB;
-      A[(size_t)r * N + kc] = redc128(bh[e][c], bl[e][c], q, ninv);
-      A[((size_t)n_ext + r) * N + kc] = redc128(ah[e][c], al[e][c], q, ninv);
+      A[(size_t)r * N + kc] = f96 ? redc96(bh[e][c], bl[e][c], q, ninv) : redc128(bh[e][c], bl[e][c], q, ninv);
+      A[((size_t)n_ext + r) * N + kc] = f96 ? redc96(ah[e][c], al[e][c], q, ninv) : redc128(ah[e][c], al[e][c], q, ninv);
     }
   }
 }

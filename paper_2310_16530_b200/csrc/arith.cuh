@@ -29,6 +29,7 @@ cudaError_t launch_modup(const FbcDev* tabs, const FbcDev* htabs, u32 ndig, cons
 // g_ks_batch (1, 2 or 4) entries (hcnn_set_option "ks_batch")
 extern int g_ks_batch;
 extern int g_fbc_fork;
+cudaError_t set_ks96(int on);
 extern int g_ks_pipe;
 extern int g_ks_tma;
 extern int g_ks_tma_min;

@@ -1378,6 +1378,7 @@ int hcnn_set_option(const char* name, long long value) {
   else if (k == "ks_rots_min_nb") g_ks_rots_min_nb = (int)value;
   else if (k == "md_fuse") g_ntt_tuning.md_fuse = (int)value;
   else if (k == "fbc_fast") CK(set_fbc_fast((int)value));
+  else if (k == "ks96") CK(set_ks96((int)value));
   else if (k == "ks_batch") g_ks_batch = (int)value;
   else if (k == "ks_pipe") g_ks_pipe = (int)value;
   else if (k == "ks_tma") g_ks_tma = (int)value;

@@ -277,13 +277,14 @@ _KNOB_DEFAULTS = {"mac_tma": 3, "mac3_stages": 4, "mac3_tpb": 128, "mac3_fork": 
                   "mac_minb": 1,
                   "ks_tpb": 128, "ks_stages": 3, "ks_tma_min": 2, "ks_tma3": 0, "ks3_stages": 3, "md_fuse": 0,
                   "ntt_pipe": 1, "fbc_fast": 1, "ntt_fork": 1, "fbc_fork": 1,
-                  "ks_rots": 1, "ks_rots_min_nb": 1}
+                  "ks_rots": 1, "ks_rots_min_nb": 1, "ks96": 1}
 _KNOB_VARIANTS = [
     {"mac_tma": 1},
     {"ntt_fork": 0},
     {"fbc_fork": 0},
     {"ks_rots": 0},
     {"ks_rots_min_nb": 2},
+    {"ks96": 0},
     {"mac3_fork": 0},
     {"md_fuse": 1},
     {"ntt_pipe": 0},
