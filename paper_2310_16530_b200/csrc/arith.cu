@@ -603,6 +603,7 @@ __global__ void __launch_bounds__(256, JB >= 4 ? 2 : 3) k_ks_inner_p(
   const u32 n_ext = basis.nlimbs();
   const u32 mod = basis.mod_of(r);
   const u64 q = mc[mod].q, ninv = mc[mod].ninv, one_sh = mc[mod].one_sh;
+  const bool f96 = g_ks96_dev && q < (1ull << 42);  // 96-bit carry chains (see k_ks_inner_tma2)
   const u32 klq = key_lq ? key_lq : basis.Lq;
   const size_t key_dst = (size_t)(klq + basis.np) * N;
   const u32 kmod = mod < basis.Lq ? mod : klq + (mod - basis.Lq);
@@ -645,6 +646,17 @@ __global__ void __launch_bounds__(256, JB >= 4 ? 2 : 3) k_ks_inner_p(
         kap += key_dst;
         rp += rstep;
       }
+      if (f96) {
+#pragma unroll
+        for (int i = 0; i < JB; ++i) {
+          const u32 x0 = (u32)X[i].x, x1 = (u32)(X[i].x >> 32), y0 = (u32)X[i].y, y1 = (u32)(X[i].y >> 32);
+          mac96(bh0, bl0, x0, x1, (u32)KB[i].x, (u32)(KB[i].x >> 32));
+          mac96(ah0, al0, x0, x1, (u32)KA[i].x, (u32)(KA[i].x >> 32));
+          mac96(bh1, bl1, y0, y1, (u32)KB[i].y, (u32)(KB[i].y >> 32));
+          mac96(ah1, al1, y0, y1, (u32)KA[i].y, (u32)(KA[i].y >> 32));
+        }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < JB; ++i) {
         mac128_lazy(bh0, bl0, X[i].x, KB[i].x);
@@ -662,8 +674,22 @@ __global__ void __launch_bounds__(256, JB >= 4 ? 2 : 3) k_ks_inner_p(
     if (c0 && r < basis.nq) {  // extended-basis output: + P * sigma_g(c0) on the Q limbs
       const u64 w = pR[r];
       const u64* src = c0 + (size_t)b * c0_bst + (size_t)r * N;
-      mac128_lazy(bh0, bl0, src[p0], w);
-      mac128_lazy(bh1, bl1, src[p1], w);
+      const u64 s0 = src[p0], s1 = src[p1];
+      if (f96) {
+        mac96(bh0, bl0, (u32)s0, (u32)(s0 >> 32), (u32)w, (u32)(w >> 32));
+        mac96(bh1, bl1, (u32)s1, (u32)(s1 >> 32), (u32)w, (u32)(w >> 32));
+      } else {
+        mac128_lazy(bh0, bl0, s0, w);
+        mac128_lazy(bh1, bl1, s1, w);
+      }
+    }
+    if (f96) {
+      u64* A = acc + (size_t)b * 2 * n_ext * N;
+      *reinterpret_cast<ulonglong2*>(A + (size_t)r * N + k) =
+          make_ulonglong2(redc96(bh0, bl0, q, ninv), redc96(bh1, bl1, q, ninv));
+      *reinterpret_cast<ulonglong2*>(A + ((size_t)n_ext + r) * N + k) =
+          make_ulonglong2(redc96(ah0, al0, q, ninv), redc96(ah1, al1, q, ninv));
+      continue;
     }
     bh0 = fold_hi(bh0, q, one_sh);
     bh1 = fold_hi(bh1, q, one_sh);
