@@ -869,6 +869,8 @@ __global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __re
   const u32 x0 = NB == 1 ? blockIdx.x / nb : blockIdx.x, xs = NB == 1 ? gridDim.x / nb : gridDim.x;
   const u32 mod = r < nq ? r : Lq + (r - nq);
   const u64 q = mc[mod].q, ninv = mc[mod].ninv, one_sh = mc[mod].one_sh;
+  // rows with q < 2^42: 96-bit carry chains (see k_ks_inner_tma2; nt <= 48 keeps T < 2^90)
+  const bool f96 = g_ks96_dev && q < (1ull << 42) && nt <= 48;
   const size_t bst = 2 * (size_t)nl * N, pst = (size_t)nl * N;
   const size_t off = (size_t)r * N + (size_t)b0 * bst, moff = (size_t)r * N;
   for (u32 kv = x0 * blockDim.x + threadIdx.x; kv < N / VEC; kv += xs * blockDim.x) {
@@ -905,10 +907,13 @@ __global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __re
             x[0] = *src;
           }
 #pragma unroll
-          for (int v = 0; v < VEC; ++v) mac128_lazy(hi[e][p][v], lo[e][p][v], x[v], m[v]);
+          for (int v = 0; v < VEC; ++v) {
+            if (f96) mac96(hi[e][p][v], lo[e][p][v], (u32)x[v], (u32)(x[v] >> 32), (u32)m[v], (u32)(m[v] >> 32));
+            else mac128_lazy(hi[e][p][v], lo[e][p][v], x[v], m[v]);
+          }
         }
       }
-      if ((t + 1) % kLazyTerms == 0 || t + 1 == nt) {
+      if (!f96 && ((t + 1) % kLazyTerms == 0 || t + 1 == nt)) {
 #pragma unroll
         for (int e = 0; e < NB; ++e)
 #pragma unroll
@@ -925,7 +930,8 @@ __global__ void __launch_bounds__(256) k_mac_terms(MacTerms T, int nt, u64* __re
         u64* dst = out + off + e * bst + p * pst + k;
         u64 y[VEC];
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) y[v] = redc128(hi[e][p][v], lo[e][p][v], q, ninv);
+        for (int v = 0; v < VEC; ++v)
+          y[v] = f96 ? redc96(hi[e][p][v], lo[e][p][v], q, ninv) : redc128(hi[e][p][v], lo[e][p][v], q, ninv);
         if (VEC == 2) {
           if (accumulate) {
             const ulonglong2 o = *reinterpret_cast<const ulonglong2*>(dst);
