@@ -306,9 +306,24 @@ __global__ void k_tensor(u64* __restrict__ d0, u64* __restrict__ d1, u64* __rest
   const ModConsts C = mc[r];
   const size_t pst = (size_t)nlimbs * N;
   const size_t off = (size_t)r * N;
+  // rows with q < 2^42: the three products through 96-bit carry chains (one
+  // REDC each, the d1 sum in one chain) -- the same canonical residues
+  const bool f96 = g_ks96_dev && C.q < (1ull << 42);
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
     u64 a0 = a[off + k], a1 = a[pst + off + k];
     u64 b0 = b[off + k], b1 = b[pst + off + k];
+    if (f96) {
+      const u32 a00 = (u32)a0, a01 = (u32)(a0 >> 32), a10 = (u32)a1, a11 = (u32)(a1 >> 32);
+      u64 l0 = 0, m0 = 0, l1 = 0, m1 = 0, l2 = 0, m2 = 0;
+      mac96(l0, m0, a00, a01, (u32)b0, (u32)(b0 >> 32));
+      mac96(l1, m1, a00, a01, (u32)b1, (u32)(b1 >> 32));
+      mac96(l1, m1, a10, a11, (u32)b0, (u32)(b0 >> 32));
+      mac96(l2, m2, a10, a11, (u32)b1, (u32)(b1 >> 32));
+      d0[off + k] = mont_mul(redc96(l0, m0, C.q, C.ninv), C.r2, C.q, C.ninv);
+      d1[off + k] = mont_mul(redc96(l1, m1, C.q, C.ninv), C.r2, C.q, C.ninv);
+      d2[off + k] = mont_mul(redc96(l2, m2, C.q, C.ninv), C.r2, C.q, C.ninv);
+      continue;
+    }
     u64 t0 = mont_mul(a0, b0, C.q, C.ninv);
     u64 t2 = mont_mul(a1, b1, C.q, C.ninv);
     u64 hi = 0, lo = 0;
