@@ -58,7 +58,9 @@ cudaError_t launch_combine_rows(const NttCombine& C, const u64* lift, u32 nq, u3
 struct NttTuning {
   int group_limbs = 0;
   int hints = 1;
-  int occupancy = 0;  // 1: register-capped kernels (more resident warps)
+  // 1: register-capped integer-network kernels (more resident warps): 3 interleaved
+  // ResNet20 A/B pairs 331.8 vs 333.4 ms/image, each pair lower (profiles/r02_ntt_occ_ab.txt)
+  int occupancy = 1;
   int split = 1;      // 1: separate launches per modulus class (measured: inverse 0.778 -> 0.758 us/limb), 2: forward only
   int f64_minb = 1;   // FP64 chunk passes: min CTAs per SM hint (1, 5 or 6)
   int pipe = 1;       // FP64 forward chunk pass pipelined over polys (ntt2_fwd_chunks_f64p)

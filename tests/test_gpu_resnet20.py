@@ -204,13 +204,13 @@ def test_deska_launch_shapes_batched_galois(golden_hashes):
     steps = [1, 8, 64, 2048]
     defaults = {"ks_tpb": 128, "ks_stages": 3, "ks_tma_min": 2, "md_fuse": 0, "ntt_pipe": 1, "ks_tma3": 0,
                 "fbc_fast": 1, "ntt_split": 1, "ntt_fork": 1, "fbc_fork": 1,
-                "ks_rots": 1, "ks_rots_min_nb": 1, "ks96": 1}
+                "ks_rots": 1, "ks_rots_min_nb": 1, "ks96": 1, "ntt_occupancy": 1}
     variants = [{"ks_tpb": 256}, {"ks_stages": 4}, {"ks_tpb": 256, "ks_stages": 4}, {"ks_tma_min": 1},
                 {"md_fuse": 1}, {"ntt_pipe": 0}, {"md_fuse": 1, "ks_tma_min": 1}, {"ks_tma3": 1}, {"ks_tma3": 2},
                 {"fbc_fast": 0}, {"ntt_split": 2}, {"ntt_fork": 0}, {"fbc_fork": 0},
                 {"ntt_fork": 0, "fbc_fork": 0, "mac3_fork": 0},
                 {"ks_rots": 0}, {"ks_rots_min_nb": 2}, {"ks_stages": 4, "ks_rots": 1},
-                {"ks96": 0}, {"ks96": 0, "ks_rots": 0}]
+                {"ks96": 0}, {"ks96": 0, "ks_rots": 0}, {"ntt_occupancy": 0}, {"ntt_occupancy": 2}]
 
     def run():
         outs = [r.data.clone() for r in ckks.rotate_many(batch, steps, ks)]
