@@ -985,31 +985,36 @@ int hcnn_rotate_hoisted_batch(hcnn_ctx* c, uint64_t* const* outs, const uint64_t
     ComboSteps S;
     // the chunk's inner products: one launch for all its rotations when
     // ks_rots_ok (raised digits read from HBM once per chunk), else one each
-    const bool rots = nr <= (u32)kKsRotMax && ks_rots_ok(nb, nr, c->logN);
-    KsRots R{};
-    for (u32 j = 0; j < nr; ++j) {
-      const u32 i = i0 + j;
-      const u64 g = galois[i] % (2ull * c->n);
-      S.out[j] = outs[i];
-      S.g[j] = g;
-      ks_acc(0, nb);
-      ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * nq) * N);
-      if (rots) {
-        R.acc[j] = w.acc + j * a_step;
-        R.kb[j] = kbs[i];
-        R.ka[j] = kas[i];
-        R.g[j] = g;
-        R.klq[j] = key_lqs ? key_lqs[i] : 0;
-        continue;
+    // (sub-groups of up to kKsRotMax rotations per launch)
+    const bool rots = ks_rots_ok(nb, nr, c->logN);
+    for (u32 j0 = 0; j0 < nr; j0 += (u32)kKsRotMax) {
+      const u32 nj = nr - j0 < (u32)kKsRotMax ? nr - j0 : (u32)kKsRotMax;
+      KsRots R{};
+      for (u32 jj = 0; jj < nj; ++jj) {
+        const u32 j = j0 + jj, i = i0 + j;
+        const u64 g = galois[i] % (2ull * c->n);
+        S.out[j] = outs[i];
+        S.g[j] = g;
+        ks_acc(0, nb);
+        ks_acc(1, 8.0 * (2.0 * nd * n_ext + 2.0 * nb * nq) * N);
+        if (rots && nj >= 2) {
+          R.acc[jj] = w.acc + j * a_step;
+          R.kb[jj] = kbs[i];
+          R.ka[jj] = kas[i];
+          R.g[jj] = g;
+          R.klq[jj] = key_lqs ? key_lqs[i] : 0;
+          continue;
+        }
+        PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
+           launch_ks_inner(w.acc + j * a_step, c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd,
+                           c->logN, g, c->d_mc, STREAM(s), nb, ct, nullptr, 0, nullptr, key_lqs ? key_lqs[i] : 0,
+                           ks_fast_from(c, nq)));
       }
-      PK("ks_inner", 8.0 * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
-         launch_ks_inner(w.acc + j * a_step, c1, w.raised, kbs[i], kas[i], c->basis(nq, c->K), c->alpha, nd,
-                         c->logN, g, c->d_mc, STREAM(s), nb, ct, nullptr, 0, nullptr, key_lqs ? key_lqs[i] : 0, ks_fast_from(c, nq)));
+      if (rots && nj >= 2)
+        PK("ks_inner", 8.0 * nj * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
+           launch_ks_inner_rots(R, nj, c1, w.raised, c->basis(nq, c->K), c->alpha, nd, c->logN, c->d_mc,
+                                STREAM(s), nb, ct));
     }
-    if (rots)
-      PK("ks_inner", 8.0 * nr * ((double)nd * n_ext * (2 + nb) + 2.0 * nb * n_ext) * N, 1, STREAM(s),
-         launch_ks_inner_rots(R, nr, c1, w.raised, c->basis(nq, c->K), c->alpha, nd, c->logN, c->d_mc, STREAM(s),
-                              nb, ct));
     const u32 np = 2 * nb * nr;
     LimbMap m{};
     m.base = w.acc + nq * N;
