@@ -63,10 +63,16 @@ __device__ __forceinline__ void mac96(u64& lh, u64& mid, u32 a0, u32 a1, u32 m0,
       : "r"(a0), "r"(a1), "r"(m0), "r"(m1));
 }
 // T = lh + mid 2^32 (< 2^90) -> T R^-1 mod q
+// Signed Montgomery form of the reduction: with m = L2 q^-1 (q^-1 = -ninv mod
+// 2^64) the low word of m q equals L2, so (T - m q) / 2^64 = H - hi(m q)
+// exactly, in (-q, q) because H < q (T < 2^90) and hi(m q) < q: one
+// correction and no carry-in term -- fewer ALU operations than redc128's
+// H + hi + (L2 != 0) with its [0, 2q) result (the same canonical residue).
 __device__ __forceinline__ u64 redc96(u64 lh, u64 mid, u64 q, u64 ninv) {
   const u64 L2 = lh + (mid << 32);
   const u64 H = (mid >> 32) + (L2 < lh ? 1ull : 0ull);
-  return redc128(H, L2, q, ninv);
+  const u64 mh = __umul64hi(L2 * (0ull - ninv), q);
+  return H >= mh ? H - mh : H - mh + q;
 }
 
 // FBC: the 96-bit path for conversions whose sources and target are all below 2^42
